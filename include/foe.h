@@ -1,0 +1,220 @@
+/*
+ * foe.h -- C ABI of libfoe, the B200 (sm_100a) hot path of FoE-prior despeckling
+ * solved by iPiano (Chen, Pock et al., arXiv:1404.5344; PAPER.md = the paper text).
+ *
+ * The library solves the combined model, Eq.(10) ("From now on,
+ * we will use the combined model (10)"):
+ *
+ *     min_w  F(w) + G(w),
+ *     F(w) = E_FoE(e^w) = sum_i theta_i sum_p rho((k_i * e^w)_p),  rho(x) = log(1+x^2)
+ *                                                       (Eq.(2))
+ *     G(w) = sum_p (l1/2)(2 w_p + f_p^2 e^{-2 w_p}) + (l2/2)(e^{2 w_p} - 2 f_p^2 w_p)
+ *
+ * with u = e^w, by iPiano
+ *
+ *     w^{n+1} = (I + a dG)^{-1}( w^n - a grad F(w^n) + b (w^n - w^{n-1}) ),
+ *     grad_w F = W sum_i theta_i K_i^T rho'(K_i e^w), W = diag(e^w)
+ *
+ * the prox of G by Newton's method, and the backtracking
+ * Lipschitz test F(w+) <= F(w) + <grad F(w), w+ - w> + (L_n/2)||w+ - w||^2 with
+ * a = safety * 2(1-b)/L_n.  l2 = 0 is model (8).
+ * Readings where the paper is silent (periodic boundary, true convolution, f~ = max(f,1),
+ * the step policy, ...) are listed in DESIGN.md as R-1 .. R-17.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns foe_status; no C++ exception crosses the ABI.  On error,
+ *    foe_last_error() returns a thread-local message naming the offending argument.
+ *  - Images are contiguous row-major [B][H][W] arrays (B images of H rows by W columns).
+ *    "device" pointers are CUDA device memory on the model's device (e.g. a torch
+ *    tensor's data_ptr()); "host" pointers are ordinary (pageable or pinned) host memory.
+ *  - The caller owns every array it passes; the model and state own their internal
+ *    device memory and free it in *_destroy.  Inputs are never modified.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
+ *    Calls are asynchronous on that stream unless they return host values, in which
+ *    case they synchronise it before returning.
+ *  - There is no CPU fallback: without a usable sm_100a device every call that needs
+ *    one fails with FOE_ERR_CUDA.
+ */
+#ifndef FOE_H_
+#define FOE_H_
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FOE_OK = 0,
+    FOE_ERR_INVALID_ARGUMENT = 1,    /* bad size/pointer/parameter (message names it)          */
+    FOE_ERR_CUDA = 2,                /* CUDA runtime error, or no sm_100 device                 */
+    FOE_ERR_OUT_OF_MEMORY = 3,
+    FOE_ERR_NONFINITE = 4,           /* accepted energy/iterate non-finite        */
+    FOE_ERR_BACKTRACK_LIMIT = 5,     /* more than max_backtracks doublings        */
+    FOE_ERR_PROX_NO_CONVERGENCE = 6, /* Newton cap exceeded in the prox           */
+    FOE_ERR_DOMAIN = 7,              /* accepted |w| above the guard (R-11)           */
+    FOE_ERR_COMM = 8,                /* multi-GPU communication error                           */
+    FOE_ERR_UNSUPPORTED = 9          /* valid request this build does not implement             */
+} foe_status;
+
+typedef enum {
+    FOE_DATA_COMBINED = 0, /* Eq.(10): l1, l2 as given                                         */
+    FOE_DATA_NAKAGAMI = 1  /* Eq.(8): l2 forced to 0, l1 = lambda            */
+} foe_data_term;
+
+/* Limits of this build (kernel-parameter-resident filter taps). */
+#define FOE_MAX_FILTERS 64
+#define FOE_MAX_TAPS 3136  /* n_filters * m * m */
+
+const char* foe_last_error(void);
+const char* foe_status_string(foe_status s);
+/* Library version string, and the compiled target (e.g. "sm_100a"). */
+const char* foe_version(void);
+
+/* ------------------------------------------------------------------------------ model */
+
+typedef struct foe_model foe_model;
+
+/* Creates the FoE model {(k_i, theta_i)} of Eq.(2) plus the data-term weights of Eq.(10).
+ *   filters  host fp32 [n_filters][m][m] row-major taps k_i
+ *   m        odd filter side, 3 <= m <= 9 supported kernels: m in {3, 5, 7} (FOE_ERR_UNSUPPORTED otherwise)
+ *   alphas   host fp32 [n_filters], the weights theta_i > 0 ("alphas" in BASELINE.json)
+ *   lambda   host fp64 [2] = {l1, l2} (Eq.(10)), both >= 0 and not both 0; NULL -> the
+ *            paper's preset for looks_L (L=8 (550,0.02), L=3 (310,0.008),
+ *            L=1 (160,0.004); L=5 (50,0.15))
+ *   looks_L  number of looks L; required (1, 3, 5 or 8) iff lambda == NULL, else informational
+ *            (L is folded into lambda, R-5)
+ *   term     FOE_DATA_COMBINED or FOE_DATA_NAKAGAMI
+ *   cuda_device  CUDA ordinal the model's kernels run on
+ * Errors: FOE_ERR_INVALID_ARGUMENT (m even/< 3, n_filters < 1 or > FOE_MAX_FILTERS,
+ * n_filters*m*m > FOE_MAX_TAPS, theta_i <= 0 or non-finite (message names filter i),
+ * non-finite taps, bad lambda/looks), FOE_ERR_CUDA (device unusable or not sm_100).
+ * The model is immutable after creation and may be shared read-only between threads. */
+foe_status foe_model_create(const float* filters, int n_filters, int m, const float* alphas,
+                            const double* lambda, double looks_L, foe_data_term term,
+                            int cuda_device, foe_model** out);
+void foe_model_destroy(foe_model* model);
+
+/* ------------------------------------------------------------------ energy / gradient */
+
+/* Energy and prior gradient at the log-amplitude w:
+ *   w                device fp64 [B][H][W]
+ *   f                device fp32 [B][H][W] observation; used only for data_energy (may be NULL
+ *                    if data_energy is NULL); f~ = max(f,1) is applied internally (R-4)
+ *   lambda_per_image host fp64 [B][2] or NULL (-> the model's {l1,l2})
+ *   prior_energy     host fp64 [B] or NULL: F(w) = E_FoE(e^w)
+ *   data_energy      host fp64 [B] or NULL: G(w) of Eq.(10)
+ *   grad             device fp32 [B][H][W] or NULL: grad_w F
+ * Requires m <= min(H, W).  Periodic boundary (R-3).  Synchronises `stream`
+ * when a host output is requested. */
+foe_status foe_energy_grad(const foe_model* model, const double* w, const float* f, int B, int H,
+                           int W, const double* lambda_per_image, double* prior_energy,
+                           double* data_energy, float* grad, void* stream);
+
+/* Hessian-vector product of F at w (R-10), device fp64 w, v -> device fp32 hv. */
+foe_status foe_hvp(const foe_model* model, const double* w, const double* v, int B, int H, int W,
+                   float* hv, void* stream);
+
+/* Lipschitz initialisation (R-10): rho_hat = |Rayleigh quotient| after
+ * `power_iters` power-iteration steps on the prior Hessian at w^0 = log max(f,1), from
+ * the caller's start vectors v0 (device fp64 [B][H][W], any scale; the method's random
+ * draw is an input).  rho_out (host [B], may be NULL) and L_out (host [B]) =
+ * 2^ceil(log2 rho_hat).  Synchronises `stream`. */
+foe_status foe_estimate_lipschitz(const foe_model* model, const float* f, int B, int H, int W,
+                                  const double* v0, int power_iters, double* rho_out,
+                                  double* L_out, void* stream);
+
+/* ---------------------------------------------------------------------------- iPiano */
+
+typedef struct {
+    double beta;             /* inertia b in [0,1); graded policy 0.4 (R-9); SPEC default 0.8      */
+    double step_safety;      /* a = step_safety * 2(1-b)/L_n, in (0,1]; 0.95          */
+    double backtrack_factor; /* eta > 1: L_n <- eta L_n on a failed test; 2           */
+    double shrink;           /* L_{n+1} = shrink * L_n after an accept, in (0,1]; 1 (R-9), SPEC 0.5  */
+    int max_iters;           /* accepted iterations, >= 1                                            */
+    int max_backtracks;      /* failed tests per iteration before FOE_ERR_BACKTRACK_LIMIT; 60       */
+    int newton_max_iters;    /* Newton cap of the prox before FOE_ERR_PROX_NO_CONVERGENCE; 30       */
+    double newton_tol;       /* |phi| tolerance of the prox root (fp64); 1e-12        */
+    double rel_change_tol;   /* stop when ||w+ - w|| / max(||w||,1) < tol; 0 = never (benchmarks)    */
+    double w_guard;          /* accepted |w| must stay <= w_guard; 40 (R-11)                          */
+    int record_trace;        /* 1: keep the per-iteration trace on device                             */
+    int filter_groups;       /* 0 = automatic; else split the N_f filters over this many CTAs
+                                per tile (partial gradients summed in fixed order)                    */
+} ipiano_config;
+
+/* Fills the defaults above (graded policy). */
+void ipiano_config_default(ipiano_config* cfg);
+
+/* Trace record per accepted iteration n (row 0 = the initial point w^0), fp64. */
+typedef struct {
+    double F;       /* F(w^n)                                             */
+    double G;       /* G(w^n)                                             */
+    double H;       /* F + G                                              */
+    double L;       /* L_n used by the accepted trial                     */
+    double trials;  /* trials of iteration n (1 = accepted at once)       */
+    double margin;  /* F(w) + <g,D> + L/2 ||D||^2 - F(w+) >= 0             */
+    double newton;  /* max Newton iterations of the accepted prox         */
+    double relchg;  /* ||w^n - w^{n-1}|| / max(||w^{n-1}||, 1)           */
+} ipiano_trace_rec;
+
+typedef struct ipiano_state ipiano_state;
+
+/* Allocates and initialises a batch of B independent problems (one per image):
+ *   f                 device fp32 [B][H][W] observations (copied into the state; f~ = max(f,1))
+ *   lambda_per_image  host fp64 [B][2] or NULL (-> model's)
+ *   lipschitz_init    host fp64 [B], each > 0 (from foe_estimate_lipschitz, or the caller's)
+ *   cfg               NULL -> defaults
+ * Sets w^0 = log f~, w^{-1} = w^0 (R-8), evaluates F(w^0) and grad F(w^0) on `stream`.
+ * Errors: FOE_ERR_INVALID_ARGUMENT (B < 1, H or W < m, bad cfg: beta outside [0,1),
+ * max_iters < 1, step_safety outside (0,1], backtrack_factor <= 1, shrink outside (0,1]). */
+foe_status ipiano_state_create(const foe_model* model, const float* f, int B, int H, int W,
+                               const double* lambda_per_image, const double* lipschitz_init,
+                               const ipiano_config* cfg, void* stream, ipiano_state** out);
+
+/* Advances every unfinished image by exactly one accepted iPiano iteration (as many
+ * backtracking trials as it needs), then synchronises.  accepted_iters_out (host [B] or
+ * NULL) receives each image's accepted-iteration count.  Returns the first per-image
+ * error status if any image failed. */
+foe_status ipiano_step(ipiano_state* st, void* stream, int* accepted_iters_out);
+
+/* Runs until every image has max_iters accepted iterations (or stopped on
+ * rel_change_tol, or failed).  Trial rounds are launched asynchronously in chunks (as a
+ * CUDA graph) with one synchronisation per chunk. */
+foe_status ipiano_solve(ipiano_state* st, void* stream);
+
+/* Copies the current iterate out: w_out device fp64 [B][H][W] and/or u_out device fp32
+ * [B][H][W] = e^w ("with u = e^w"); either may be NULL. */
+foe_status ipiano_get_iterate(const ipiano_state* st, double* w_out, float* u_out, void* stream);
+
+/* Per-image counters (host arrays [B], each may be NULL): accepted iterations, total
+ * trials, status (foe_status per image), current L_n.  Synchronises the state's stream. */
+foe_status ipiano_get_counters(const ipiano_state* st, int* iters, int* trials, int* status,
+                               double* lipschitz);
+
+/* Copies the trace to host: [B][max_iters+1] ipiano_trace_rec (bytes must be at least
+ * B*(max_iters+1)*sizeof(ipiano_trace_rec)); rows past an image's iteration count are 0. */
+foe_status ipiano_get_trace(const ipiano_state* st, void* host_trace, size_t bytes);
+
+/* Device time (ms) spent in the fused prior-gradient kernel since the last call, and the
+ * number of its launches; enabled by ipiano_profile(st, 1) (CUDA events around each launch). */
+foe_status ipiano_profile(ipiano_state* st, int enable);
+foe_status ipiano_profile_read(ipiano_state* st, double* k1_ms, long long* k1_launches,
+                               long long* total_launches);
+
+void ipiano_state_destroy(ipiano_state* st);
+
+/* One-shot convenience: state_create + solve + get_iterate + get_trace + destroy.
+ *   f      fp32 [B][H][W], host OR device (detected); host buffers are copied in/out on
+ *          `stream` inside the call
+ *   u_out  fp32 [B][H][W] = e^w, host or device
+ *   trace  host, may be NULL (then trace_bytes is ignored)
+ * Synchronises `stream`. */
+foe_status ipiano_run(const foe_model* model, const float* f, int B, int H, int W,
+                      const double* lambda_per_image, const double* lipschitz_init,
+                      const ipiano_config* cfg, float* u_out, void* trace, size_t trace_bytes,
+                      void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FOE_H_ */

@@ -1,0 +1,918 @@
+// foe_api.cu -- C ABI of libfoe (include/foe.h): model, energy/gradient, Lipschitz
+// estimate and the device-controlled iPiano solver loop.  Host code only orchestrates
+// launches of the kernels in foe_kernels.cuh; every step of the method runs on the GPU.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "foe.h"
+#include "foe_kernels.cuh"
+
+using foe::ImgCtl;
+using foe::K1Args;
+using foe::kThreads;
+using foe::kTile;
+using foe::TapParams;
+
+namespace {
+
+thread_local std::string g_err;
+
+foe_status fail(foe_status s, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+foe_status cuda_fail(cudaError_t e, const char* what, int line) {
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? FOE_ERR_OUT_OF_MEMORY : FOE_ERR_CUDA,
+                "%s failed: %s (foe_api.cu:%d)", what, cudaGetErrorString(e), line);
+}
+
+#define CK(call)                                                        \
+    do {                                                                \
+        cudaError_t e_ = (call);                                        \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call, __LINE__);   \
+    } while (0)
+#define CKL(what)                                                       \
+    do {                                                                \
+        cudaError_t e_ = cudaGetLastError();                            \
+        if (e_ != cudaSuccess) return cuda_fail(e_, what, __LINE__);    \
+    } while (0)
+
+// Kernel configuration per filter size: NC filters per shared-memory chunk, SF forward
+// rows per thread item (K1), SFH for the HVP variant.
+template <int M> struct Tr;
+template <> struct Tr<7> { static constexpr int NC = 4, SF = 7, SFH = 5; };
+template <> struct Tr<5> { static constexpr int NC = 4, SF = 4, SFH = 4; };
+template <> struct Tr<3> { static constexpr int NC = 4, SF = 6, SFH = 6; };
+
+template <int M, bool HVP>
+constexpr int smem_bytes() {
+    using G = foe::K1Geom<M, Tr<M>::NC, HVP ? Tr<M>::SFH : Tr<M>::SF>;
+    return (HVP ? G::SMEM_FLOATS_HVP : G::SMEM_FLOATS) * 4;
+}
+
+template <int M, bool HVP>
+cudaError_t k1_set_attr() {
+    constexpr int SF = HVP ? Tr<M>::SFH : Tr<M>::SF;
+    return cudaFuncSetAttribute(foe::k_prior_grad<M, Tr<M>::NC, SF, HVP>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes<M, HVP>());
+}
+
+template <int M, bool HVP>
+void k1_launch(const K1Args& a, const TapParams& tp, dim3 grid, cudaStream_t s) {
+    constexpr int SF = HVP ? Tr<M>::SFH : Tr<M>::SF;
+    foe::k_prior_grad<M, Tr<M>::NC, SF, HVP><<<grid, kThreads, smem_bytes<M, HVP>(), s>>>(a, tp);
+}
+
+void k1_dispatch(int m, bool hvp, const K1Args& a, const TapParams& tp, dim3 grid, cudaStream_t s) {
+    switch (m) {
+        case 7: hvp ? k1_launch<7, true>(a, tp, grid, s) : k1_launch<7, false>(a, tp, grid, s); break;
+        case 5: hvp ? k1_launch<5, true>(a, tp, grid, s) : k1_launch<5, false>(a, tp, grid, s); break;
+        default: hvp ? k1_launch<3, true>(a, tp, grid, s) : k1_launch<3, false>(a, tp, grid, s); break;
+    }
+}
+
+constexpr int kPxt2 = 8;  // pixels per thread of the pointwise kernels
+
+int div_up(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace
+
+// ------------------------------------------------------------------------------- model
+
+struct foe_model {
+    int dev = 0, nf = 0, m = 0, nsm = 148;
+    foe_data_term term = FOE_DATA_COMBINED;
+    double lam[2] = {0, 0};
+    TapParams* tp = nullptr;  // host copy, passed by value to K1 launches
+};
+
+struct ipiano_state {
+    const foe_model* model = nullptr;
+    int B = 0, H = 0, W = 0;
+    size_t HW = 0;
+    ipiano_config cfg{};
+    foe::SolverParams sp{};
+    int tiles_x = 0, ntiles = 0, groups = 1, nchunks = 0, nblk2 = 0;
+    double* w = nullptr;      // [3][B][HW]
+    float* g = nullptr;       // [2][groups][B][HW]
+    float* ft = nullptr;      // [B][HW]
+    double* epart = nullptr;  // [B][ntiles*groups]
+    double* ppart = nullptr;  // [B][nblk2][8]
+    double* trace = nullptr;  // [B][max_iters+1][8]
+    ImgCtl* ctl = nullptr;
+    ImgCtl* hctl = nullptr;   // pinned mirror
+    cudaStream_t s = nullptr;
+    cudaEvent_t sync_ev = nullptr;
+    cudaGraphExec_t graph = nullptr;
+    int graph_rounds = 0;
+    bool profile = false;
+    std::vector<cudaEvent_t> ev_pool;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_live;
+    double k1_ms = 0.0;
+    long long k1_launches = 0, total_launches = 0;
+};
+
+extern "C" {
+
+const char* foe_last_error(void) { return g_err.c_str(); }
+
+const char* foe_status_string(foe_status s) {
+    switch (s) {
+        case FOE_OK: return "FOE_OK";
+        case FOE_ERR_INVALID_ARGUMENT: return "FOE_ERR_INVALID_ARGUMENT";
+        case FOE_ERR_CUDA: return "FOE_ERR_CUDA";
+        case FOE_ERR_OUT_OF_MEMORY: return "FOE_ERR_OUT_OF_MEMORY";
+        case FOE_ERR_NONFINITE: return "FOE_ERR_NONFINITE";
+        case FOE_ERR_BACKTRACK_LIMIT: return "FOE_ERR_BACKTRACK_LIMIT";
+        case FOE_ERR_PROX_NO_CONVERGENCE: return "FOE_ERR_PROX_NO_CONVERGENCE";
+        case FOE_ERR_DOMAIN: return "FOE_ERR_DOMAIN";
+        case FOE_ERR_COMM: return "FOE_ERR_COMM";
+        case FOE_ERR_UNSUPPORTED: return "FOE_ERR_UNSUPPORTED";
+    }
+    return "FOE_ERR_UNKNOWN";
+}
+
+const char* foe_version(void) { return "libfoe 0.1.0 sm_100a"; }
+
+foe_status foe_model_create(const float* filters, int n_filters, int m, const float* alphas,
+                            const double* lambda, double looks_L, foe_data_term term,
+                            int cuda_device, foe_model** out) {
+    if (!out) return fail(FOE_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (!filters) return fail(FOE_ERR_INVALID_ARGUMENT, "filters is NULL");
+    if (!alphas) return fail(FOE_ERR_INVALID_ARGUMENT, "alphas is NULL");
+    if (m < 3 || m % 2 == 0) return fail(FOE_ERR_INVALID_ARGUMENT, "filter side m=%d must be odd and >= 3", m);
+    if (m != 3 && m != 5 && m != 7) return fail(FOE_ERR_UNSUPPORTED, "filter side m=%d: this build has kernels for m in {3,5,7}", m);
+    if (n_filters < 1 || n_filters > foe::kMaxFilters)
+        return fail(FOE_ERR_INVALID_ARGUMENT, "n_filters=%d outside [1,%d]", n_filters, foe::kMaxFilters);
+    if ((long long)n_filters * m * m > foe::kMaxTaps)
+        return fail(FOE_ERR_INVALID_ARGUMENT, "n_filters*m*m=%d exceeds %d", n_filters * m * m, foe::kMaxTaps);
+    if (term != FOE_DATA_COMBINED && term != FOE_DATA_NAKAGAMI)
+        return fail(FOE_ERR_INVALID_ARGUMENT, "unknown data term %d", (int)term);
+    for (int i = 0; i < n_filters; ++i) {
+        if (!(alphas[i] > 0.0f) || !std::isfinite(alphas[i]))
+            return fail(FOE_ERR_INVALID_ARGUMENT, "non-positive weight at filter %d (theta=%g)", i, (double)alphas[i]);
+        for (int t = 0; t < m * m; ++t)
+            if (!std::isfinite(filters[i * m * m + t]))
+                return fail(FOE_ERR_INVALID_ARGUMENT, "non-finite tap at filter %d", i);
+    }
+    double lam[2];
+    if (lambda) {
+        lam[0] = lambda[0];
+        lam[1] = lambda[1];
+    } else {
+        // PAPER.md:272-274 (Sec. III-B) and :389 (Sec. III-C)
+        if (looks_L == 8) { lam[0] = 550; lam[1] = 0.02; }
+        else if (looks_L == 3) { lam[0] = 310; lam[1] = 0.008; }
+        else if (looks_L == 1) { lam[0] = 160; lam[1] = 0.004; }
+        else if (looks_L == 5) { lam[0] = 50; lam[1] = 0.15; }
+        else return fail(FOE_ERR_INVALID_ARGUMENT, "lambda is NULL and looks_L=%g has no preset (1,3,5,8)", looks_L);
+    }
+    if (term == FOE_DATA_NAKAGAMI) lam[1] = 0.0;
+    if (!(lam[0] >= 0) || !(lam[1] >= 0) || !std::isfinite(lam[0]) || !std::isfinite(lam[1]) ||
+        (lam[0] == 0 && lam[1] == 0))
+        return fail(FOE_ERR_INVALID_ARGUMENT, "lambda=(%g,%g) must be finite, >= 0 and not both 0", lam[0], lam[1]);
+
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (cuda_device < 0 || cuda_device >= ndev)
+        return fail(FOE_ERR_INVALID_ARGUMENT, "cuda_device=%d outside [0,%d)", cuda_device, ndev);
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, cuda_device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(FOE_ERR_CUDA, "libfoe is built for sm_100a (B200); device %d is sm_%d%d", cuda_device,
+                    prop.major, prop.minor);
+    CK(cudaSetDevice(cuda_device));
+    switch (m) {
+        case 7: CK((k1_set_attr<7, false>())); CK((k1_set_attr<7, true>())); break;
+        case 5: CK((k1_set_attr<5, false>())); CK((k1_set_attr<5, true>())); break;
+        default: CK((k1_set_attr<3, false>())); CK((k1_set_attr<3, true>())); break;
+    }
+
+    foe_model* md = new (std::nothrow) foe_model();
+    if (!md) return fail(FOE_ERR_OUT_OF_MEMORY, "host allocation");
+    md->tp = new (std::nothrow) TapParams();
+    if (!md->tp) { delete md; return fail(FOE_ERR_OUT_OF_MEMORY, "host allocation"); }
+    std::memset(md->tp, 0, sizeof(TapParams));
+    md->dev = cuda_device;
+    md->nf = n_filters;
+    md->m = m;
+    md->nsm = prop.multiProcessorCount;
+    md->term = term;
+    md->lam[0] = lam[0];
+    md->lam[1] = lam[1];
+    for (int i = 0; i < n_filters; ++i) {
+        const float* k = filters + (size_t)i * m * m;
+        double s = 0.0;
+        for (int a = 0; a < m; ++a)
+            for (int b = 0; b < m; ++b) {
+                // forward: K_i u (true convolution) = correlation with the flipped kernel
+                md->tp->fwd[i * m * m + a * m + b] = k[(m - 1 - a) * m + (m - 1 - b)];
+                // backward: theta_i K_i^T = correlation with theta_i k_i; x2 of rho'(x)=2x/(1+x^2)
+                md->tp->bwd[i * m * m + a * m + b] = (float)(2.0 * (double)alphas[i] * (double)k[a * m + b]);
+                s += (double)k[a * m + b];
+            }
+        md->tp->sumk[i] = (float)s;
+        md->tp->theta_ln2[i] = (double)alphas[i] * 0.69314718055994530942;
+    }
+    *out = md;
+    return FOE_OK;
+}
+
+void foe_model_destroy(foe_model* model) {
+    if (!model) return;
+    delete model->tp;
+    delete model;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------------ helpers
+
+namespace {
+
+// Choose the number of filter groups (split-N_f) so that a launch fills the machine.
+int choose_groups(const foe_model* md, int ntiles, int B, int requested) {
+    const int nchunks = div_up(md->nf, Tr<7>::NC);
+    if (requested > 0) return std::min(requested, nchunks);
+    const long long slots = 2LL * md->nsm;  // 2 CTAs / SM
+    double best = 1e30;
+    int bg = 1;
+    for (int g = 1; g <= nchunks; ++g) {
+        const long long ctas = (long long)ntiles * B * g;
+        const double waves = std::ceil((double)ctas / (double)slots);
+        const double per = std::ceil((double)nchunks / g) + 0.15;  // chunk work + staging/epilogue
+        const double cost = waves * per;
+        if (cost < best - 1e-9) { best = cost; bg = g; }
+    }
+    return bg;
+}
+
+foe_status check_dims(const foe_model* md, int B, int H, int W) {
+    if (!md) return fail(FOE_ERR_INVALID_ARGUMENT, "model is NULL");
+    if (B < 1) return fail(FOE_ERR_INVALID_ARGUMENT, "B=%d must be >= 1", B);
+    if (H < md->m || W < md->m)
+        return fail(FOE_ERR_INVALID_ARGUMENT, "image %dx%d smaller than the %dx%d filters (SPEC.md:92)", H, W,
+                    md->m, md->m);
+    if ((long long)B * H * W > (1LL << 40)) return fail(FOE_ERR_INVALID_ARGUMENT, "B*H*W too large");
+    return FOE_OK;
+}
+
+struct StreamJoin {  // run work on `inner` ordered after `outer`, and `outer` after the work
+    cudaStream_t outer, inner;
+    cudaEvent_t ev;
+};
+
+bool is_device_ptr(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// Evaluate K1 at device w[B][HW] (no control block); fills epart[B][ntiles*groups] and
+// the gradient planes gparts[groups][B][HW].
+foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int W, int groups,
+                        double* epart, float* gparts, bool hvp, const double* v, const float* gw,
+                        cudaStream_t s) {
+    K1Args a{};
+    a.w = w;
+    a.w_slot_stride = 0;
+    a.g = gparts;
+    a.g_slot_stride = 0;
+    a.g_group_stride = (size_t)B * H * W;
+    a.epart = epart;
+    a.ctl = nullptr;
+    a.which_cur = 1;
+    a.H = H;
+    a.W = W;
+    a.tiles_x = div_up(W, kTile);
+    a.ntiles = a.tiles_x * div_up(H, kTile);
+    a.groups = groups;
+    a.nf = md->nf;
+    a.nchunks = div_up(md->nf, Tr<7>::NC);
+    a.v = v;
+    a.gw = gw;
+    dim3 grid(a.ntiles * groups, B);
+    k1_dispatch(md->m, hvp, a, *md->tp, grid, s);
+    CKL("k_prior_grad launch");
+    return FOE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+foe_status foe_energy_grad(const foe_model* md, const double* w, const float* f, int B, int H, int W,
+                           const double* lambda_per_image, double* prior_energy, double* data_energy,
+                           float* grad, void* stream) {
+    foe_status st = check_dims(md, B, H, W);
+    if (st != FOE_OK) return st;
+    if (!w) return fail(FOE_ERR_INVALID_ARGUMENT, "w is NULL");
+    if (data_energy && !f) return fail(FOE_ERR_INVALID_ARGUMENT, "f is NULL but data_energy requested");
+    CK(cudaSetDevice(md->dev));
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t HW = (size_t)H * W;
+    const int tiles = div_up(W, kTile) * div_up(H, kTile);
+    const int groups = choose_groups(md, tiles, B, 0);
+    const int ne = tiles * groups;
+    double* epart = nullptr;
+    float* gparts = nullptr;
+    double* dred = nullptr;
+    double* dpart = nullptr;
+    double* dlam = nullptr;
+    const int nblk = div_up((long long)HW, (long long)kThreads * kPxt2);
+    CK(cudaMallocAsync((void**)&epart, sizeof(double) * B * ne, s));
+    const bool direct = (groups == 1 && grad != nullptr);
+    if (!direct) CK(cudaMallocAsync((void**)&gparts, sizeof(float) * groups * B * HW, s));
+    CK(cudaMallocAsync((void**)&dred, sizeof(double) * B * 2, s));
+    st = run_k1_plain(md, w, B, H, W, groups, epart, direct ? grad : gparts, false, nullptr, nullptr, s);
+    if (st != FOE_OK) return st;
+    if (grad && !direct) {
+        const size_t n = (size_t)B * HW;
+        foe::k_sum_groups<<<div_up((long long)n, 256), 256, 0, s>>>(gparts, n, groups, grad, n);
+        CKL("k_sum_groups");
+    }
+    foe::k_reduce_rows<<<B, kThreads, 0, s>>>(epart, ne, 1, 1, dred);
+    CKL("k_reduce_rows");
+    if (data_energy) {
+        std::vector<double> lam(2 * (size_t)B);
+        for (int b = 0; b < B; ++b) {
+            lam[2 * b] = lambda_per_image ? lambda_per_image[2 * b] : md->lam[0];
+            lam[2 * b + 1] = md->term == FOE_DATA_NAKAGAMI ? 0.0 : (lambda_per_image ? lambda_per_image[2 * b + 1] : md->lam[1]);
+        }
+        CK(cudaMallocAsync((void**)&dlam, sizeof(double) * 2 * B, s));
+        CK(cudaMallocAsync((void**)&dpart, sizeof(double) * B * nblk, s));
+        CK(cudaMemcpyAsync(dlam, lam.data(), sizeof(double) * 2 * B, cudaMemcpyHostToDevice, s));
+        foe::k_data_energy<<<dim3(nblk, B), kThreads, 0, s>>>(w, f, dlam, dpart, nblk, HW, kPxt2);
+        CKL("k_data_energy");
+        foe::k_reduce_rows<<<B, kThreads, 0, s>>>(dpart, nblk, 1, 1, dred + B);
+        CKL("k_reduce_rows");
+    }
+    std::vector<double> hred(2 * (size_t)B);
+    if (prior_energy || data_energy) {
+        CK(cudaMemcpyAsync(hred.data(), dred, sizeof(double) * 2 * B, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaFreeAsync(epart, s));
+    if (gparts) CK(cudaFreeAsync(gparts, s));
+    if (dpart) CK(cudaFreeAsync(dpart, s));
+    if (dlam) CK(cudaFreeAsync(dlam, s));
+    CK(cudaFreeAsync(dred, s));
+    if (prior_energy || data_energy) {
+        CK(cudaStreamSynchronize(s));
+        for (int b = 0; b < B; ++b) {
+            if (prior_energy) prior_energy[b] = hred[b];
+            if (data_energy) data_energy[b] = hred[B + b];
+        }
+    }
+    return FOE_OK;
+}
+
+foe_status foe_hvp(const foe_model* md, const double* w, const double* v, int B, int H, int W, float* hv,
+                   void* stream) {
+    foe_status st = check_dims(md, B, H, W);
+    if (st != FOE_OK) return st;
+    if (!w || !v || !hv) return fail(FOE_ERR_INVALID_ARGUMENT, "w, v and hv must be non-NULL");
+    CK(cudaSetDevice(md->dev));
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t n = (size_t)B * H * W;
+    const int tiles = div_up(W, kTile) * div_up(H, kTile);
+    double* epart = nullptr;
+    float* gw = nullptr;
+    CK(cudaMallocAsync((void**)&epart, sizeof(double) * B * tiles, s));
+    CK(cudaMallocAsync((void**)&gw, sizeof(float) * n, s));
+    st = run_k1_plain(md, w, B, H, W, 1, epart, gw, false, nullptr, nullptr, s);
+    if (st == FOE_OK) st = run_k1_plain(md, w, B, H, W, 1, epart, hv, true, v, gw, s);
+    CK(cudaFreeAsync(epart, s));
+    CK(cudaFreeAsync(gw, s));
+    return st;
+}
+
+foe_status foe_estimate_lipschitz(const foe_model* md, const float* f, int B, int H, int W, const double* v0,
+                                  int power_iters, double* rho_out, double* L_out, void* stream) {
+    foe_status st = check_dims(md, B, H, W);
+    if (st != FOE_OK) return st;
+    if (!f || !v0 || !L_out) return fail(FOE_ERR_INVALID_ARGUMENT, "f, v0 and L_out must be non-NULL");
+    if (power_iters < 1) return fail(FOE_ERR_INVALID_ARGUMENT, "power_iters=%d must be >= 1", power_iters);
+    CK(cudaSetDevice(md->dev));
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t HW = (size_t)H * W, n = (size_t)B * HW;
+    const int tiles = div_up(W, kTile) * div_up(H, kTile);
+    const int nblk = div_up((long long)HW, (long long)kThreads * kPxt2);
+    double *w0 = nullptr, *v = nullptr, *epart = nullptr, *part = nullptr, *sums = nullptr;
+    float *gw = nullptr, *h = nullptr;
+    CK(cudaMallocAsync((void**)&w0, sizeof(double) * n, s));
+    CK(cudaMallocAsync((void**)&v, sizeof(double) * n, s));
+    CK(cudaMallocAsync((void**)&gw, sizeof(float) * n, s));
+    CK(cudaMallocAsync((void**)&h, sizeof(float) * n, s));
+    CK(cudaMallocAsync((void**)&epart, sizeof(double) * B * tiles, s));
+    CK(cudaMallocAsync((void**)&part, sizeof(double) * B * nblk * 3, s));
+    CK(cudaMallocAsync((void**)&sums, sizeof(double) * B * 3, s));
+    const int eb = div_up((long long)n, 256);
+    foe::k_log_ftilde<<<eb, 256, 0, s>>>(f, w0, n);
+    CKL("k_log_ftilde");
+    // v <- v0 / ||v0||
+    foe::k_dot3<<<dim3(nblk, B), kThreads, 0, s>>>(v0, nullptr, part, nblk, HW, kPxt2);
+    foe::k_reduce_rows<<<B, kThreads, 0, s>>>(part, nblk, 3, 3, sums);
+    foe::k_normalize<double><<<eb, 256, 0, s>>>(v0, v, sums, 3, 2, HW, B);
+    CKL("power-iteration init");
+    st = run_k1_plain(md, w0, B, H, W, 1, epart, gw, false, nullptr, nullptr, s);
+    for (int it = 0; it < power_iters && st == FOE_OK; ++it) {
+        st = run_k1_plain(md, w0, B, H, W, 1, epart, h, true, v, gw, s);   // h = Hess v
+        foe::k_dot3<<<dim3(nblk, B), kThreads, 0, s>>>(v, h, part, nblk, HW, kPxt2);
+        foe::k_reduce_rows<<<B, kThreads, 0, s>>>(part, nblk, 3, 3, sums);  // <v,h>, <h,h>
+        foe::k_normalize<float><<<eb, 256, 0, s>>>(h, v, sums, 3, 1, HW, B);
+        CKL("power iteration");
+    }
+    std::vector<double> hs(3 * (size_t)B);
+    CK(cudaMemcpyAsync(hs.data(), sums, sizeof(double) * 3 * B, cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(w0, s)); CK(cudaFreeAsync(v, s)); CK(cudaFreeAsync(gw, s)); CK(cudaFreeAsync(h, s));
+    CK(cudaFreeAsync(epart, s)); CK(cudaFreeAsync(part, s)); CK(cudaFreeAsync(sums, s));
+    CK(cudaStreamSynchronize(s));
+    if (st != FOE_OK) return st;
+    for (int b = 0; b < B; ++b) {
+        const double rho = std::fabs(hs[3 * b]);
+        if (!(rho > 0) || !std::isfinite(rho))
+            return fail(FOE_ERR_NONFINITE, "Lipschitz estimate of image %d is %g", b, rho);
+        if (rho_out) rho_out[b] = rho;
+        L_out[b] = std::ldexp(1.0, (int)std::ceil(std::log2(rho)));
+    }
+    return FOE_OK;
+}
+
+void ipiano_config_default(ipiano_config* c) {
+    if (!c) return;
+    c->beta = 0.4;
+    c->step_safety = 0.95;
+    c->backtrack_factor = 2.0;
+    c->shrink = 1.0;
+    c->max_iters = 300;
+    c->max_backtracks = 60;
+    c->newton_max_iters = 30;
+    c->newton_tol = 1e-12;
+    c->rel_change_tol = 0.0;
+    c->w_guard = 40.0;
+    c->record_trace = 1;
+    c->filter_groups = 0;
+}
+
+}  // extern "C"
+
+// --------------------------------------------------------------------------- solver
+
+namespace {
+
+foe_status join_begin(ipiano_state* st, cudaStream_t user) {
+    CK(cudaEventRecord(st->sync_ev, user));
+    CK(cudaStreamWaitEvent(st->s, st->sync_ev, 0));
+    return FOE_OK;
+}
+foe_status join_end(ipiano_state* st, cudaStream_t user) {
+    CK(cudaEventRecord(st->sync_ev, st->s));
+    CK(cudaStreamWaitEvent(user, st->sync_ev, 0));
+    return FOE_OK;
+}
+
+K1Args state_k1_args(const ipiano_state* st, int which_cur) {
+    K1Args a{};
+    a.w = st->w;
+    a.w_slot_stride = (size_t)st->B * st->HW;
+    a.g = st->g;
+    a.g_group_stride = (size_t)st->B * st->HW;
+    a.g_slot_stride = a.g_group_stride * st->groups;
+    a.epart = st->epart;
+    a.ctl = st->ctl;
+    a.which_cur = which_cur;
+    a.H = st->H;
+    a.W = st->W;
+    a.tiles_x = st->tiles_x;
+    a.ntiles = st->ntiles;
+    a.groups = st->groups;
+    a.nf = st->model->nf;
+    a.nchunks = st->nchunks;
+    return a;
+}
+
+cudaEvent_t pool_event(ipiano_state* st) {
+    if (!st->ev_pool.empty()) {
+        cudaEvent_t e = st->ev_pool.back();
+        st->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// One trial round for every active image: K2 -> K1 (candidate) -> K3.
+foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
+    foe::K2Args a2{};
+    a2.w = st->w;
+    a2.w_slot_stride = (size_t)st->B * st->HW;
+    a2.g = st->g;
+    a2.g_group_stride = (size_t)st->B * st->HW;
+    a2.g_slot_stride = a2.g_group_stride * st->groups;
+    a2.ft = st->ft;
+    a2.ppart = st->ppart;
+    a2.ctl = st->ctl;
+    a2.sp = st->sp;
+    a2.groups = st->groups;
+    a2.nblk = st->nblk2;
+    a2.HW = st->HW;
+    foe::k_inertial_prox<kPxt2><<<dim3(st->nblk2, st->B), kThreads, 0, s>>>(a2);
+    CKL("k_inertial_prox");
+    const K1Args a1 = state_k1_args(st, 0);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timed) {
+        e0 = pool_event(st);
+        e1 = pool_event(st);
+        CK(cudaEventRecord(e0, s));
+    }
+    k1_dispatch(st->model->m, false, a1, *st->model->tp, dim3(st->ntiles * st->groups, st->B), s);
+    CKL("k_prior_grad");
+    if (timed) {
+        CK(cudaEventRecord(e1, s));
+        st->ev_live.emplace_back(e0, e1);
+        st->k1_launches += 1;
+    }
+    foe::K3Args a3{};
+    a3.ctl = st->ctl;
+    a3.epart = st->epart;
+    a3.ppart = st->ppart;
+    a3.trace = st->trace;
+    a3.ne = st->ntiles * st->groups;
+    a3.nblk = st->nblk2;
+    a3.sp = st->sp;
+    foe::k_decide<<<st->B, kThreads, 0, s>>>(a3);
+    CKL("k_decide");
+    st->total_launches += 3;
+    return FOE_OK;
+}
+
+constexpr int kGraphRounds = 10;
+
+foe_status ensure_graph(ipiano_state* st) {
+    if (st->graph) return FOE_OK;
+    cudaGraph_t g = nullptr;
+    CK(cudaStreamBeginCapture(st->s, cudaStreamCaptureModeThreadLocal));
+    foe_status r = FOE_OK;
+    const long long tl = st->total_launches;
+    for (int i = 0; i < kGraphRounds && r == FOE_OK; ++i) r = launch_round(st, st->s, false);
+    st->total_launches = tl;
+    cudaError_t e = cudaStreamEndCapture(st->s, &g);
+    if (r != FOE_OK) { if (g) cudaGraphDestroy(g); return r; }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture", __LINE__);
+    e = cudaGraphInstantiate(&st->graph, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate", __LINE__);
+    st->graph_rounds = kGraphRounds;
+    return FOE_OK;
+}
+
+foe_status launch_rounds(ipiano_state* st, int rounds) {
+    if (st->profile) {
+        for (int i = 0; i < rounds; ++i) {
+            foe_status r = launch_round(st, st->s, true);
+            if (r != FOE_OK) return r;
+        }
+        return FOE_OK;
+    }
+    foe_status r = ensure_graph(st);
+    if (r != FOE_OK) return r;
+    const int reps = div_up(rounds, st->graph_rounds);
+    for (int i = 0; i < reps; ++i) {
+        CK(cudaGraphLaunch(st->graph, st->s));
+        st->total_launches += 3LL * st->graph_rounds;
+    }
+    return FOE_OK;
+}
+
+foe_status sync_ctl(ipiano_state* st) {
+    CK(cudaMemcpyAsync(st->hctl, st->ctl, sizeof(ImgCtl) * st->B, cudaMemcpyDeviceToHost, st->s));
+    CK(cudaStreamSynchronize(st->s));
+    for (auto& pr : st->ev_live) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) st->k1_ms += ms;
+        st->ev_pool.push_back(pr.first);
+        st->ev_pool.push_back(pr.second);
+    }
+    st->ev_live.clear();
+    return FOE_OK;
+}
+
+foe_status first_image_error(const ipiano_state* st) {
+    for (int b = 0; b < st->B; ++b) {
+        const ImgCtl& c = st->hctl[b];
+        if (c.status != 0) {
+            const char* what = c.status == foe::ST_PROX        ? "prox Newton cap exceeded (SPEC.md:198)"
+                               : c.status == foe::ST_BACKTRACK ? "more than max_backtracks doublings (SPEC.md:288)"
+                               : c.status == foe::ST_DOMAIN    ? "accepted |w| above w_guard (R-11)"
+                                                               : "non-finite accepted energy or iterate (SPEC.md:288)";
+            return fail((foe_status)c.status, "image %d, iteration %d: %s", b, c.n + 1, what);
+        }
+    }
+    return FOE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void ipiano_state_destroy(ipiano_state* st) {
+    if (!st) return;
+    cudaSetDevice(st->model->dev);
+    if (st->s) cudaStreamSynchronize(st->s);
+    if (st->graph) cudaGraphExecDestroy(st->graph);
+    cudaFree(st->w); cudaFree(st->g); cudaFree(st->ft); cudaFree(st->epart); cudaFree(st->ppart);
+    cudaFree(st->trace); cudaFree(st->ctl);
+    if (st->hctl) cudaFreeHost(st->hctl);
+    for (auto e : st->ev_pool) cudaEventDestroy(e);
+    for (auto& pr : st->ev_live) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    if (st->sync_ev) cudaEventDestroy(st->sync_ev);
+    if (st->s) cudaStreamDestroy(st->s);
+    delete st;
+}
+
+foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H, int W,
+                               const double* lambda_per_image, const double* lipschitz_init,
+                               const ipiano_config* cfg_in, void* stream, ipiano_state** out) {
+    if (!out) return fail(FOE_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    foe_status rs = check_dims(md, B, H, W);
+    if (rs != FOE_OK) return rs;
+    if (!f) return fail(FOE_ERR_INVALID_ARGUMENT, "f is NULL");
+    if (!lipschitz_init) return fail(FOE_ERR_INVALID_ARGUMENT, "lipschitz_init is NULL");
+    ipiano_config cfg;
+    if (cfg_in) cfg = *cfg_in; else ipiano_config_default(&cfg);
+    if (!(cfg.beta >= 0.0 && cfg.beta < 1.0)) return fail(FOE_ERR_INVALID_ARGUMENT, "beta=%g outside [0,1)", cfg.beta);
+    if (cfg.max_iters < 1) return fail(FOE_ERR_INVALID_ARGUMENT, "max_iters=%d must be >= 1", cfg.max_iters);
+    if (!(cfg.step_safety > 0.0 && cfg.step_safety <= 1.0))
+        return fail(FOE_ERR_INVALID_ARGUMENT, "step_safety=%g outside (0,1]", cfg.step_safety);
+    if (!(cfg.backtrack_factor > 1.0)) return fail(FOE_ERR_INVALID_ARGUMENT, "backtrack_factor=%g must be > 1", cfg.backtrack_factor);
+    if (!(cfg.shrink > 0.0 && cfg.shrink <= 1.0)) return fail(FOE_ERR_INVALID_ARGUMENT, "shrink=%g outside (0,1]", cfg.shrink);
+    if (cfg.max_backtracks < 0 || cfg.newton_max_iters < 1 || !(cfg.newton_tol > 0.0) || !(cfg.w_guard > 0.0) ||
+        !(cfg.rel_change_tol >= 0.0))
+        return fail(FOE_ERR_INVALID_ARGUMENT, "invalid solver limits (max_backtracks, newton_max_iters, newton_tol, w_guard, rel_change_tol)");
+    for (int b = 0; b < B; ++b) {
+        if (!(lipschitz_init[b] > 0.0) || !std::isfinite(lipschitz_init[b]))
+            return fail(FOE_ERR_INVALID_ARGUMENT, "lipschitz_init[%d]=%g must be > 0", b, lipschitz_init[b]);
+        if (lambda_per_image) {
+            const double l1 = lambda_per_image[2 * b], l2 = lambda_per_image[2 * b + 1];
+            if (!(l1 >= 0) || !(l2 >= 0) || !std::isfinite(l1) || !std::isfinite(l2) || (l1 == 0 && l2 == 0))
+                return fail(FOE_ERR_INVALID_ARGUMENT, "lambda of image %d = (%g,%g) invalid", b, l1, l2);
+        }
+    }
+    CK(cudaSetDevice(md->dev));
+    ipiano_state* st = new (std::nothrow) ipiano_state();
+    if (!st) return fail(FOE_ERR_OUT_OF_MEMORY, "host allocation");
+    st->model = md;
+    st->B = B; st->H = H; st->W = W;
+    st->HW = (size_t)H * W;
+    st->cfg = cfg;
+    st->sp.beta = cfg.beta;
+    st->sp.safety = cfg.step_safety;
+    st->sp.eta = cfg.backtrack_factor;
+    st->sp.shrink = cfg.shrink;
+    st->sp.newton_tol = cfg.newton_tol;
+    st->sp.rel_tol = cfg.rel_change_tol;
+    st->sp.w_guard = cfg.w_guard;
+    st->sp.max_backtracks = cfg.max_backtracks;
+    st->sp.newton_cap = cfg.newton_max_iters;
+    st->sp.record_trace = cfg.record_trace;
+    st->sp.max_iters = cfg.max_iters;
+    st->tiles_x = div_up(W, kTile);
+    st->ntiles = st->tiles_x * div_up(H, kTile);
+    st->nchunks = div_up(md->nf, Tr<7>::NC);
+    st->groups = choose_groups(md, st->ntiles, B, cfg.filter_groups);
+    st->nblk2 = div_up((long long)st->HW, (long long)kThreads * kPxt2);
+    auto cleanup = [&](foe_status s) { ipiano_state_destroy(st); return s; };
+#define CKS(call)                                                                    \
+    do {                                                                             \
+        cudaError_t e_ = (call);                                                     \
+        if (e_ != cudaSuccess) return cleanup(cuda_fail(e_, #call, __LINE__));       \
+    } while (0)
+    CKS(cudaStreamCreateWithFlags(&st->s, cudaStreamNonBlocking));
+    CKS(cudaEventCreateWithFlags(&st->sync_ev, cudaEventDisableTiming));
+    const size_t n = (size_t)B * st->HW;
+    CKS(cudaMalloc((void**)&st->w, sizeof(double) * 3 * n));
+    CKS(cudaMalloc((void**)&st->g, sizeof(float) * 2 * st->groups * n));
+    CKS(cudaMalloc((void**)&st->ft, sizeof(float) * n));
+    CKS(cudaMalloc((void**)&st->epart, sizeof(double) * B * st->ntiles * st->groups));
+    CKS(cudaMalloc((void**)&st->ppart, sizeof(double) * B * st->nblk2 * foe::kNumPart));
+    CKS(cudaMalloc((void**)&st->trace, sizeof(double) * B * (cfg.max_iters + 1) * 8));
+    CKS(cudaMemset(st->trace, 0, sizeof(double) * B * (cfg.max_iters + 1) * 8));
+    CKS(cudaMalloc((void**)&st->ctl, sizeof(ImgCtl) * B));
+    CKS(cudaMallocHost((void**)&st->hctl, sizeof(ImgCtl) * B));
+    for (int b = 0; b < B; ++b) {
+        ImgCtl& c = st->hctl[b];
+        std::memset(&c, 0, sizeof(c));
+        c.L = lipschitz_init[b];
+        c.lam1 = lambda_per_image ? lambda_per_image[2 * b] : md->lam[0];
+        c.lam2 = md->term == FOE_DATA_NAKAGAMI ? 0.0 : (lambda_per_image ? lambda_per_image[2 * b + 1] : md->lam[1]);
+        c.cur = 0; c.prev = 1; c.cand = 2;
+        c.gcur = 0; c.gcand = 1;
+        c.active = 1;  // for the initial evaluation
+        c.target = 0;
+    }
+    cudaStream_t user = (cudaStream_t)stream;
+    if (join_begin(st, user) != FOE_OK) return cleanup(FOE_ERR_CUDA);
+    CKS(cudaMemcpyAsync(st->ctl, st->hctl, sizeof(ImgCtl) * B, cudaMemcpyHostToDevice, st->s));
+    foe::k_init<<<dim3(st->nblk2, B), kThreads, 0, st->s>>>(f, st->ft, st->w, n, st->ppart, st->nblk2, st->ctl,
+                                                             st->HW, kPxt2);
+    CKS(cudaGetLastError());
+    const K1Args a1 = state_k1_args(st, 1);
+    k1_dispatch(md->m, false, a1, *md->tp, dim3(st->ntiles * st->groups, B), st->s);
+    CKS(cudaGetLastError());
+    foe::k_init_finalize<<<B, kThreads, 0, st->s>>>(st->ctl, st->epart, st->ntiles * st->groups, st->ppart,
+                                                    st->nblk2, st->trace, cfg.max_iters, cfg.record_trace);
+    CKS(cudaGetLastError());
+    foe::k_set_target<<<div_up(B, 128), 128, 0, st->s>>>(st->ctl, B, 0);
+    CKS(cudaGetLastError());
+    if (join_end(st, user) != FOE_OK) return cleanup(FOE_ERR_CUDA);
+#undef CKS
+    *out = st;
+    return FOE_OK;
+}
+
+foe_status ipiano_solve(ipiano_state* st, void* stream) {
+    if (!st) return fail(FOE_ERR_INVALID_ARGUMENT, "state is NULL");
+    CK(cudaSetDevice(st->model->dev));
+    cudaStream_t user = (cudaStream_t)stream;
+    foe_status r = join_begin(st, user);
+    if (r != FOE_OK) return r;
+    foe::k_set_target<<<div_up(st->B, 128), 128, 0, st->s>>>(st->ctl, st->B, st->cfg.max_iters);
+    CKL("k_set_target");
+    r = sync_ctl(st);
+    if (r != FOE_OK) return r;
+    const long long max_rounds = (long long)st->cfg.max_iters * (st->cfg.max_backtracks + 2) + 8;
+    long long done_rounds = 0;
+    for (;;) {
+        int min_n = st->cfg.max_iters;
+        bool any = false;
+        for (int b = 0; b < st->B; ++b)
+            if (st->hctl[b].active) { any = true; min_n = std::min(min_n, st->hctl[b].n); }
+        if (!any || done_rounds > max_rounds) break;
+        const int rounds = std::max(1, st->cfg.max_iters - min_n);
+        r = launch_rounds(st, rounds);
+        if (r != FOE_OK) return r;
+        done_rounds += rounds;
+        r = sync_ctl(st);
+        if (r != FOE_OK) return r;
+    }
+    r = join_end(st, user);
+    if (r != FOE_OK) return r;
+    return first_image_error(st);
+}
+
+foe_status ipiano_step(ipiano_state* st, void* stream, int* accepted_iters_out) {
+    if (!st) return fail(FOE_ERR_INVALID_ARGUMENT, "state is NULL");
+    CK(cudaSetDevice(st->model->dev));
+    cudaStream_t user = (cudaStream_t)stream;
+    foe_status r = join_begin(st, user);
+    if (r != FOE_OK) return r;
+    r = sync_ctl(st);
+    if (r != FOE_OK) return r;
+    // per-image target n_b + 1 (capped at max_iters)
+    for (int b = 0; b < st->B; ++b) {
+        ImgCtl& c = st->hctl[b];
+        c.target = std::min(c.n + 1, st->cfg.max_iters);
+        c.active = (c.status == 0 && !c.done && c.n < c.target) ? 1 : 0;
+    }
+    CK(cudaMemcpyAsync(st->ctl, st->hctl, sizeof(ImgCtl) * st->B, cudaMemcpyHostToDevice, st->s));
+    const int max_rounds = st->cfg.max_backtracks + 2;
+    for (int i = 0; i < max_rounds; ++i) {
+        bool any = false;
+        for (int b = 0; b < st->B; ++b) any |= st->hctl[b].active != 0;
+        if (!any) break;
+        r = launch_rounds(st, 1);
+        if (r != FOE_OK) return r;
+        r = sync_ctl(st);
+        if (r != FOE_OK) return r;
+    }
+    if (accepted_iters_out)
+        for (int b = 0; b < st->B; ++b) accepted_iters_out[b] = st->hctl[b].n;
+    r = join_end(st, user);
+    if (r != FOE_OK) return r;
+    return first_image_error(st);
+}
+
+foe_status ipiano_get_iterate(const ipiano_state* st, double* w_out, float* u_out, void* stream) {
+    if (!st) return fail(FOE_ERR_INVALID_ARGUMENT, "state is NULL");
+    CK(cudaSetDevice(st->model->dev));
+    ipiano_state* s = const_cast<ipiano_state*>(st);
+    cudaStream_t user = (cudaStream_t)stream;
+    foe_status r = join_begin(s, user);
+    if (r != FOE_OK) return r;
+    r = sync_ctl(s);  // the current slot index lives in the control block
+    if (r != FOE_OK) return r;
+    const size_t n = (size_t)st->B * st->HW;
+    // images may sit in different slots: copy per image
+    for (int b = 0; b < st->B; ++b) {
+        const double* src = st->w + (size_t)st->hctl[b].cur * n + (size_t)b * st->HW;
+        if (w_out) CK(cudaMemcpyAsync(w_out + (size_t)b * st->HW, src, sizeof(double) * st->HW, cudaMemcpyDeviceToDevice, s->s));
+        if (u_out) {
+            foe::k_exp_out<<<div_up((long long)st->HW, 256), 256, 0, s->s>>>(src, u_out + (size_t)b * st->HW, st->HW);
+            CKL("k_exp_out");
+        }
+    }
+    return join_end(s, user);
+}
+
+foe_status ipiano_get_counters(const ipiano_state* st, int* iters, int* trials, int* status, double* lipschitz) {
+    if (!st) return fail(FOE_ERR_INVALID_ARGUMENT, "state is NULL");
+    CK(cudaSetDevice(st->model->dev));
+    ipiano_state* s = const_cast<ipiano_state*>(st);
+    foe_status r = sync_ctl(s);
+    if (r != FOE_OK) return r;
+    for (int b = 0; b < st->B; ++b) {
+        if (iters) iters[b] = st->hctl[b].n;
+        if (trials) trials[b] = st->hctl[b].total_trials;
+        if (status) status[b] = st->hctl[b].status;
+        if (lipschitz) lipschitz[b] = st->hctl[b].L;
+    }
+    return FOE_OK;
+}
+
+foe_status ipiano_get_trace(const ipiano_state* st, void* host_trace, size_t bytes) {
+    if (!st || !host_trace) return fail(FOE_ERR_INVALID_ARGUMENT, "state or host_trace is NULL");
+    const size_t need = sizeof(double) * 8 * st->B * (size_t)(st->cfg.max_iters + 1);
+    if (bytes < need) return fail(FOE_ERR_INVALID_ARGUMENT, "trace buffer %zu bytes < %zu", bytes, need);
+    CK(cudaSetDevice(st->model->dev));
+    CK(cudaMemcpyAsync(host_trace, st->trace, need, cudaMemcpyDeviceToHost, st->s));
+    CK(cudaStreamSynchronize(st->s));
+    return FOE_OK;
+}
+
+foe_status ipiano_profile(ipiano_state* st, int enable) {
+    if (!st) return fail(FOE_ERR_INVALID_ARGUMENT, "state is NULL");
+    st->profile = enable != 0;
+    return FOE_OK;
+}
+
+foe_status ipiano_profile_read(ipiano_state* st, double* k1_ms, long long* k1_launches, long long* total_launches) {
+    if (!st) return fail(FOE_ERR_INVALID_ARGUMENT, "state is NULL");
+    CK(cudaSetDevice(st->model->dev));
+    foe_status r = sync_ctl(st);
+    if (r != FOE_OK) return r;
+    if (k1_ms) *k1_ms = st->k1_ms;
+    if (k1_launches) *k1_launches = st->k1_launches;
+    if (total_launches) *total_launches = st->total_launches;
+    st->k1_ms = 0.0;
+    st->k1_launches = 0;
+    st->total_launches = 0;
+    return FOE_OK;
+}
+
+foe_status ipiano_run(const foe_model* md, const float* f, int B, int H, int W, const double* lambda_per_image,
+                      const double* lipschitz_init, const ipiano_config* cfg, float* u_out, void* trace,
+                      size_t trace_bytes, void* stream) {
+    foe_status r = check_dims(md, B, H, W);
+    if (r != FOE_OK) return r;
+    if (!f || !u_out) return fail(FOE_ERR_INVALID_ARGUMENT, "f and u_out must be non-NULL");
+    CK(cudaSetDevice(md->dev));
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t n = (size_t)B * H * W;
+    const bool f_dev = is_device_ptr(f), u_dev = is_device_ptr(u_out);
+    float* df = nullptr;
+    float* du = nullptr;
+    if (!f_dev) {
+        CK(cudaMallocAsync((void**)&df, sizeof(float) * n, s));
+        CK(cudaMemcpyAsync(df, f, sizeof(float) * n, cudaMemcpyHostToDevice, s));
+    }
+    if (!u_dev) CK(cudaMallocAsync((void**)&du, sizeof(float) * n, s));
+    ipiano_state* st = nullptr;
+    r = ipiano_state_create(md, f_dev ? f : df, B, H, W, lambda_per_image, lipschitz_init, cfg, stream, &st);
+    if (r == FOE_OK) r = ipiano_solve(st, stream);
+    foe_status r2 = FOE_OK;
+    if (st) {
+        const std::string keep = g_err;
+        r2 = ipiano_get_iterate(st, nullptr, u_dev ? u_out : du, stream);
+        if (r2 == FOE_OK && trace) r2 = ipiano_get_trace(st, trace, trace_bytes);
+        ipiano_state_destroy(st);
+        if (r != FOE_OK) g_err = keep;
+    }
+    if (!u_dev && r2 == FOE_OK) CK(cudaMemcpyAsync(u_out, du, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+    if (df) CK(cudaFreeAsync(df, s));
+    if (du) CK(cudaFreeAsync(du, s));
+    CK(cudaStreamSynchronize(s));
+    return r != FOE_OK ? r : r2;
+}
+
+}  // extern "C"

@@ -1,0 +1,645 @@
+// foe_kernels.cuh -- sm_100a kernels of the FoE/iPiano despeckling hot path.
+//
+//   K1  k_prior_grad   fused FoE prior energy + gradient stencil (Eq.(2),
+//                      :176-183 grad_w F = W sum_i theta_i K_i^T rho'(K_i e^w)).  FP32 FFMA
+//                      register-blocked correlations out of shared memory; taps are
+//                      kernel parameters read through the uniform datapath (LDCU + FFMA
+//                      with a UR operand).
+//   K1h k_prior_hvp    the same stencil for the Hessian-vector product (R-10).
+//   K2  k_inertial_prox  w_hat = w - a g + b (w - w_prev) and the
+//                      Newton prox of Eq.(10) in fp64, plus the
+//                      fixed-order block partials of the backtracking test.
+//   K3  k_decide       per-image decision of the descent-lemma test, state rotation,
+//                      Lipschitz update and trace (device-side control: no host sync per trial).
+//
+// Numerics: the iterate w is fp64 in HBM; the stencil computes in
+// fp32 on u - c (c = e^w at the tile centre; K(u - c) + c sum(k) = K u exactly), the
+// energy accumulates per response in fp32 and per thread/block in fp64, and every
+// reduction has a fixed order (no atomics), so results are bitwise reproducible.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace foe {
+
+constexpr int kMaxFilters = 64;
+constexpr int kMaxTaps = 3136;
+constexpr int kThreads = 256;
+constexpr int kTile = 64;  // output tile side of K1
+constexpr int kNumPart = 8;  // K2 block partials
+
+// Filter taps, resident in the kernel-parameter constant bank.
+struct TapParams {
+    float fwd[kMaxTaps];           // flipped taps: K_i u is a correlation with k_i[m-1-a][m-1-b]
+    float bwd[kMaxTaps];           // 2 theta_i k_i[a][b]: K_i^T is a correlation with k_i (x2 of rho')
+    float sumk[kMaxFilters];       // sum_ab k_i[a][b] (fp64-summed), restores the DC shift
+    double theta_ln2[kMaxFilters]; // theta_i * ln 2 (energy accumulates log2)
+};
+
+// Per-image iPiano control block (device resident; written only by K3 / host setup).
+struct ImgCtl {
+    double L;        // current Lipschitz estimate L_n
+    double F;        // F(w^n)
+    double lam1, lam2;
+    int n;           // accepted iterations
+    int trials;      // failed trials so far in the current iteration
+    int total_trials;
+    int status;      // foe_status of this image
+    int cur, prev, cand;  // w slots
+    int gcur, gcand;      // gradient slots
+    int active;      // take part in the next trial round
+    int done;        // stopped by rel_change_tol
+    int target;      // iterations to reach
+    int pad;
+};
+
+struct SolverParams {
+    double beta, safety, eta, shrink, newton_tol, rel_tol, w_guard;
+    int max_backtracks, newton_cap, record_trace, max_iters;
+};
+
+struct K1Args {
+    const double* w;        // [slots][B][H][W] (or one image set when ctl == nullptr)
+    size_t w_slot_stride;
+    float* g;               // [slots][groups][B][H][W]
+    size_t g_slot_stride;
+    size_t g_group_stride;
+    double* epart;          // [B][tiles*groups] energy partials
+    const ImgCtl* ctl;      // nullable
+    int which_cur;          // 1: evaluate at ctl.cur -> ctl.gcur; 0: ctl.cand -> ctl.gcand
+    int H, W, tiles_x, ntiles, groups, nf, nchunks;
+    // HVP only
+    const double* v;        // [B][H][W]
+    const float* gw;        // [B][H][W] gradient at w
+};
+
+__device__ __forceinline__ int wrap_idx(int i, int n) {
+    int r = i % n;
+    return r < 0 ? r + n : r;
+}
+
+// ---------------------------------------------------------------------------------
+// Geometry of K1 for an m x m bank.
+// ---------------------------------------------------------------------------------
+template <int M, int NC, int SF>
+struct K1Geom {
+    static constexpr int C = (M - 1) / 2;
+    static constexpr int CW = 4;                                  // columns per thread item
+    static constexpr int RX = ((kTile + 2 * C + 3) / 4) * 4;      // response cols computed
+    static constexpr int NSTRIP_F = RX / CW;
+    static constexpr int RY = ((kTile + 2 * C + SF - 1) / SF) * SF;  // response rows computed
+    static constexpr int NSEG_F = RY / SF;
+    static constexpr int ITEMS_F = NSTRIP_F * NSEG_F;             // forward items per filter
+    static constexpr int NV = (CW + M - 1 + 3) / 4;               // float4 per row read
+    static constexpr int UY = RY + M - 1;                         // staged rows
+    static constexpr int UX = RX + M - 1;                         // staged cols used
+    static constexpr int UP0 = ((RX - CW + 4 * NV) > UX ? (RX - CW + 4 * NV) : UX);
+    static constexpr int UP1 = ((UP0 + 3) / 4) * 4;
+    static constexpr int UP = ((UP1 * SF) % 32 == 0) ? UP1 + 4 : UP1;  // staged pitch
+    static constexpr int SB = 4;                                  // backward rows per item
+    static constexpr int PP0 = ((kTile - CW + 4 * NV) > RX ? (kTile - CW + 4 * NV) : RX);
+    static constexpr int PP = ((PP0 + 3) / 4) * 4;                // rho' pitch
+    static constexpr int WPF = (kThreads / 32) / NC;              // warps per filter (forward)
+    static_assert(WPF * NC == kThreads / 32, "NC must divide the warp count");
+    static constexpr int SMEM_FLOATS = UY * UP + NC * RY * PP;
+    static constexpr int SMEM_FLOATS_HVP = 2 * UY * UP + NC * RY * PP;
+};
+
+// out[o][x] += sum_{a,b} taps[a*M+b] * in[(o+a)*pitch + x + b],  o < S, x < 4.
+// `in` is 16-byte aligned; taps are warp-uniform (constant bank, UR operand).
+template <int M, int S, int NV>
+__device__ __forceinline__ void corr_block(const float* __restrict__ in, int pitch,
+                                           const float* __restrict__ taps, float (&acc)[S][4]) {
+#pragma unroll
+    for (int i = 0; i < S + M - 1; ++i) {
+        float row[4 * NV];
+        const float4* rp = reinterpret_cast<const float4*>(in + i * pitch);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const float4 t = rp[v];
+            row[4 * v + 0] = t.x; row[4 * v + 1] = t.y; row[4 * v + 2] = t.z; row[4 * v + 3] = t.w;
+        }
+#pragma unroll
+        for (int a = 0; a < M; ++a) {
+            const int o = i - a;
+            if (o >= 0 && o < S) {
+#pragma unroll
+                for (int b = 0; b < M; ++b) {
+                    const float t = taps[a * M + b];
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) acc[o][x] = fmaf(t, row[x + b], acc[o][x]);
+                }
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Fixed-order block sum (all threads get the result).  `red` holds >= 32 doubles.
+__device__ __forceinline__ double block_sum_d(double v, double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum_d(v);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int i = 0; i < nw; ++i) t += red[i];
+    return t;
+}
+__device__ __forceinline__ double block_max_d(double v, double* red) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_max_d(v);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double t = red[0];
+    for (int i = 1; i < nw; ++i) t = fmax(t, red[i]);
+    return t;
+}
+
+// ---------------------------------------------------------------------------------
+// K1: fused prior energy + gradient.  One CTA = one 64x64 output tile x one filter group.
+// ---------------------------------------------------------------------------------
+template <int M, int NC, int SF, bool HVP>
+__global__ void __launch_bounds__(kThreads, 2)
+k_prior_grad(const K1Args args, const __grid_constant__ TapParams tp) {
+    using G = K1Geom<M, NC, SF>;
+    constexpr int C = G::C;
+    extern __shared__ float4 smem4[];
+    float* us = reinterpret_cast<float*>(smem4);           // [UY][UP]  u - c
+    float* uvs = us + G::UY * G::UP;                        // [UY][UP]  u * v (HVP only)
+    float* ps = us + (HVP ? 2 : 1) * G::UY * G::UP;         // [NC][RY][PP] rho' (or rho'' t)
+    __shared__ double red[32];
+
+    const int b = blockIdx.y;
+    int wslot = 0, gslot = 0;
+    if (args.ctl != nullptr) {
+        const ImgCtl& c = args.ctl[b];
+        if (!c.active) return;
+        wslot = args.which_cur ? c.cur : c.cand;
+        gslot = args.which_cur ? c.gcur : c.gcand;
+    }
+    const int H = args.H, W = args.W;
+    const size_t HW = (size_t)H * W;
+    const int tile = blockIdx.x / args.groups, grp = blockIdx.x - tile * args.groups;
+    const int ty = tile / args.tiles_x, tx = tile - ty * args.tiles_x;
+    const int y0 = ty * kTile, x0 = tx * kTile;
+    const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
+    const double* vv = HVP ? args.v + (size_t)b * HW : nullptr;
+    const int ck0 = (grp * args.nchunks) / args.groups;
+    const int ck1 = ((grp + 1) * args.nchunks) / args.groups;
+
+    // (a2) stage u - c on the tile + 2C halo, with c = e^w at the tile centre (fp64 exp).
+    const int yc = wrap_idx(y0 + kTile / 2, H), xc = wrap_idx(x0 + kTile / 2, W);
+    const float cst = (float)exp(w[(size_t)yc * W + xc]);
+    const double cstd = (double)cst;
+    for (int idx = threadIdx.x; idx < G::UY * G::UX; idx += kThreads) {
+        const int uy = idx / G::UX, ux = idx - uy * G::UX;
+        const int gy = wrap_idx(y0 - 2 * C + uy, H), gx = wrap_idx(x0 - 2 * C + ux, W);
+        const size_t gi = (size_t)gy * W + gx;
+        const double u = exp(w[gi]);
+        us[uy * G::UP + ux] = (float)(u - cstd);
+        if (HVP) uvs[uy * G::UP + ux] = (float)(u * vv[gi]);
+    }
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int fj = warp / G::WPF;                               // filter slot of this warp
+    const int flane = (warp - fj * G::WPF) * 32 + lane;        // lane within the filter group
+    const int bstrip = threadIdx.x & 15, bseg = threadIdx.x >> 4;
+    float acc[G::SB][4];
+#pragma unroll
+    for (int o = 0; o < G::SB; ++o)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) acc[o][x] = 0.f;
+    double e_acc = 0.0;
+
+    for (int ck = ck0; ck < ck1; ++ck) {
+        const int fbase = ck * NC;
+        const int nc = min(NC, args.nf - fbase);
+        // (a3, a4, a7) forward responses, rho, rho' of this warp's filter
+        const int j = __shfl_sync(0xffffffffu, fj, 0);
+        if (j < nc) {
+            const int fi = fbase + j;
+            const float* tf = &tp.fwd[fi * M * M];
+            const float cs = cst * tp.sumk[fi];
+            float el = 0.f;
+            for (int it = flane; it < G::ITEMS_F; it += 32 * G::WPF) {
+                const int seg = it / G::NSTRIP_F, strip = it - seg * G::NSTRIP_F;
+                float r[SF][4];
+#pragma unroll
+                for (int o = 0; o < SF; ++o)
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) r[o][x] = 0.f;
+                corr_block<M, SF, G::NV>(us + seg * SF * G::UP + strip * 4, G::UP, tf, r);
+                float* pdst = ps + j * G::RY * G::PP + seg * SF * G::PP + strip * 4;
+                if (!HVP) {
+                    // owned responses: tile rows/cols [0,64) inside the image (energy only)
+                    bool colok[4];
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const int tcx = strip * 4 + x - C;
+                        colok[x] = tcx >= 0 && tcx < kTile && x0 + tcx < W;
+                    }
+#pragma unroll
+                    for (int o = 0; o < SF; ++o) {
+                        const int tcy = seg * SF + o - C;
+                        const bool rowok = tcy >= 0 && tcy < kTile && y0 + tcy < H;
+                        float4 q;
+                        float* qp = reinterpret_cast<float*>(&q);
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) {
+                            const float rv = r[o][x] + cs;
+                            const float d = fmaf(rv, rv, 1.f);
+                            const float lg = __log2f(d);
+                            el += (rowok && colok[x]) ? lg : 0.f;
+                            qp[x] = __fdividef(rv, d);        // rho'(r)/2; the 2 is in bwd taps
+                        }
+                        *reinterpret_cast<float4*>(pdst + o * G::PP) = q;
+                    }
+                } else {
+                    float t[SF][4];
+#pragma unroll
+                    for (int o = 0; o < SF; ++o)
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) t[o][x] = 0.f;
+                    corr_block<M, SF, G::NV>(uvs + seg * SF * G::UP + strip * 4, G::UP, tf, t);
+#pragma unroll
+                    for (int o = 0; o < SF; ++o) {
+                        float4 q;
+                        float* qp = reinterpret_cast<float*>(&q);
+#pragma unroll
+                        for (int x = 0; x < 4; ++x) {
+                            const float rv = r[o][x] + cs;
+                            const float r2 = rv * rv;
+                            const float d = 1.f + r2;
+                            qp[x] = __fdividef((1.f - r2) * t[o][x], d * d);  // rho''(r) t / 2
+                        }
+                        *reinterpret_cast<float4*>(pdst + o * G::PP) = q;
+                    }
+                }
+            }
+            if (!HVP) e_acc += tp.theta_ln2[fi] * (double)el;
+        }
+        __syncthreads();
+        // (a5) transposed correlations, summed over the chunk's filters
+        for (int jj = 0; jj < nc; ++jj) {
+            corr_block<M, G::SB, G::NV>(ps + jj * G::RY * G::PP + bseg * G::SB * G::PP + bstrip * 4,
+                                        G::PP, &tp.bwd[(fbase + jj) * M * M], acc);
+        }
+        __syncthreads();
+    }
+
+    // (a6) chain rule g = u (.) s and store (owned pixels only)
+    float* gout = args.g + (size_t)gslot * args.g_slot_stride + (size_t)grp * args.g_group_stride +
+                  (size_t)b * HW;
+#pragma unroll
+    for (int o = 0; o < G::SB; ++o) {
+        const int oy = bseg * G::SB + o;
+        const int gy = y0 + oy;
+        if (gy >= H) continue;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            const int ox = bstrip * 4 + x;
+            const int gx = x0 + ox;
+            if (gx >= W) continue;
+            const float u = us[(oy + 2 * C) * G::UP + ox + 2 * C] + cst;
+            float val;
+            if (!HVP) {
+                val = u * acc[o][x];
+            } else {
+                const size_t gi = (size_t)gy * W + gx;
+                val = (float)(vv[gi] * (double)args.gw[(size_t)b * HW + gi] + (double)(u * acc[o][x]));
+            }
+            gout[(size_t)gy * W + gx] = val;
+        }
+    }
+    if (!HVP) {
+        const double e = block_sum_d(e_acc, red);
+        if (threadIdx.x == 0) args.epart[(size_t)b * args.ntiles * args.groups + blockIdx.x] = e;
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// K2: inertial forward point + Newton prox of Eq.(10) + block partials of the test.
+// ---------------------------------------------------------------------------------
+
+// Root of phi(z) = z - what + tau [l1 (1 - f^2 e^{-2z}) + l2 (e^{2z} - f^2)]:
+// Newton from what, bisection safeguard on [min(what, log f) - 1, max(what, log f) + 1]
+// (SPEC.md:248), |phi| <= tol.  Returns Newton updates, or -1 past the cap.
+__device__ __forceinline__ int prox_newton(double what, double ft, double tau, double l1,
+                                           double l2, double tol, int cap, double& z_out,
+                                           double& em_out, double& ep_out) {
+    const double lf = log(ft), f2 = ft * ft;
+    double lo = fmin(what, lf) - 1.0, hi = fmax(what, lf) + 1.0;
+    double z = what;
+    for (int it = 0; it <= cap; ++it) {
+        const double em = exp(-2.0 * z), ep = exp(2.0 * z);
+        const double phi = z - what + tau * (l1 * (1.0 - f2 * em) + l2 * (ep - f2));
+        if (fabs(phi) <= tol) { z_out = z; em_out = em; ep_out = ep; return it; }
+        if (phi > 0.0) hi = z; else lo = z;
+        const double dphi = 1.0 + tau * (2.0 * l1 * f2 * em + 2.0 * l2 * ep);
+        double zn = z - phi / dphi;
+        if (!(zn > lo && zn < hi)) zn = 0.5 * (lo + hi);
+        if (zn == z) { z_out = z; em_out = em; ep_out = ep; return it; }
+        z = zn;
+    }
+    z_out = z; em_out = exp(-2.0 * z); ep_out = exp(2.0 * z);
+    return -1;
+}
+
+struct K2Args {
+    double* w;            // [3][B][HW]
+    size_t w_slot_stride;
+    const float* g;       // [2][groups][B][HW]
+    size_t g_slot_stride, g_group_stride;
+    const float* ft;      // [B][HW]  f~ = max(f,1)
+    double* ppart;        // [B][nblk][kNumPart]
+    const ImgCtl* ctl;
+    SolverParams sp;
+    int groups, nblk;
+    size_t HW;
+};
+
+template <int PXT>
+__global__ void __launch_bounds__(kThreads)
+k_inertial_prox(const K2Args a) {
+    __shared__ double red[32];
+    const int b = blockIdx.y;
+    const ImgCtl& c = a.ctl[b];
+    if (!c.active) return;
+    const double alpha = a.sp.safety * 2.0 * (1.0 - a.sp.beta) / c.L;
+    const double beta = a.sp.beta, l1 = c.lam1, l2 = c.lam2;
+    const double* w = a.w + (size_t)c.cur * a.w_slot_stride + (size_t)b * a.HW;
+    const double* wp = a.w + (size_t)c.prev * a.w_slot_stride + (size_t)b * a.HW;
+    double* wn = a.w + (size_t)c.cand * a.w_slot_stride + (size_t)b * a.HW;
+    const float* g = a.g + (size_t)c.gcur * a.g_slot_stride + (size_t)b * a.HW;
+    const float* ft = a.ft + (size_t)b * a.HW;
+    double gd = 0, dd = 0, Gp = 0, ww = 0, wmax = 0, nit = 0, fail = 0;
+    const size_t base = (size_t)blockIdx.x * (kThreads * PXT);
+#pragma unroll 2
+    for (int k = 0; k < PXT; ++k) {
+        const size_t p = base + (size_t)k * kThreads + threadIdx.x;
+        if (p >= a.HW) break;
+        float gs = g[p];
+        for (int q = 1; q < a.groups; ++q) gs += g[(size_t)q * a.g_group_stride + p];
+        const double gv = (double)gs;
+        const double wv = w[p];
+        const double what = wv - alpha * gv + beta * (wv - wp[p]);
+        const double f = (double)ft[p];
+        double z, em, ep;
+        const int it = prox_newton(what, f, alpha, l1, l2, a.sp.newton_tol, a.sp.newton_cap, z, em, ep);
+        wn[p] = z;
+        const double d = z - wv;
+        gd += gv * d;
+        dd += d * d;
+        const double f2 = f * f;
+        Gp += 0.5 * l1 * (2.0 * z + f2 * em) + 0.5 * l2 * (ep - 2.0 * f2 * z);
+        ww += wv * wv;
+        wmax = fmax(wmax, fabs(z));
+        if (it < 0) fail += 1.0; else nit = fmax(nit, (double)it);
+        if (!(z == z)) wmax = INFINITY;
+    }
+    double* out = a.ppart + ((size_t)b * a.nblk + blockIdx.x) * kNumPart;
+    const double s0 = block_sum_d(gd, red);
+    const double s1 = block_sum_d(dd, red);
+    const double s2 = block_sum_d(Gp, red);
+    const double s3 = block_sum_d(ww, red);
+    const double s4 = block_max_d(wmax, red);
+    const double s5 = block_max_d(nit, red);
+    const double s6 = block_sum_d(fail, red);
+    if (threadIdx.x == 0) {
+        out[0] = s0; out[1] = s1; out[2] = s2; out[3] = s3; out[4] = s4; out[5] = s5; out[6] = s6; out[7] = 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// K3: decision, rotation, Lipschitz update, trace (one CTA per image).
+// ---------------------------------------------------------------------------------
+struct K3Args {
+    ImgCtl* ctl;
+    const double* epart;  // [B][ne]
+    const double* ppart;  // [B][nblk][kNumPart]
+    double* trace;        // [B][max_iters+1][8]
+    int ne, nblk;
+    SolverParams sp;
+};
+
+enum { ST_OK = 0, ST_NONFINITE = 4, ST_BACKTRACK = 5, ST_PROX = 6, ST_DOMAIN = 7 };
+
+__global__ void __launch_bounds__(kThreads) k_decide(const K3Args a) {
+    __shared__ double red[32];
+    const int b = blockIdx.x;
+    ImgCtl& c = a.ctl[b];
+    if (!c.active) return;
+    double e = 0.0;
+    for (int i = threadIdx.x; i < a.ne; i += kThreads) e += a.epart[(size_t)b * a.ne + i];
+    double s[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int i = threadIdx.x; i < a.nblk; i += kThreads) {
+        const double* p = a.ppart + ((size_t)b * a.nblk + i) * kNumPart;
+        s[0] += p[0]; s[1] += p[1]; s[2] += p[2]; s[3] += p[3];
+        s[4] = fmax(s[4], p[4]); s[5] = fmax(s[5], p[5]); s[6] += p[6];
+    }
+    const double Fp = block_sum_d(e, red);
+    const double gd = block_sum_d(s[0], red);
+    const double dd = block_sum_d(s[1], red);
+    const double Gp = block_sum_d(s[2], red);
+    const double ww = block_sum_d(s[3], red);
+    const double wmax = block_max_d(s[4], red);
+    const double nit = block_max_d(s[5], red);
+    const double fail = block_sum_d(s[6], red);
+    if (threadIdx.x != 0) return;
+    c.trials += 1;
+    c.total_trials += 1;
+    if (fail > 0.0) {
+        c.status = ST_PROX;
+        c.active = 0;
+        return;
+    }
+    const double L = c.L;
+    const double margin = c.F + gd + 0.5 * L * dd - Fp;
+    const bool ok = isfinite(Fp) && isfinite(gd) && isfinite(dd) && isfinite(Gp) && margin >= 0.0;
+    if (ok) {
+        if (!(wmax <= a.sp.w_guard)) c.status = isfinite(wmax) ? ST_DOMAIN : ST_NONFINITE;  // R-11
+        const int old_prev = c.prev;
+        c.prev = c.cur; c.cur = c.cand; c.cand = old_prev;
+        const int og = c.gcur; c.gcur = c.gcand; c.gcand = og;
+        c.F = Fp;
+        c.n += 1;
+        const double relchg = sqrt(dd) / fmax(sqrt(ww), 1.0);
+        if (a.sp.record_trace) {
+            double* r = a.trace + ((size_t)b * (a.sp.max_iters + 1) + c.n) * 8;
+            r[0] = Fp; r[1] = Gp; r[2] = Fp + Gp; r[3] = L; r[4] = (double)c.trials;
+            r[5] = margin; r[6] = nit; r[7] = relchg;
+        }
+        c.trials = 0;
+        c.L = L * a.sp.shrink;                                        // R-9
+        if (a.sp.rel_tol > 0.0 && relchg < a.sp.rel_tol) c.done = 1;
+    } else {
+        if (c.trials > a.sp.max_backtracks) c.status = ST_BACKTRACK;
+        c.L = L * a.sp.eta;
+    }
+    c.active = (c.status == ST_OK && !c.done && c.n < c.target) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------------
+// Setup / helper kernels
+// ---------------------------------------------------------------------------------
+
+// f~ = max(f,1) (R-4); w^0 = log f~ into slots 0 and 1 (w^{-1} = w^0, R-8); per-block
+// partials of G(w^0) (slot 2 of ppart).
+__global__ void __launch_bounds__(kThreads)
+k_init(const float* f, float* ft, double* w, size_t w_slot_stride, double* ppart, int nblk,
+       const ImgCtl* ctl, size_t HW, int pxt) {
+    __shared__ double red[32];
+    const int b = blockIdx.y;
+    const double l1 = ctl[b].lam1, l2 = ctl[b].lam2;
+    double G = 0.0;
+    const size_t base = (size_t)blockIdx.x * kThreads * pxt;
+    for (int k = 0; k < pxt; ++k) {
+        const size_t p = base + (size_t)k * kThreads + threadIdx.x;
+        if (p >= HW) break;
+        const size_t gi = (size_t)b * HW + p;
+        const float fv = fmaxf(f[gi], 1.0f);
+        ft[gi] = fv;
+        const double fd = (double)fv;
+        const double z = log(fd);
+        w[gi] = z;
+        w[w_slot_stride + gi] = z;
+        const double f2 = fd * fd;
+        G += 0.5 * l1 * (2.0 * z + f2 * exp(-2.0 * z)) + 0.5 * l2 * (exp(2.0 * z) - 2.0 * f2 * z);
+    }
+    const double s = block_sum_d(G, red);
+    if (threadIdx.x == 0) {
+        double* out = ppart + ((size_t)b * nblk + blockIdx.x) * kNumPart;
+        for (int i = 0; i < kNumPart; ++i) out[i] = 0.0;
+        out[2] = s;
+    }
+}
+
+// F(w^0), G(w^0) -> ctl, trace row 0.
+__global__ void __launch_bounds__(kThreads)
+k_init_finalize(ImgCtl* ctl, const double* epart, int ne, const double* ppart, int nblk,
+                double* trace, int max_iters, int record) {
+    __shared__ double red[32];
+    const int b = blockIdx.x;
+    double e = 0.0, g = 0.0;
+    for (int i = threadIdx.x; i < ne; i += kThreads) e += epart[(size_t)b * ne + i];
+    for (int i = threadIdx.x; i < nblk; i += kThreads) g += ppart[((size_t)b * nblk + i) * kNumPart + 2];
+    const double F = block_sum_d(e, red);
+    const double G = block_sum_d(g, red);
+    if (threadIdx.x == 0) {
+        ctl[b].F = F;
+        if (!isfinite(F)) ctl[b].status = ST_NONFINITE;
+        if (record) {
+            double* r = trace + (size_t)b * (max_iters + 1) * 8;
+            r[0] = F; r[1] = G; r[2] = F + G; r[3] = ctl[b].L;
+            r[4] = 0; r[5] = 0; r[6] = 0; r[7] = 0;
+        }
+    }
+}
+
+__global__ void k_set_target(ImgCtl* ctl, int B, int target) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    ImgCtl& c = ctl[b];
+    c.target = target;
+    c.active = (c.status == ST_OK && !c.done && c.n < target) ? 1 : 0;
+}
+
+// out[b][k] = fixed-order sum over blocks of part[b][blk][k] (k < K) -- generic finaliser.
+__global__ void __launch_bounds__(kThreads)
+k_reduce_rows(const double* part, int nblk, int stride, int K, double* out) {
+    __shared__ double red[32];
+    const int b = blockIdx.x;
+    for (int k = 0; k < K; ++k) {
+        double s = 0.0;
+        for (int i = threadIdx.x; i < nblk; i += kThreads) s += part[((size_t)b * nblk + i) * stride + k];
+        s = block_sum_d(s, red);
+        if (threadIdx.x == 0) out[(size_t)b * K + k] = s;
+    }
+}
+
+// data energy partials of a given w (foe_energy_grad): part[b][blk][0]
+__global__ void __launch_bounds__(kThreads)
+k_data_energy(const double* w, const float* f, const double* lam, double* part, int nblk, size_t HW, int pxt) {
+    __shared__ double red[32];
+    const int b = blockIdx.y;
+    const double l1 = lam[2 * b], l2 = lam[2 * b + 1];
+    double G = 0.0;
+    const size_t base = (size_t)blockIdx.x * kThreads * pxt;
+    for (int k = 0; k < pxt; ++k) {
+        const size_t p = base + (size_t)k * kThreads + threadIdx.x;
+        if (p >= HW) break;
+        const size_t gi = (size_t)b * HW + p;
+        const double fd = (double)fmaxf(f[gi], 1.0f);
+        const double z = w[gi];
+        const double f2 = fd * fd;
+        G += 0.5 * l1 * (2.0 * z + f2 * exp(-2.0 * z)) + 0.5 * l2 * (exp(2.0 * z) - 2.0 * f2 * z);
+    }
+    const double s = block_sum_d(G, red);
+    if (threadIdx.x == 0) part[(size_t)b * nblk + blockIdx.x] = s;
+}
+
+// g = sum over groups of the partial gradient planes (fixed order)
+__global__ void k_sum_groups(const float* gparts, size_t group_stride, int groups, float* out, size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    float s = gparts[i];
+    for (int q = 1; q < groups; ++q) s += gparts[(size_t)q * group_stride + i];
+    out[i] = s;
+}
+
+// power iteration helpers: part[b][blk] = {<v,h>, <h,h>, <v0,v0>}
+__global__ void __launch_bounds__(kThreads)
+k_dot3(const double* v, const float* h, double* part, int nblk, size_t HW, int pxt) {
+    __shared__ double red[32];
+    const int b = blockIdx.y;
+    double vh = 0.0, hh = 0.0, vv = 0.0;
+    const size_t base = (size_t)blockIdx.x * kThreads * pxt;
+    for (int k = 0; k < pxt; ++k) {
+        const size_t p = base + (size_t)k * kThreads + threadIdx.x;
+        if (p >= HW) break;
+        const size_t gi = (size_t)b * HW + p;
+        const double a = v[gi];
+        const double c = h ? (double)h[gi] : 0.0;
+        vh += a * c; hh += c * c; vv += a * a;
+    }
+    const double s0 = block_sum_d(vh, red), s1 = block_sum_d(hh, red), s2 = block_sum_d(vv, red);
+    if (threadIdx.x == 0) {
+        double* o = part + ((size_t)b * nblk + blockIdx.x) * 3;
+        o[0] = s0; o[1] = s1; o[2] = s2;
+    }
+}
+
+// v <- src / sqrt(norm2[b*K + k])
+template <typename T>
+__global__ void k_normalize(const T* src, double* v, const double* sums, int K, int k, size_t HW, int B) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= HW * B) return;
+    const int b = (int)(i / HW);
+    v[i] = (double)src[i] / sqrt(sums[(size_t)b * K + k]);
+}
+
+__global__ void k_log_ftilde(const float* f, double* w, size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) w[i] = log((double)fmaxf(f[i], 1.0f));
+}
+
+__global__ void k_exp_out(const double* w, float* u, size_t n) {
+    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) u[i] = (float)exp(w[i]);
+}
+
+}  // namespace foe
