@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 FoE/iPiano despeckling hot path (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl foe|reference]
+
+A *step* is one full pass of the hot path over one batch:
+a1 init (w^0 = log max(f,1), F and grad F at w^0), `iters` iPiano iterations (inertial
+step, Newton prox, energy + gradient at the candidate, backtracking decision), a13 output
+u = e^w.  The metric is megapixel-iterations/s = images * H * W * iters / time (BASELINE.json
+metric).  The Lipschitz initialisation (R-10) is setup, timed separately (lipschitz_ms).
+
+Default workload: BASELINE.json configs[3] (c4) -- 64 independent 512x512 images per GPU
+(L in {1,3,8}), 48 filters 7x7, 300 iterations -- weak scaling (N GPUs -> 64N images,
+global image i keeps its seeds).  c4 is the configuration the FP32-roofline target and the
+multi-GPU scaling target are quoted on.
+
+Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA events on the
+launching stream, with a 256 MiB L2 flush between steps (outside the events); barrier +
+synchronize on both sides; max over ranks.  The fused prior-gradient kernel (K1) is timed
+per launch with CUDA events on its own stream for the roofline entry.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "megapixel-iterations/s of iPiano (FoE grad+prox) and % of B200 FP32 peak"
+UNIT = "MP-it/s"
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["foe", "reference"], default="foe")
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--images", type=int, default=0, help="images per GPU (default: the config's batch)")
+    ap.add_argument("--iters", type=int, default=0, help="override iteration count (quick runs only)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=4, help="oracle sample: iterations on one image")
+    ap.add_argument("--traffic-bytes", type=float, default=None,
+                    help="dram bytes per K1 launch from an ncu --set full capture (roofline.traffic)")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0])); mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def smi_index(local_rank: int) -> int:
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [v for v in vis.split(",") if v.strip()]
+        if local_rank < len(ids) and ids[local_rank].strip().isdigit():
+            return int(ids[local_rank])
+    return local_rank
+
+
+# ------------------------------------------------------------------------- CPU oracle
+
+def oracle_sample(cfg, d, iters):
+    """Time the fp64 oracle (as it stands) on image 0 of the batch for `iters` iterations."""
+    import oracle
+    import foe_synth as S
+    f = d["f"][0]
+    l1, l2 = d["lambdas"][0]
+    v0 = S.lipschitz_start_vector(1, cfg.H, cfg.W)[0]
+    L0 = d.get("L0")
+    L_init = float(L0[0]) if L0 is not None else 2.0 ** 18
+    c = oracle.make_cfg(L_init, iters)
+    t0 = time.perf_counter()
+    run = oracle.ipiano_run(f, d["filters"], d["theta"], l1, l2, c)
+    dt = time.perf_counter() - t0
+    mp_it = cfg.H * cfg.W * iters / 1e6
+    return dict(value=mp_it / dt, seconds=dt, cores=oracle.num_threads(), status=run["status"],
+                sample=f"1 image {cfg.H}x{cfg.W} of {cfg.name}, {iters} iPiano iterations "
+                       f"(+ initial gradient), fp64 C oracle, OpenMP over rows")
+
+
+def run_reference(args, cfg):
+    """--impl reference: the oracle as the reference arm (rank 0 only)."""
+    import foe_synth as S
+    from paper_1404_5344_b200 import dist as D
+    rank, ws, local = D.world()
+    if rank != 0:
+        return 0
+    d = S.make_inputs(cfg, images=[0])
+    d["L0"] = None
+    for _ in range(args.warmup):
+        oracle_sample(cfg, d, 1)
+    vals, secs = [], []
+    for _ in range(args.steps):
+        r = oracle_sample(cfg, d, args.cpu_iters)
+        vals.append(r["value"]); secs.append(r["seconds"])
+    value = len(vals) / sum(1.0 / v for v in vals)  # total MP-it / total time
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / len(secs),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_block(cfg, 1, 1, cfg.H * cfg.W, args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": "oracle",
+                         "sample": r["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(cfg, n_gpus, images_per_gpu, px, args):
+    iters = args.iters or cfg.iters
+    return {
+        "workload": f"{cfg.name}: {cfg.description}" + (f" [iters overridden to {iters}]" if args.iters else ""),
+        "images_per_gpu": images_per_gpu, "global_images": images_per_gpu * n_gpus,
+        "H": cfg.H, "W": cfg.W, "filters": f"{cfg.n_filters}x{cfg.m}x{cfg.m}", "iters": iters,
+        "policy": "iPiano beta=0.4, a=0.95*2(1-b)/L_n, doubling backtracking, L nondecreasing, "
+                  "L_init=2^ceil(log2 rho_hat) (DESIGN.md R-9/R-10)",
+        "l2": "256 MiB buffer written between timed steps (outside the events)",
+        "parallelism": f"dp{n_gpus} (independent images, no data-path collective)",
+    }
+
+
+# ------------------------------------------------------------------------------ main
+
+def main():
+    args = parse_args()
+    import foe_synth as S
+    cfg = S.config(args.config)
+    if args.iters:
+        cfg = S.config(args.config, iters=args.iters)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import paper_1404_5344_b200 as P
+    from paper_1404_5344_b200 import dist as D
+
+    rank, ws, local = D.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n_img = args.images or cfg.B
+    images = D.weak_shard(n_img, rank)
+    d = S.make_inputs(cfg, images=images)
+    B, H, W = d["f"].shape
+    stream = torch.cuda.current_stream(dev)
+    md = P.foe_model_create(d["filters"], d["theta"], lam=tuple(d["lambdas"][0]), device=local)
+    f_dev = torch.as_tensor(d["f"], device=dev)
+    v0 = torch.as_tensor(S.lipschitz_start_vector(B, H, W), device=dev)
+
+    # setup: Lipschitz initialisation (R-10), timed separately
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rho, L0 = P.foe_estimate_lipschitz(md, f_dev, v0, 25)
+    lipschitz_ms = 1e3 * (time.perf_counter() - t0)
+    d["L0"] = L0
+    del v0
+
+    cfgc = P.ipiano_config_default(max_iters=cfg.iters, record_trace=0)
+    st = P.ipiano_state_create(md, f_dev, d["lambdas"], L0, cfgc)
+    u_dev = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+
+    def step():
+        P.ipiano_state_reset(st, f_dev, L0)
+        P.ipiano_solve(st)
+        P.ipiano_get_iterate(st, want_w=False, u_out=u_dev)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region (value): inputs resident in HBM
+    P.ipiano_profile(st, True)
+    P.ipiano_profile_read(st)  # reset counters
+    sampler = ClockSampler(smi_index(local)) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    D.barrier()
+    torch.cuda.synchronize()
+    launches0 = P.foe_kernel_launches()
+    step_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    launches = P.foe_kernel_launches() - launches0
+    D.barrier()
+    clocks = sampler.stop() if sampler else None
+    k1_ms, k1_launches, _ = P.ipiano_profile_read(st)
+    cnt = P.ipiano_get_counters(st)
+    total_ms = D.max_over_ranks(sum(step_ms), dev)
+    mp_it_rank = B * H * W * cfg.iters / 1e6
+    mp_it_total = D.sum_over_ranks(mp_it_rank * args.steps, dev)
+    value = mp_it_total / (total_ms / 1e3)
+
+    # K1 roofline: algorithmic flops = 4 N_f m^2 per pixel per evaluation;
+    # evaluations in the timed region = trials (candidates) of every image, all steps
+    trials_per_step = float(np.sum(cnt["trials"]))
+    flops_per_eval_px = 4.0 * cfg.n_filters * cfg.m * cfg.m
+    k1_flops = flops_per_eval_px * H * W * trials_per_step * args.steps
+    k1_tflops = k1_flops / (k1_ms / 1e3) / 1e12 if k1_ms > 0 else None
+    peaks, peak_src = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak = nsm * 128 * 2 * sm_max * 1e6 / 1e12
+    roofline = {
+        "bound": "alu", "achieved": k1_tflops, "peak": fp32_peak, "unit": "TFLOP/s",
+        "frac": (k1_tflops / fp32_peak) if k1_tflops else None,
+        "traffic": args.traffic_bytes,
+        "kernel": "k_prior_grad (K1, fused FoE energy+gradient stencil)",
+        "peak_source": f"derived: {nsm} SMs x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz "
+                       f"(sm_max_mhz, {peak_src} MEASURED_PEAKS.json) -- DESIGN.md",
+        "k1_ms_per_launch": k1_ms / max(k1_launches, 1), "k1_launches": k1_launches,
+        "k1_share_of_step": (k1_ms / sum(step_ms)) if step_ms else None,
+    }
+
+    # ---- e2e: the public C-ABI call with host buffers (H2D of f and D2H of u inside)
+    e2e = None
+    if not args.no_e2e:
+        f_pin = torch.empty((B, H, W), dtype=torch.float32, pin_memory=True)
+        f_pin.copy_(torch.as_tensor(d["f"]))
+        u_pin = torch.empty((B, H, W), dtype=torch.float32, pin_memory=True)
+        f_np, u_np = f_pin.numpy(), u_pin.numpy()
+        P.ipiano_run(md, f_np, d["lambdas"], L0, cfgc, u_out=u_np, want_trace=False)  # warm
+        D.barrier()
+        torch.cuda.synchronize()
+        e2e_ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            P.ipiano_run(md, f_np, d["lambdas"], L0, cfgc, u_out=u_np, want_trace=False)
+            e1.record(stream)
+            e1.synchronize()
+            e2e_ms.append(e0.elapsed_time(e1))
+        D.barrier()
+        e2e_total = D.max_over_ranks(sum(e2e_ms), dev)
+        e2e = {"value": mp_it_total / (e2e_total / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(f_np.nbytes), "d2h_bytes_per_step": int(u_np.nbytes),
+               "ms_per_step": e2e_total / args.steps,
+               "call": "ipiano_run (C ABI) with pinned host f and u; state alloc + a1..a13 + copies"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        r = oracle_sample(cfg, d, args.cpu_iters)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "oracle",
+               "sample": r["sample"], "seconds": r["seconds"]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "dtype_detail": "fp32 stencil (FFMA), fp64 iterate/prox/reductions",
+            "data": "synthetic", "config": config_block(cfg, ws, B, H * W, args),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks, "trials_per_iter": trials_per_step / (B * cfg.iters),
+            "run_fp32_frac": (flops_per_eval_px * H * W * trials_per_step * args.steps * ws / (total_ms / 1e3) / 1e12)
+                             / fp32_peak / ws,
+            "lipschitz_ms": lipschitz_ms, "status": [int(s) for s in set(cnt["status"].tolist())],
+        }
+        print(json.dumps(line), flush=True)
+    st.destroy()
+    md.destroy()
+    D.barrier()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

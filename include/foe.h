@@ -70,6 +70,9 @@ const char* foe_last_error(void);
 const char* foe_status_string(foe_status s);
 /* Library version string, and the compiled target (e.g. "sm_100a"). */
 const char* foe_version(void);
+/* Number of CUDA kernels this library has launched in this process (graph replays count
+ * each captured kernel); for launch accounting in benchmarks. */
+long long foe_kernel_launches(void);
 
 /* ------------------------------------------------------------------------------ model */
 
@@ -77,7 +80,7 @@ typedef struct foe_model foe_model;
 
 /* Creates the FoE model {(k_i, theta_i)} of Eq.(2) plus the data-term weights of Eq.(10).
  *   filters  host fp32 [n_filters][m][m] row-major taps k_i
- *   m        odd filter side, 3 <= m <= 9 supported kernels: m in {3, 5, 7} (FOE_ERR_UNSUPPORTED otherwise)
+ *   m        odd filter side; this build has kernels for m in {3, 5, 7} (else FOE_ERR_UNSUPPORTED)
  *   alphas   host fp32 [n_filters], the weights theta_i > 0 ("alphas" in BASELINE.json)
  *   lambda   host fp64 [2] = {l1, l2} (Eq.(10)), both >= 0 and not both 0; NULL -> the
  *            paper's preset for looks_L (L=8 (550,0.02), L=3 (310,0.008),
@@ -170,6 +173,11 @@ typedef struct ipiano_state ipiano_state;
 foe_status ipiano_state_create(const foe_model* model, const float* f, int B, int H, int W,
                                const double* lambda_per_image, const double* lipschitz_init,
                                const ipiano_config* cfg, void* stream, ipiano_state** out);
+
+/* Re-initialises an existing state from new observations f (same B, H, W; device fp32) and
+ * Lipschitz initialisations, without reallocating: w^0 = log f~, w^{-1} = w^0, F(w^0),
+ * grad F(w^0) (the same a1 step as ipiano_state_create).  Asynchronous on `stream`. */
+foe_status ipiano_state_reset(ipiano_state* st, const float* f, const double* lipschitz_init, void* stream);
 
 /* Advances every unfinished image by exactly one accepted iPiano iteration (as many
  * backtracking trials as it needs), then synchronises.  accepted_iters_out (host [B] or

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -24,6 +25,11 @@ using foe::TapParams;
 namespace {
 
 thread_local std::string g_err;
+std::atomic<long long> g_launches{0};  // kernels launched by this library (process-wide)
+thread_local bool t_capturing = false;   // graph capture: replays are counted instead
+inline void count_launch(long long n) {
+    if (!t_capturing) g_launches.fetch_add(n, std::memory_order_relaxed);
+}
 
 foe_status fail(foe_status s, const char* fmt, ...) {
     char buf[1024];
@@ -79,6 +85,7 @@ void k1_launch(const K1Args& a, const TapParams& tp, dim3 grid, cudaStream_t s) 
 }
 
 void k1_dispatch(int m, bool hvp, const K1Args& a, const TapParams& tp, dim3 grid, cudaStream_t s) {
+    count_launch(1);
     switch (m) {
         case 7: hvp ? k1_launch<7, true>(a, tp, grid, s) : k1_launch<7, false>(a, tp, grid, s); break;
         case 5: hvp ? k1_launch<5, true>(a, tp, grid, s) : k1_launch<5, false>(a, tp, grid, s); break;
@@ -116,6 +123,7 @@ struct ipiano_state {
     double* trace = nullptr;  // [B][max_iters+1][8]
     ImgCtl* ctl = nullptr;
     ImgCtl* hctl = nullptr;   // pinned mirror
+    std::vector<double> lam;  // [B][2]
     cudaStream_t s = nullptr;
     cudaEvent_t sync_ev = nullptr;
     cudaGraphExec_t graph = nullptr;
@@ -148,6 +156,8 @@ const char* foe_status_string(foe_status s) {
 }
 
 const char* foe_version(void) { return "libfoe 0.1.0 sm_100a"; }
+
+long long foe_kernel_launches(void) { return g_launches.load(); }
 
 foe_status foe_model_create(const float* filters, int n_filters, int m, const float* alphas,
                             const double* lambda, double looks_L, foe_data_term term,
@@ -348,9 +358,11 @@ foe_status foe_energy_grad(const foe_model* md, const double* w, const float* f,
     if (grad && !direct) {
         const size_t n = (size_t)B * HW;
         foe::k_sum_groups<<<div_up((long long)n, 256), 256, 0, s>>>(gparts, n, groups, grad, n);
+        count_launch(1);
         CKL("k_sum_groups");
     }
     foe::k_reduce_rows<<<B, kThreads, 0, s>>>(epart, ne, 1, 1, dred);
+    count_launch(1);
     CKL("k_reduce_rows");
     if (data_energy) {
         std::vector<double> lam(2 * (size_t)B);
@@ -362,8 +374,10 @@ foe_status foe_energy_grad(const foe_model* md, const double* w, const float* f,
         CK(cudaMallocAsync((void**)&dpart, sizeof(double) * B * nblk, s));
         CK(cudaMemcpyAsync(dlam, lam.data(), sizeof(double) * 2 * B, cudaMemcpyHostToDevice, s));
         foe::k_data_energy<<<dim3(nblk, B), kThreads, 0, s>>>(w, f, dlam, dpart, nblk, HW, kPxt2);
+        count_launch(1);
         CKL("k_data_energy");
         foe::k_reduce_rows<<<B, kThreads, 0, s>>>(dpart, nblk, 1, 1, dred + B);
+        count_launch(1);
         CKL("k_reduce_rows");
     }
     std::vector<double> hred(2 * (size_t)B);
@@ -427,18 +441,24 @@ foe_status foe_estimate_lipschitz(const foe_model* md, const float* f, int B, in
     CK(cudaMallocAsync((void**)&sums, sizeof(double) * B * 3, s));
     const int eb = div_up((long long)n, 256);
     foe::k_log_ftilde<<<eb, 256, 0, s>>>(f, w0, n);
+    count_launch(1);
     CKL("k_log_ftilde");
     // v <- v0 / ||v0||
     foe::k_dot3<<<dim3(nblk, B), kThreads, 0, s>>>(v0, nullptr, part, nblk, HW, kPxt2);
+    count_launch(1);
     foe::k_reduce_rows<<<B, kThreads, 0, s>>>(part, nblk, 3, 3, sums);
+    count_launch(1);
     foe::k_normalize<double><<<eb, 256, 0, s>>>(v0, v, sums, 3, 2, HW, B);
+    count_launch(1);
     CKL("power-iteration init");
     st = run_k1_plain(md, w0, B, H, W, 1, epart, gw, false, nullptr, nullptr, s);
     for (int it = 0; it < power_iters && st == FOE_OK; ++it) {
         st = run_k1_plain(md, w0, B, H, W, 1, epart, h, true, v, gw, s);   // h = Hess v
         foe::k_dot3<<<dim3(nblk, B), kThreads, 0, s>>>(v, h, part, nblk, HW, kPxt2);
+        count_launch(1);
         foe::k_reduce_rows<<<B, kThreads, 0, s>>>(part, nblk, 3, 3, sums);  // <v,h>, <h,h>
         foe::k_normalize<float><<<eb, 256, 0, s>>>(h, v, sums, 3, 1, HW, B);
+        count_launch(1);
         CKL("power iteration");
     }
     std::vector<double> hs(3 * (size_t)B);
@@ -537,6 +557,7 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
     a2.nblk = st->nblk2;
     a2.HW = st->HW;
     foe::k_inertial_prox<kPxt2><<<dim3(st->nblk2, st->B), kThreads, 0, s>>>(a2);
+    count_launch(1);
     CKL("k_inertial_prox");
     const K1Args a1 = state_k1_args(st, 0);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -561,6 +582,7 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
     a3.nblk = st->nblk2;
     a3.sp = st->sp;
     foe::k_decide<<<st->B, kThreads, 0, s>>>(a3);
+    count_launch(1);
     CKL("k_decide");
     st->total_launches += 3;
     return FOE_OK;
@@ -574,7 +596,9 @@ foe_status ensure_graph(ipiano_state* st) {
     CK(cudaStreamBeginCapture(st->s, cudaStreamCaptureModeThreadLocal));
     foe_status r = FOE_OK;
     const long long tl = st->total_launches;
+    t_capturing = true;
     for (int i = 0; i < kGraphRounds && r == FOE_OK; ++i) r = launch_round(st, st->s, false);
+    t_capturing = false;
     st->total_launches = tl;
     cudaError_t e = cudaStreamEndCapture(st->s, &g);
     if (r != FOE_OK) { if (g) cudaGraphDestroy(g); return r; }
@@ -600,6 +624,7 @@ foe_status launch_rounds(ipiano_state* st, int rounds) {
     for (int i = 0; i < reps; ++i) {
         CK(cudaGraphLaunch(st->graph, st->s));
         st->total_launches += 3LL * st->graph_rounds;
+        count_launch(3LL * st->graph_rounds);
     }
     return FOE_OK;
 }
@@ -629,6 +654,44 @@ foe_status first_image_error(const ipiano_state* st) {
         }
     }
     return FOE_OK;
+}
+
+
+// a1: f~ = max(f,1), w^0 = log f~, w^{-1} = w^0, F(w^0) and grad F(w^0), trace row 0.
+foe_status state_init(ipiano_state* st, const float* f, const double* lipschitz_init, cudaStream_t user) {
+    const int B = st->B;
+    const size_t n = (size_t)B * st->HW;
+    for (int b = 0; b < B; ++b) {
+        ImgCtl& c = st->hctl[b];
+        std::memset(&c, 0, sizeof(c));
+        c.L = lipschitz_init[b];
+        c.lam1 = st->lam[2 * b];
+        c.lam2 = st->lam[2 * b + 1];
+        c.cur = 0; c.prev = 1; c.cand = 2;
+        c.gcur = 0; c.gcand = 1;
+        c.active = 1;  // for the initial evaluation
+        c.target = 0;
+    }
+    foe_status r = join_begin(st, user);
+    if (r != FOE_OK) return r;
+    CK(cudaMemcpyAsync(st->ctl, st->hctl, sizeof(ImgCtl) * B, cudaMemcpyHostToDevice, st->s));
+    if (st->cfg.record_trace)
+        CK(cudaMemsetAsync(st->trace, 0, sizeof(double) * B * (st->cfg.max_iters + 1) * 8, st->s));
+    foe::k_init<<<dim3(st->nblk2, B), kThreads, 0, st->s>>>(f, st->ft, st->w, n, st->ppart, st->nblk2, st->ctl,
+                                                             st->HW, kPxt2);
+    count_launch(1);
+    CKL("k_init");
+    const K1Args a1 = state_k1_args(st, 1);
+    k1_dispatch(st->model->m, false, a1, *st->model->tp, dim3(st->ntiles * st->groups, B), st->s);
+    CKL("k_prior_grad (init)");
+    foe::k_init_finalize<<<B, kThreads, 0, st->s>>>(st->ctl, st->epart, st->ntiles * st->groups, st->ppart,
+                                                    st->nblk2, st->trace, st->cfg.max_iters, st->cfg.record_trace);
+    count_launch(1);
+    CKL("k_init_finalize");
+    foe::k_set_target<<<div_up(B, 128), 128, 0, st->s>>>(st->ctl, B, 0);
+    count_launch(1);
+    CKL("k_set_target");
+    return join_end(st, user);
 }
 
 }  // namespace
@@ -720,35 +783,26 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     CKS(cudaMemset(st->trace, 0, sizeof(double) * B * (cfg.max_iters + 1) * 8));
     CKS(cudaMalloc((void**)&st->ctl, sizeof(ImgCtl) * B));
     CKS(cudaMallocHost((void**)&st->hctl, sizeof(ImgCtl) * B));
+    st->lam.resize(2 * (size_t)B);
     for (int b = 0; b < B; ++b) {
-        ImgCtl& c = st->hctl[b];
-        std::memset(&c, 0, sizeof(c));
-        c.L = lipschitz_init[b];
-        c.lam1 = lambda_per_image ? lambda_per_image[2 * b] : md->lam[0];
-        c.lam2 = md->term == FOE_DATA_NAKAGAMI ? 0.0 : (lambda_per_image ? lambda_per_image[2 * b + 1] : md->lam[1]);
-        c.cur = 0; c.prev = 1; c.cand = 2;
-        c.gcur = 0; c.gcand = 1;
-        c.active = 1;  // for the initial evaluation
-        c.target = 0;
+        st->lam[2 * b] = lambda_per_image ? lambda_per_image[2 * b] : md->lam[0];
+        st->lam[2 * b + 1] = md->term == FOE_DATA_NAKAGAMI ? 0.0 : (lambda_per_image ? lambda_per_image[2 * b + 1] : md->lam[1]);
     }
-    cudaStream_t user = (cudaStream_t)stream;
-    if (join_begin(st, user) != FOE_OK) return cleanup(FOE_ERR_CUDA);
-    CKS(cudaMemcpyAsync(st->ctl, st->hctl, sizeof(ImgCtl) * B, cudaMemcpyHostToDevice, st->s));
-    foe::k_init<<<dim3(st->nblk2, B), kThreads, 0, st->s>>>(f, st->ft, st->w, n, st->ppart, st->nblk2, st->ctl,
-                                                             st->HW, kPxt2);
-    CKS(cudaGetLastError());
-    const K1Args a1 = state_k1_args(st, 1);
-    k1_dispatch(md->m, false, a1, *md->tp, dim3(st->ntiles * st->groups, B), st->s);
-    CKS(cudaGetLastError());
-    foe::k_init_finalize<<<B, kThreads, 0, st->s>>>(st->ctl, st->epart, st->ntiles * st->groups, st->ppart,
-                                                    st->nblk2, st->trace, cfg.max_iters, cfg.record_trace);
-    CKS(cudaGetLastError());
-    foe::k_set_target<<<div_up(B, 128), 128, 0, st->s>>>(st->ctl, B, 0);
-    CKS(cudaGetLastError());
-    if (join_end(st, user) != FOE_OK) return cleanup(FOE_ERR_CUDA);
+    rs = state_init(st, f, lipschitz_init, (cudaStream_t)stream);
+    if (rs != FOE_OK) return cleanup(rs);
 #undef CKS
     *out = st;
     return FOE_OK;
+}
+
+foe_status ipiano_state_reset(ipiano_state* st, const float* f, const double* lipschitz_init, void* stream) {
+    if (!st) return fail(FOE_ERR_INVALID_ARGUMENT, "state is NULL");
+    if (!f || !lipschitz_init) return fail(FOE_ERR_INVALID_ARGUMENT, "f and lipschitz_init must be non-NULL");
+    for (int b = 0; b < st->B; ++b)
+        if (!(lipschitz_init[b] > 0.0) || !std::isfinite(lipschitz_init[b]))
+            return fail(FOE_ERR_INVALID_ARGUMENT, "lipschitz_init[%d]=%g must be > 0", b, lipschitz_init[b]);
+    CK(cudaSetDevice(st->model->dev));
+    return state_init(st, f, lipschitz_init, (cudaStream_t)stream);
 }
 
 foe_status ipiano_solve(ipiano_state* st, void* stream) {
@@ -758,6 +812,7 @@ foe_status ipiano_solve(ipiano_state* st, void* stream) {
     foe_status r = join_begin(st, user);
     if (r != FOE_OK) return r;
     foe::k_set_target<<<div_up(st->B, 128), 128, 0, st->s>>>(st->ctl, st->B, st->cfg.max_iters);
+    count_launch(1);
     CKL("k_set_target");
     r = sync_ctl(st);
     if (r != FOE_OK) return r;
@@ -820,17 +875,12 @@ foe_status ipiano_get_iterate(const ipiano_state* st, double* w_out, float* u_ou
     cudaStream_t user = (cudaStream_t)stream;
     foe_status r = join_begin(s, user);
     if (r != FOE_OK) return r;
-    r = sync_ctl(s);  // the current slot index lives in the control block
-    if (r != FOE_OK) return r;
-    const size_t n = (size_t)st->B * st->HW;
-    // images may sit in different slots: copy per image
-    for (int b = 0; b < st->B; ++b) {
-        const double* src = st->w + (size_t)st->hctl[b].cur * n + (size_t)b * st->HW;
-        if (w_out) CK(cudaMemcpyAsync(w_out + (size_t)b * st->HW, src, sizeof(double) * st->HW, cudaMemcpyDeviceToDevice, s->s));
-        if (u_out) {
-            foe::k_exp_out<<<div_up((long long)st->HW, 256), 256, 0, s->s>>>(src, u_out + (size_t)b * st->HW, st->HW);
-            CKL("k_exp_out");
-        }
+    if (w_out || u_out) {
+        const int gx = std::max(1, std::min(div_up((long long)st->HW, 256), 4 * st->model->nsm));
+        foe::k_iterate_out<<<dim3(gx, st->B), 256, 0, s->s>>>(st->ctl, st->w, (size_t)st->B * st->HW, w_out,
+                                                              u_out, st->HW);
+        CKL("k_iterate_out");
+        count_launch(1);
     }
     return join_end(s, user);
 }

@@ -637,9 +637,16 @@ __global__ void k_log_ftilde(const float* f, double* w, size_t n) {
     if (i < n) w[i] = log((double)fmaxf(f[i], 1.0f));
 }
 
-__global__ void k_exp_out(const double* w, float* u, size_t n) {
-    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) u[i] = (float)exp(w[i]);
+// a13: u = e^w of each image's current slot (and/or a copy of w)
+__global__ void k_iterate_out(const ImgCtl* ctl, const double* w, size_t slot_stride, double* w_out,
+                              float* u_out, size_t HW) {
+    const int b = blockIdx.y;
+    const double* src = w + (size_t)ctl[b].cur * slot_stride + (size_t)b * HW;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += (size_t)gridDim.x * blockDim.x) {
+        const double v = src[i];
+        if (w_out) w_out[(size_t)b * HW + i] = v;
+        if (u_out) u_out[(size_t)b * HW + i] = (float)exp(v);
+    }
 }
 
 }  // namespace foe

@@ -24,9 +24,9 @@ FOE_DATA_COMBINED, FOE_DATA_NAKAGAMI = 0, 1
 TRACE_FIELDS = ("F", "G", "H", "L", "trials", "margin", "newton", "relchg")
 
 EXPORTED = (
-    "foe_last_error", "foe_status_string", "foe_version", "foe_model_create", "foe_model_destroy",
+    "foe_last_error", "foe_status_string", "foe_version", "foe_kernel_launches", "foe_model_create", "foe_model_destroy",
     "foe_energy_grad", "foe_hvp", "foe_estimate_lipschitz", "ipiano_config_default",
-    "ipiano_state_create", "ipiano_step", "ipiano_solve", "ipiano_get_iterate",
+    "ipiano_state_create", "ipiano_state_reset", "ipiano_step", "ipiano_solve", "ipiano_get_iterate",
     "ipiano_get_counters", "ipiano_get_trace", "ipiano_profile", "ipiano_profile_read",
     "ipiano_state_destroy", "ipiano_run",
 )
@@ -65,6 +65,8 @@ def lib():
     L.foe_status_string.restype = C.c_char_p
     L.foe_status_string.argtypes = [C.c_int]
     L.foe_version.restype = C.c_char_p
+    L.foe_kernel_launches.restype = C.c_longlong
+    L.foe_kernel_launches.argtypes = []
     L.foe_model_create.argtypes = [_vp, C.c_int, C.c_int, _vp, _dp, C.c_double, C.c_int, C.c_int,
                                    C.POINTER(_vp)]
     L.foe_model_destroy.argtypes = [_vp]
@@ -76,6 +78,7 @@ def lib():
     L.ipiano_config_default.restype = None
     L.ipiano_state_create.argtypes = [_vp, _vp, C.c_int, C.c_int, C.c_int, _dp, _dp,
                                       C.POINTER(IPianoConfig), _vp, C.POINTER(_vp)]
+    L.ipiano_state_reset.argtypes = [_vp, _vp, _dp, _vp]
     L.ipiano_step.argtypes = [_vp, _vp, _ip]
     L.ipiano_solve.argtypes = [_vp, _vp]
     L.ipiano_get_iterate.argtypes = [_vp, _vp, _vp, _vp]
@@ -98,6 +101,19 @@ def _check(status: int):
 
 def foe_version() -> str:
     return lib().foe_version().decode()
+
+
+def foe_kernel_launches() -> int:
+    """Kernels launched by libfoe in this process (graph replays count each kernel)."""
+    return int(lib().foe_kernel_launches())
+
+
+def foe_last_error() -> str:
+    return lib().foe_last_error().decode()
+
+
+def foe_status_string(status: int) -> str:
+    return lib().foe_status_string(int(status)).decode()
 
 
 # ------------------------------------------------------------------------ marshalling
@@ -290,6 +306,14 @@ def ipiano_state_create(model: Model, f, lam_per_image=None, lipschitz_init=None
     return State(h, model, B, H, W, cfg)
 
 
+def ipiano_state_reset(state: State, f, lipschitz_init, stream=None):
+    """Re-initialise ``state`` from new device observations f (same shape), no reallocation."""
+    torch = _torch()
+    L_arr, L_p = _host_d(lipschitz_init, state.B, "lipschitz_init")
+    _check(lib().ipiano_state_reset(state.handle, _dev_ptr(f, torch.float32, "f", (state.B, state.H, state.W),
+                                                           state.model.device), L_p, _stream(stream)))
+
+
 def ipiano_step(state: State, stream=None) -> np.ndarray:
     it = np.zeros(state.B, np.int32)
     _check(lib().ipiano_step(state.handle, _stream(stream), it.ctypes.data_as(_ip)))
@@ -300,12 +324,18 @@ def ipiano_solve(state: State, stream=None):
     _check(lib().ipiano_solve(state.handle, _stream(stream)))
 
 
-def ipiano_get_iterate(state: State, want_w=True, want_u=True, stream=None):
+def ipiano_get_iterate(state: State, want_w=True, want_u=True, stream=None, w_out=None, u_out=None):
+    """Current iterate: (w fp64, u = e^w fp32) device tensors (preallocated outputs optional)."""
     torch = _torch()
     dev = torch.device("cuda", state.model.device)
     shp = (state.B, state.H, state.W)
-    w = torch.empty(shp, dtype=torch.float64, device=dev) if want_w else None
-    u = torch.empty(shp, dtype=torch.float32, device=dev) if want_u else None
+    w = w_out if w_out is not None else (torch.empty(shp, dtype=torch.float64, device=dev) if want_w else None)
+    u = u_out if u_out is not None else (torch.empty(shp, dtype=torch.float32, device=dev) if want_u else None)
+    want_w, want_u = w is not None, u is not None
+    if want_w:
+        _dev_ptr(w, torch.float64, "w_out", shp, state.model.device)
+    if want_u:
+        _dev_ptr(u, torch.float32, "u_out", shp, state.model.device)
     _check(lib().ipiano_get_iterate(state.handle, C.c_void_p(w.data_ptr()) if want_w else None,
                                     C.c_void_p(u.data_ptr()) if want_u else None, _stream(stream)))
     return w, u

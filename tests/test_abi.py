@@ -17,7 +17,8 @@ HDR = os.path.join(_lib.ROOT, "include", "foe.h")
 def _declared():
     src = open(HDR).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    names = re.findall(r"^\s*(?:const\s+)?[A-Za-z_]\w*\s*\*?\s*([a-z_][a-z0-9_]*)\s*\(", src, flags=re.M)
+    names = re.findall(r"^\s*(?:const\s+)?(?:(?:unsigned|long|short)\s+)*[A-Za-z_]\w*(?:\s+|\s*\*\s*)([a-z_][a-z0-9_]*)\s*\(",
+                       src, flags=re.M)
     return sorted(set(n for n in names if n.startswith(("foe_", "ipiano_"))))
 
 
