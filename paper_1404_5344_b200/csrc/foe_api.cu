@@ -84,12 +84,28 @@ void k1_launch(const K1Args& a, const TapParams& tp, dim3 grid, cudaStream_t s) 
     foe::k_prior_grad<M, Tr<M>::NC, SF, HVP><<<grid, kThreads, smem_bytes<M, HVP>(), s>>>(a, tp);
 }
 
-void k1_dispatch(int m, bool hvp, const K1Args& a, const TapParams& tp, dim3 grid, cudaStream_t s) {
+// K1 v2 (paired FFMA2): NCP filter pairs per shared-memory chunk, SF forward rows per item
+constexpr int kNCP = 2, kSF2 = 5;
+template <int M>
+constexpr int smem2_bytes() { return foe::G2<M, kNCP, kSF2>::SMEM_BYTES; }
+template <int M>
+cudaError_t k2g_set_attr() {
+    return cudaFuncSetAttribute(foe::k_prior_grad2<M, kNCP, kSF2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem2_bytes<M>());
+}
+template <int M>
+void k2g_launch(const K1Args& a, const foe::TapParams2& tp, dim3 grid, cudaStream_t s) {
+    foe::k_prior_grad2<M, kNCP, kSF2><<<grid, kThreads, smem2_bytes<M>(), s>>>(a, tp);
+}
+
+// hvp: the v1 stencil (setup only); gradient/energy: the v2 paired-FMA stencil
+void k1_dispatch(int m, bool hvp, const K1Args& a, const TapParams& tp, const foe::TapParams2& tp2, dim3 grid,
+                 cudaStream_t s) {
     count_launch(1);
     switch (m) {
-        case 7: hvp ? k1_launch<7, true>(a, tp, grid, s) : k1_launch<7, false>(a, tp, grid, s); break;
-        case 5: hvp ? k1_launch<5, true>(a, tp, grid, s) : k1_launch<5, false>(a, tp, grid, s); break;
-        default: hvp ? k1_launch<3, true>(a, tp, grid, s) : k1_launch<3, false>(a, tp, grid, s); break;
+        case 7: hvp ? k1_launch<7, true>(a, tp, grid, s) : k2g_launch<7>(a, tp2, grid, s); break;
+        case 5: hvp ? k1_launch<5, true>(a, tp, grid, s) : k2g_launch<5>(a, tp2, grid, s); break;
+        default: hvp ? k1_launch<3, true>(a, tp, grid, s) : k2g_launch<3>(a, tp2, grid, s); break;
     }
 }
 
@@ -105,7 +121,8 @@ struct foe_model {
     int dev = 0, nf = 0, m = 0, nsm = 148;
     foe_data_term term = FOE_DATA_COMBINED;
     double lam[2] = {0, 0};
-    TapParams* tp = nullptr;  // host copy, passed by value to K1 launches
+    TapParams* tp = nullptr;        // host copy, passed by value to the HVP stencil launches
+    foe::TapParams2* tp2 = nullptr; // pair-interleaved taps of the paired-FMA stencil
 };
 
 struct ipiano_state {
@@ -209,16 +226,18 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
                     prop.major, prop.minor);
     CK(cudaSetDevice(cuda_device));
     switch (m) {
-        case 7: CK((k1_set_attr<7, false>())); CK((k1_set_attr<7, true>())); break;
-        case 5: CK((k1_set_attr<5, false>())); CK((k1_set_attr<5, true>())); break;
-        default: CK((k1_set_attr<3, false>())); CK((k1_set_attr<3, true>())); break;
+        case 7: CK((k2g_set_attr<7>())); CK((k1_set_attr<7, true>())); break;
+        case 5: CK((k2g_set_attr<5>())); CK((k1_set_attr<5, true>())); break;
+        default: CK((k2g_set_attr<3>())); CK((k1_set_attr<3, true>())); break;
     }
 
     foe_model* md = new (std::nothrow) foe_model();
     if (!md) return fail(FOE_ERR_OUT_OF_MEMORY, "host allocation");
     md->tp = new (std::nothrow) TapParams();
-    if (!md->tp) { delete md; return fail(FOE_ERR_OUT_OF_MEMORY, "host allocation"); }
+    md->tp2 = new (std::nothrow) foe::TapParams2();
+    if (!md->tp || !md->tp2) { delete md->tp; delete md->tp2; delete md; return fail(FOE_ERR_OUT_OF_MEMORY, "host allocation"); }
     std::memset(md->tp, 0, sizeof(TapParams));
+    std::memset(md->tp2, 0, sizeof(foe::TapParams2));
     md->dev = cuda_device;
     md->nf = n_filters;
     md->m = m;
@@ -239,6 +258,16 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
             }
         md->tp->sumk[i] = (float)s;
         md->tp->theta_ln2[i] = (double)alphas[i] * 0.69314718055994530942;
+        // pair layout: filter i is lane (i & 1) of pair i/2; an odd N_f leaves a zero partner
+        const int pr = i / 2, ln = i & 1;
+        for (int t = 0; t < m * m; ++t) {
+            float* f2 = reinterpret_cast<float*>(&md->tp2->fwd[pr * m * m + t]);
+            float* b2 = reinterpret_cast<float*>(&md->tp2->bwd[pr * m * m + t]);
+            f2[ln] = md->tp->fwd[i * m * m + t];
+            b2[ln] = md->tp->bwd[i * m * m + t];
+        }
+        md->tp2->sumk[i] = md->tp->sumk[i];
+        md->tp2->theta_ln2[i] = md->tp->theta_ln2[i];
     }
     *out = md;
     return FOE_OK;
@@ -247,6 +276,7 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
 void foe_model_destroy(foe_model* model) {
     if (!model) return;
     delete model->tp;
+    delete model->tp2;
     delete model;
 }
 
@@ -321,7 +351,7 @@ foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int 
     a.v = v;
     a.gw = gw;
     dim3 grid(a.ntiles * groups, B);
-    k1_dispatch(md->m, hvp, a, *md->tp, grid, s);
+    k1_dispatch(md->m, hvp, a, *md->tp, *md->tp2, grid, s);
     CKL("k_prior_grad launch");
     return FOE_OK;
 }
@@ -566,7 +596,7 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
         e1 = pool_event(st);
         CK(cudaEventRecord(e0, s));
     }
-    k1_dispatch(st->model->m, false, a1, *st->model->tp, dim3(st->ntiles * st->groups, st->B), s);
+    k1_dispatch(st->model->m, false, a1, *st->model->tp, *st->model->tp2, dim3(st->ntiles * st->groups, st->B), s);
     CKL("k_prior_grad");
     if (timed) {
         CK(cudaEventRecord(e1, s));
@@ -682,7 +712,7 @@ foe_status state_init(ipiano_state* st, const float* f, const double* lipschitz_
     count_launch(1);
     CKL("k_init");
     const K1Args a1 = state_k1_args(st, 1);
-    k1_dispatch(st->model->m, false, a1, *st->model->tp, dim3(st->ntiles * st->groups, B), st->s);
+    k1_dispatch(st->model->m, false, a1, *st->model->tp, *st->model->tp2, dim3(st->ntiles * st->groups, B), st->s);
     CKL("k_prior_grad (init)");
     foe::k_init_finalize<<<B, kThreads, 0, st->s>>>(st->ctl, st->epart, st->ntiles * st->groups, st->ppart,
                                                     st->nblk2, st->trace, st->cfg.max_iters, st->cfg.record_trace);

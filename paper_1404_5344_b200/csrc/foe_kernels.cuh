@@ -332,6 +332,241 @@ k_prior_grad(const K1Args args, const __grid_constant__ TapParams tp) {
 }
 
 // ---------------------------------------------------------------------------------
+// K1 v2: the same fused stencil with filters processed in PAIRS so that every FMA
+// instruction is a paired fp32 FMA (FFMA2, sm_100): forward  r_(A,B) += u * (kA, kB)
+// (the input pixel is broadcast to both lanes of the pair), backward
+// s_(A,B) += (rho'_A, rho'_B) * (2 theta_A kA, 2 theta_B kB) with rho' of the pair stored
+// interleaved (float2) in shared memory.  This halves the FMA issue slots of v1, which
+// ncu showed issue-bound (82% issue active, FMA pipe 68%).
+// ---------------------------------------------------------------------------------
+constexpr int kMaxPairs = kMaxFilters / 2;
+
+struct TapParams2 {
+    float2 fwd[kMaxPairs * 49];    // (kA, kB) flipped taps of pair p (m <= 7)
+    float2 bwd[kMaxPairs * 49];    // (2 theta_A kA, 2 theta_B kB)
+    float sumk[kMaxFilters];       // sum_ab k_i (restores the DC shift), pair order (A,B) = (2p, 2p+1)
+    double theta_ln2[kMaxFilters];
+};
+
+// smallest pitch >= lo (multiple of 4 floats) with pitch*sf = 8 (mod 32): the two row
+// segments a forward quarter-warp may straddle then hit disjoint banks
+__host__ __device__ constexpr int pick_pitch_safe(int lo, int sf) {
+    int p = lo;
+    for (int k = 0; k < 8; ++k, p += 4)
+        if ((p * sf) % 32 == 8) return p;
+    return lo;
+}
+
+template <int M, int NCP, int SF>
+struct G2 {
+    static constexpr int C = (M - 1) / 2;
+    static constexpr int RX = ((kTile + 2 * C + 3) / 4) * 4;          // response cols
+    static constexpr int NSTRIP = RX / 4;
+    static constexpr int RY = ((kTile + 2 * C + SF - 1) / SF) * SF;   // response rows
+    static constexpr int NSEG = RY / SF;
+    static constexpr int ITEMS = NSTRIP * NSEG;                        // forward items per pair
+    static constexpr int NVF = (4 + M - 1 + 3) / 4;                    // float4 per forward row
+    static constexpr int UY = RY + M - 1;
+    static constexpr int UX = RX + M - 1;
+    static constexpr int UPMIN0 = (RX - 4 + 4 * NVF) > UX ? (RX - 4 + 4 * NVF) : UX;
+    static constexpr int UPMIN = ((UPMIN0 + 3) / 4) * 4;
+    static constexpr int UP = pick_pitch_safe(UPMIN, SF);
+    static constexpr int SB = 8, CWB = 2;                               // backward thread tile 8x2
+    static constexpr int NBSTRIP = kTile / CWB, NBSEG = kTile / SB;
+    static_assert(NBSTRIP * NBSEG == kThreads, "backward tiling must use every thread once");
+    static constexpr int NVB = (CWB + M - 1 + 1) / 2;                  // float4 (= 2 float2) per bwd row
+    static constexpr int PP0 = (kTile - CWB + 2 * NVB) > RX ? (kTile - CWB + 2 * NVB) : RX;
+    static constexpr int PP = PP0;                                     // rho' pitch in float2
+    static constexpr int SMEM_BYTES = UY * UP * 4 + NCP * RY * PP * 8;
+};
+
+// acc[o][x] += u[(o+a)][x+b] * (kA, kB)[a][b]   (FFMA2 with a broadcast scalar)
+template <int M, int S, int NV>
+__device__ __forceinline__ void corr_fwd2(const float* __restrict__ in, int pitch,
+                                          const float2* __restrict__ taps, float2 (&acc)[S][4]) {
+#pragma unroll
+    for (int i = 0; i < S + M - 1; ++i) {
+        float row[4 * NV];
+        const float4* rp = reinterpret_cast<const float4*>(in + i * pitch);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const float4 t = rp[v];
+            row[4 * v + 0] = t.x; row[4 * v + 1] = t.y; row[4 * v + 2] = t.z; row[4 * v + 3] = t.w;
+        }
+#pragma unroll
+        for (int a = 0; a < M; ++a) {
+            const int o = i - a;
+            if (o >= 0 && o < S) {
+#pragma unroll
+                for (int b = 0; b < M; ++b) {
+                    const float2 t = taps[a * M + b];
+#pragma unroll
+                    for (int x = 0; x < 4; ++x)
+                        acc[o][x] = __ffma2_rn(make_float2(row[x + b], row[x + b]), t, acc[o][x]);
+                }
+            }
+        }
+    }
+}
+
+// acc[o][x] += (pA, pB)[(o+a)][x+b] * (tA, tB)[a][b]   (FFMA2 on interleaved pairs)
+template <int M, int S, int NV>
+__device__ __forceinline__ void corr_bwd2(const float2* __restrict__ in, int pitch2,
+                                          const float2* __restrict__ taps, float2 (&acc)[S][2]) {
+#pragma unroll
+    for (int i = 0; i < S + M - 1; ++i) {
+        float2 row[2 * NV];
+        const float4* rp = reinterpret_cast<const float4*>(in + i * pitch2);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const float4 t = rp[v];
+            row[2 * v + 0] = make_float2(t.x, t.y);
+            row[2 * v + 1] = make_float2(t.z, t.w);
+        }
+#pragma unroll
+        for (int a = 0; a < M; ++a) {
+            const int o = i - a;
+            if (o >= 0 && o < S) {
+#pragma unroll
+                for (int b = 0; b < M; ++b) {
+                    const float2 t = taps[a * M + b];
+#pragma unroll
+                    for (int x = 0; x < 2; ++x) acc[o][x] = __ffma2_rn(row[x + b], t, acc[o][x]);
+                }
+            }
+        }
+    }
+}
+
+template <int M, int NCP, int SF>
+__global__ void __launch_bounds__(kThreads, 2)
+k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
+    using G = G2<M, NCP, SF>;
+    constexpr int C = G::C;
+    extern __shared__ float4 smem4[];
+    float* us = reinterpret_cast<float*>(smem4);                          // [UY][UP]  u - c
+    float2* ps = reinterpret_cast<float2*>(us + G::UY * G::UP);          // [NCP][RY][PP] (rho'_A, rho'_B)/2
+    __shared__ double red[32];
+
+    const int b = blockIdx.y;
+    int wslot = 0, gslot = 0;
+    if (args.ctl != nullptr) {
+        const ImgCtl& c = args.ctl[b];
+        if (!c.active) return;
+        wslot = args.which_cur ? c.cur : c.cand;
+        gslot = args.which_cur ? c.gcur : c.gcand;
+    }
+    const int H = args.H, W = args.W;
+    const size_t HW = (size_t)H * W;
+    const int tile = blockIdx.x / args.groups, grp = blockIdx.x - tile * args.groups;
+    const int ty = tile / args.tiles_x, tx = tile - ty * args.tiles_x;
+    const int y0 = ty * kTile, x0 = tx * kTile;
+    const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
+    const int npairs = (args.nf + 1) / 2;
+    const int ck0 = (grp * args.nchunks) / args.groups;
+    const int ck1 = ((grp + 1) * args.nchunks) / args.groups;
+
+    // (a2) stage u - c on the tile + 2C halo (fp64 exp, one rounding to fp32)
+    const int yc = wrap_idx(y0 + kTile / 2, H), xc = wrap_idx(x0 + kTile / 2, W);
+    const float cst = (float)exp(w[(size_t)yc * W + xc]);
+    const double cstd = (double)cst;
+    for (int idx = threadIdx.x; idx < G::UY * G::UX; idx += kThreads) {
+        const int uy = idx / G::UX, ux = idx - uy * G::UX;
+        const int gy = wrap_idx(y0 - 2 * C + uy, H), gx = wrap_idx(x0 - 2 * C + ux, W);
+        us[uy * G::UP + ux] = (float)(exp(w[(size_t)gy * W + gx]) - cstd);
+    }
+    __syncthreads();
+
+    // fixed forward item of this thread (one per filter pair) and its energy weights
+    const int tid = threadIdx.x;
+    const bool fwd_on = tid < G::ITEMS;
+    const int fseg = tid / G::NSTRIP, fstrip = tid - fseg * G::NSTRIP;
+    float cw[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+        const int tcx = fstrip * 4 + x - C;
+        cw[x] = (tcx >= 0 && tcx < kTile && x0 + tcx < W) ? 1.f : 0.f;
+    }
+    float rw[SF];
+#pragma unroll
+    for (int o = 0; o < SF; ++o) {
+        const int tcy = fseg * SF + o - C;
+        rw[o] = (tcy >= 0 && tcy < kTile && y0 + tcy < H) ? 1.f : 0.f;
+    }
+    const int bstrip = tid % G::NBSTRIP, bseg = tid / G::NBSTRIP;
+    float2 bacc[G::SB][G::CWB];
+#pragma unroll
+    for (int o = 0; o < G::SB; ++o)
+#pragma unroll
+        for (int x = 0; x < G::CWB; ++x) bacc[o][x] = make_float2(0.f, 0.f);
+    double e_acc = 0.0;
+
+    for (int ck = ck0; ck < ck1; ++ck) {
+        const int pbase = ck * NCP;
+        const int ncp = min(NCP, npairs - pbase);
+        // (a3, a4, a7) forward responses of each pair, rho for the energy, rho' to smem
+        for (int p = 0; p < ncp; ++p) {
+            const int pi = pbase + p;
+            if (fwd_on) {
+                float2 r[SF][4];
+#pragma unroll
+                for (int o = 0; o < SF; ++o)
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) r[o][x] = make_float2(0.f, 0.f);
+                corr_fwd2<M, SF, G::NVF>(us + fseg * SF * G::UP + fstrip * 4, G::UP, &tp.fwd[pi * M * M], r);
+                const float2 cs = make_float2(cst * tp.sumk[2 * pi], cst * tp.sumk[2 * pi + 1]);
+                float2 el = make_float2(0.f, 0.f);
+                float2* pdst = ps + (size_t)p * G::RY * G::PP + (size_t)(fseg * SF) * G::PP + fstrip * 4;
+#pragma unroll
+                for (int o = 0; o < SF; ++o) {
+                    float2 q[4];
+#pragma unroll
+                    for (int x = 0; x < 4; ++x) {
+                        const float2 rv = __fadd2_rn(r[o][x], cs);
+                        const float2 d = __ffma2_rn(rv, rv, make_float2(1.f, 1.f));
+                        const float2 lg = make_float2(__log2f(d.x), __log2f(d.y));
+                        const float wgt = rw[o] * cw[x];
+                        el = __ffma2_rn(lg, make_float2(wgt, wgt), el);
+                        q[x] = __fmul2_rn(rv, make_float2(__fdividef(1.f, d.x), __fdividef(1.f, d.y)));
+                    }
+                    float4* dst = reinterpret_cast<float4*>(pdst + o * G::PP);
+                    dst[0] = make_float4(q[0].x, q[0].y, q[1].x, q[1].y);
+                    dst[1] = make_float4(q[2].x, q[2].y, q[3].x, q[3].y);
+                }
+                e_acc += tp.theta_ln2[2 * pi] * (double)el.x + tp.theta_ln2[2 * pi + 1] * (double)el.y;
+            }
+        }
+        __syncthreads();
+        // (a5) transposed correlations of the chunk's pairs, summed in registers
+        for (int p = 0; p < ncp; ++p) {
+            corr_bwd2<M, G::SB, G::NVB>(ps + (size_t)p * G::RY * G::PP + (size_t)(bseg * G::SB) * G::PP + bstrip * G::CWB,
+                                        G::PP, &tp.bwd[(pbase + p) * M * M], bacc);
+        }
+        __syncthreads();
+    }
+
+    // (a6) g = u (.) (s_A + s_B) on owned pixels
+    float* gout = args.g + (size_t)gslot * args.g_slot_stride + (size_t)grp * args.g_group_stride +
+                  (size_t)b * HW;
+#pragma unroll
+    for (int o = 0; o < G::SB; ++o) {
+        const int oy = bseg * G::SB + o;
+        const int gy = y0 + oy;
+        if (gy >= H) continue;
+#pragma unroll
+        for (int x = 0; x < G::CWB; ++x) {
+            const int ox = bstrip * G::CWB + x;
+            const int gx = x0 + ox;
+            if (gx >= W) continue;
+            const float u = us[(oy + 2 * C) * G::UP + ox + 2 * C] + cst;
+            gout[(size_t)gy * W + gx] = u * (bacc[o][x].x + bacc[o][x].y);
+        }
+    }
+    const double e = block_sum_d(e_acc, red);
+    if (threadIdx.x == 0) args.epart[(size_t)b * args.ntiles * args.groups + blockIdx.x] = e;
+}
+
+// ---------------------------------------------------------------------------------
 // K2: inertial forward point + Newton prox of Eq.(10) + block partials of the test.
 // ---------------------------------------------------------------------------------
 
