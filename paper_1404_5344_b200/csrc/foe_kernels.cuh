@@ -74,6 +74,18 @@ struct K1Args {
     const float* gw;        // [B][H][W] gradient at w
 };
 
+// raw MUFU approximations (argument d = 1 + r^2 >= 1: no denormal/range guards needed)
+__device__ __forceinline__ float lg2_approx(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ int wrap_idx(int i, int n) {
     int r = i % n;
     return r < 0 ? r + n : r;
@@ -481,17 +493,17 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
     const int tid = threadIdx.x;
     const bool fwd_on = tid < G::ITEMS;
     const int fseg = tid / G::NSTRIP, fstrip = tid - fseg * G::NSTRIP;
-    float cw[4];
-#pragma unroll
-    for (int x = 0; x < 4; ++x) {
-        const int tcx = fstrip * 4 + x - C;
-        cw[x] = (tcx >= 0 && tcx < kTile && x0 + tcx < W) ? 1.f : 0.f;
-    }
-    float rw[SF];
+    static_assert(SF * 4 <= 32, "ownership mask is 32 bits");
+    unsigned own = 0u;   // bit o*4+x: response (o,x) of this item is owned by the tile (energy)
 #pragma unroll
     for (int o = 0; o < SF; ++o) {
         const int tcy = fseg * SF + o - C;
-        rw[o] = (tcy >= 0 && tcy < kTile && y0 + tcy < H) ? 1.f : 0.f;
+        const bool rok = tcy >= 0 && tcy < kTile && y0 + tcy < H;
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+            const int tcx = fstrip * 4 + x - C;
+            if (rok && tcx >= 0 && tcx < kTile && x0 + tcx < W) own |= 1u << (o * 4 + x);
+        }
     }
     const int bstrip = tid % G::NBSTRIP, bseg = tid / G::NBSTRIP;
     float2 bacc[G::SB][G::CWB];
@@ -508,13 +520,14 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
         for (int p = 0; p < ncp; ++p) {
             const int pi = pbase + p;
             if (fwd_on) {
+                // r = c sum(k) + K(u - c): the DC restore is the accumulator's initial value
+                const float2 cs = make_float2(cst * tp.sumk[2 * pi], cst * tp.sumk[2 * pi + 1]);
                 float2 r[SF][4];
 #pragma unroll
                 for (int o = 0; o < SF; ++o)
 #pragma unroll
-                    for (int x = 0; x < 4; ++x) r[o][x] = make_float2(0.f, 0.f);
+                    for (int x = 0; x < 4; ++x) r[o][x] = cs;
                 corr_fwd2<M, SF, G::NVF>(us + fseg * SF * G::UP + fstrip * 4, G::UP, &tp.fwd[pi * M * M], r);
-                const float2 cs = make_float2(cst * tp.sumk[2 * pi], cst * tp.sumk[2 * pi + 1]);
                 float2 el = make_float2(0.f, 0.f);
                 float2* pdst = ps + (size_t)p * G::RY * G::PP + (size_t)(fseg * SF) * G::PP + fstrip * 4;
 #pragma unroll
@@ -522,12 +535,11 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
                     float2 q[4];
 #pragma unroll
                     for (int x = 0; x < 4; ++x) {
-                        const float2 rv = __fadd2_rn(r[o][x], cs);
+                        const float2 rv = r[o][x];
                         const float2 d = __ffma2_rn(rv, rv, make_float2(1.f, 1.f));
-                        const float2 lg = make_float2(__log2f(d.x), __log2f(d.y));
-                        const float wgt = rw[o] * cw[x];
-                        el = __ffma2_rn(lg, make_float2(wgt, wgt), el);
-                        q[x] = __fmul2_rn(rv, make_float2(__fdividef(1.f, d.x), __fdividef(1.f, d.y)));
+                        const float2 lg = make_float2(lg2_approx(d.x), lg2_approx(d.y));
+                        if (own & (1u << (o * 4 + x))) el = __fadd2_rn(el, lg);   // owned responses only
+                        q[x] = __fmul2_rn(rv, make_float2(rcp_approx(d.x), rcp_approx(d.y)));
                     }
                     float4* dst = reinterpret_cast<float4*>(pdst + o * G::PP);
                     dst[0] = make_float4(q[0].x, q[0].y, q[1].x, q[1].y);
@@ -570,27 +582,55 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
 // K2: inertial forward point + Newton prox of Eq.(10) + block partials of the test.
 // ---------------------------------------------------------------------------------
 
-// Root of phi(z) = z - what + tau [l1 (1 - f^2 e^{-2z}) + l2 (e^{2z} - f^2)]:
-// Newton from what, bisection safeguard on [min(what, log f) - 1, max(what, log f) + 1]
-// (SPEC.md:248), |phi| <= tol.  Returns Newton updates, or -1 past the cap.
+// e^x for |x| <= 1/16: Taylor polynomial of degree 10 (remainder < 1e-20 relative)
+__device__ __forceinline__ double exp_small(double x) {
+    double p = 2.7557319223985893e-07;            // 1/10!
+    p = fma(p, x, 2.7557319223985888e-06);        // 1/9!
+    p = fma(p, x, 2.4801587301587302e-05);        // 1/8!
+    p = fma(p, x, 1.9841269841269841e-04);        // 1/7!
+    p = fma(p, x, 1.3888888888888889e-03);        // 1/6!
+    p = fma(p, x, 8.3333333333333332e-03);        // 1/5!
+    p = fma(p, x, 4.1666666666666664e-02);        // 1/4!
+    p = fma(p, x, 1.6666666666666666e-01);        // 1/3!
+    p = fma(p, x, 0.5);
+    p = fma(p, x, 1.0);
+    return fma(p, x, 1.0);
+}
+
+// Root of phi(z) = z - what + tau [l1 (1 - f^2 e^{-2z}) + l2 (e^{2z} - f^2)],
+// solved for the increment d = z - what:
+//   phi(d) = d + tau(l1 - l2 f^2) - A e^{-2d} + Bc e^{2d},  A = tau l1 f^2 e^{-2 what},
+//   Bc = tau l2 e^{2 what},  phi'(d) = 1 + 2 A e^{-2d} + 2 Bc e^{2d} > 0,
+// so e^{+-2 what} are computed once per pixel and e^{+-2d} (|d| small) by a polynomial.
+// Newton from d = 0 with bisection on the bracket [min(0, log f - what) - 1,
+// max(0, log f - what) + 1] (log f only needs to be approximate: the +-1
+// widening keeps the bracket valid), stopping at |phi| <= tol.
+// Returns the Newton updates, or -1 past the cap; em_out = e^{-2z}, ep_out = e^{2z}.
 __device__ __forceinline__ int prox_newton(double what, double ft, double tau, double l1,
                                            double l2, double tol, int cap, double& z_out,
                                            double& em_out, double& ep_out) {
-    const double lf = log(ft), f2 = ft * ft;
-    double lo = fmin(what, lf) - 1.0, hi = fmax(what, lf) + 1.0;
-    double z = what;
+    const double f2 = ft * ft;
+    const double Em = exp(-2.0 * what);
+    const double Ep = 1.0 / Em;
+    const double A = tau * l1 * f2 * Em, Bc = tau * l2 * Ep, c0 = tau * (l1 - l2 * f2);
+    const double lfw = (double)__logf((float)ft) - what;
+    double lo = fmin(0.0, lfw) - 1.0, hi = fmax(0.0, lfw) + 1.0;
+    double d = 0.0;
     for (int it = 0; it <= cap; ++it) {
-        const double em = exp(-2.0 * z), ep = exp(2.0 * z);
-        const double phi = z - what + tau * (l1 * (1.0 - f2 * em) + l2 * (ep - f2));
-        if (fabs(phi) <= tol) { z_out = z; em_out = em; ep_out = ep; return it; }
-        if (phi > 0.0) hi = z; else lo = z;
-        const double dphi = 1.0 + tau * (2.0 * l1 * f2 * em + 2.0 * l2 * ep);
-        double zn = z - phi / dphi;
-        if (!(zn > lo && zn < hi)) zn = 0.5 * (lo + hi);
-        if (zn == z) { z_out = z; em_out = em; ep_out = ep; return it; }
-        z = zn;
+        const double x = 2.0 * d;
+        double ep2, em2;
+        if (fabs(x) <= 0.0625) { ep2 = exp_small(x); em2 = exp_small(-x); }
+        else { ep2 = exp(x); em2 = exp(-x); }
+        const double phi = d + c0 - A * em2 + Bc * ep2;
+        if (fabs(phi) <= tol) { z_out = what + d; em_out = Em * em2; ep_out = Ep * ep2; return it; }
+        if (phi > 0.0) hi = d; else lo = d;
+        const double dphi = 1.0 + 2.0 * (A * em2 + Bc * ep2);
+        double dn = d - phi / dphi;
+        if (!(dn > lo && dn < hi)) dn = 0.5 * (lo + hi);
+        if (dn == d) { z_out = what + d; em_out = Em * em2; ep_out = Ep * ep2; return it; }
+        d = dn;
     }
-    z_out = z; em_out = exp(-2.0 * z); ep_out = exp(2.0 * z);
+    z_out = what + d; em_out = exp(-2.0 * z_out); ep_out = exp(2.0 * z_out);
     return -1;
 }
 
