@@ -596,16 +596,19 @@ __device__ __forceinline__ double exp_small(double x) {
     p = fma(p, x, 1.0);
     return fma(p, x, 1.0);
 }
+__device__ __forceinline__ double exp_near0(double x) { return fabs(x) <= 0.0625 ? exp_small(x) : exp(x); }
 
 // Root of phi(z) = z - what + tau [l1 (1 - f^2 e^{-2z}) + l2 (e^{2z} - f^2)],
 // solved for the increment d = z - what:
 //   phi(d) = d + tau(l1 - l2 f^2) - A e^{-2d} + Bc e^{2d},  A = tau l1 f^2 e^{-2 what},
 //   Bc = tau l2 e^{2 what},  phi'(d) = 1 + 2 A e^{-2d} + 2 Bc e^{2d} > 0,
-// so e^{+-2 what} are computed once per pixel and e^{+-2d} (|d| small) by a polynomial.
-// Newton from d = 0 with bisection on the bracket [min(0, log f - what) - 1,
-// max(0, log f - what) + 1] (log f only needs to be approximate: the +-1
-// widening keeps the bracket valid), stopping at |phi| <= tol.
-// Returns the Newton updates, or -1 past the cap; em_out = e^{-2z}, ep_out = e^{2z}.
+//   |phi''(d)| <= 4 (A e^{-2d} + Bc e^{2d}) = 2 (phi'(d) - 1).
+// Newton's method from d = 0: the first step needs no exponential; at d1 one fp64
+// evaluation gives the second step st, and the Newton error bound |phi(d1 - st)| <~
+// |phi''|/2 st^2 <= (phi' - 1) st^2 accepts d2 = d1 - st when that bound is <= tol/4.  Otherwise
+// (large steps, overflow) the safeguarded fp64 Newton/bisection iteration on the bracket
+// [min(0, log f - what) - 1, max(0, log f - what) + 1] runs to |phi| <= tol
+// (SPEC.md:251).  Returns the Newton updates, or -1 past the cap; em_out = e^{-2z}, ep_out = e^{2z}.
 __device__ __forceinline__ int prox_newton(double what, double ft, double tau, double l1,
                                            double l2, double tol, int cap, double& z_out,
                                            double& em_out, double& ep_out) {
@@ -613,14 +616,31 @@ __device__ __forceinline__ int prox_newton(double what, double ft, double tau, d
     const double Em = exp(-2.0 * what);
     const double Ep = 1.0 / Em;
     const double A = tau * l1 * f2 * Em, Bc = tau * l2 * Ep, c0 = tau * (l1 - l2 * f2);
+    {
+        const double phi0 = c0 - A + Bc;
+        if (fabs(phi0) <= tol) { z_out = what; em_out = Em; ep_out = Ep; return 0; }
+        const double d1 = -phi0 / (1.0 + 2.0 * (A + Bc));
+        if (fabs(d1) <= 0.03125) {
+            const double ep2 = exp_small(2.0 * d1), em2 = exp_small(-2.0 * d1);
+            const double phi = d1 + c0 - A * em2 + Bc * ep2;
+            if (fabs(phi) <= tol) { z_out = what + d1; em_out = Em * em2; ep_out = Ep * ep2; return 1; }
+            const double dphi = 1.0 + 2.0 * (A * em2 + Bc * ep2);
+            const double st = phi / dphi;
+            if ((dphi - 1.0) * st * st <= 0.25 * tol && fabs(st) <= 1e-6) {
+                const double e = -2.0 * st;                              // e^{+-e}, |e| <= 2e-6
+                z_out = what + (d1 - st);
+                ep_out = Ep * ep2 * fma(0.5 * e, e, 1.0 + e);
+                em_out = Em * em2 * fma(0.5 * e, e, 1.0 - e);
+                return 2;
+            }
+        }
+    }
     const double lfw = (double)__logf((float)ft) - what;
     double lo = fmin(0.0, lfw) - 1.0, hi = fmax(0.0, lfw) + 1.0;
     double d = 0.0;
     for (int it = 0; it <= cap; ++it) {
         const double x = 2.0 * d;
-        double ep2, em2;
-        if (fabs(x) <= 0.0625) { ep2 = exp_small(x); em2 = exp_small(-x); }
-        else { ep2 = exp(x); em2 = exp(-x); }
+        const double ep2 = exp_near0(x), em2 = exp_near0(-x);
         const double phi = d + c0 - A * em2 + Bc * ep2;
         if (fabs(phi) <= tol) { z_out = what + d; em_out = Em * em2; ep_out = Ep * ep2; return it; }
         if (phi > 0.0) hi = d; else lo = d;
