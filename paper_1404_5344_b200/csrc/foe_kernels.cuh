@@ -668,9 +668,8 @@ struct K2Args {
 };
 
 template <int PXT>
-__global__ void __launch_bounds__(kThreads)
-k_inertial_prox(const K2Args a) {
-    __shared__ double red[32];
+__global__ void __launch_bounds__(kThreads, 3)
+k_inertial_prox(const K2Args a) {  // (3 CTAs/SM: <= 80 registers)
     const int b = blockIdx.y;
     const ImgCtl& c = a.ctl[b];
     if (!c.active) return;
@@ -706,16 +705,27 @@ k_inertial_prox(const K2Args a) {
         if (it < 0) fail += 1.0; else nit = fmax(nit, (double)it);
         if (!(z == z)) wmax = INFINITY;
     }
-    double* out = a.ppart + ((size_t)b * a.nblk + blockIdx.x) * kNumPart;
-    const double s0 = block_sum_d(gd, red);
-    const double s1 = block_sum_d(dd, red);
-    const double s2 = block_sum_d(Gp, red);
-    const double s3 = block_sum_d(ww, red);
-    const double s4 = block_max_d(wmax, red);
-    const double s5 = block_max_d(nit, red);
-    const double s6 = block_sum_d(fail, red);
-    if (threadIdx.x == 0) {
-        out[0] = s0; out[1] = s1; out[2] = s2; out[3] = s3; out[4] = s4; out[5] = s5; out[6] = s6; out[7] = 0.0;
+    // one fixed-order block reduction of the 7 partials (sums, except slots 4/5 = max)
+    double v[7] = {gd, dd, Gp, ww, wmax, nit, fail};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+            const double t = __shfl_xor_sync(0xffffffffu, v[k], o);
+            v[k] = (k == 4 || k == 5) ? fmax(v[k], t) : v[k] + t;
+        }
+    __shared__ double wred[kThreads / 32][8];
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int k = 0; k < 7; ++k) wred[threadIdx.x >> 5][k] = v[k];
+    __syncthreads();
+    if (threadIdx.x < 7) {
+        const int k = threadIdx.x;
+        double t = wred[0][k];
+        for (int i = 1; i < kThreads / 32; ++i) t = (k == 4 || k == 5) ? fmax(t, wred[i][k]) : t + wred[i][k];
+        double* out = a.ppart + ((size_t)b * a.nblk + blockIdx.x) * kNumPart;
+        out[k] = t;
+        if (k == 0) out[7] = 0.0;
     }
 }
 
