@@ -1,0 +1,76 @@
+#!/usr/bin/env python
+"""Summarise ncu output for profiles/ (run here, on the CPU box, on files gpurun brought back).
+
+    python tools/ncu_summary.py launches <launches.csv>        # per-kernel share of device time
+    python tools/ncu_summary.py report <file.ncu-rep> [...]     # key counters of a --set full capture
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    "gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum",
+    "smsp__sass_thread_inst_executed_op_ffma_pred_on.sum",
+    "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
+    "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic", "launch__grid_size",
+    "launch__occupancy_limit_registers", "sm__maximum_warps_per_active_cycle_pct",
+]
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    h = rows[start]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[start + 1:]:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0].replace("void ", "")
+        scale = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0}.get(r[ui], 1e-6)
+        agg[name][0] += 1
+        agg[name][1] += float(r[vi].replace(",", "")) * scale
+    tot = sum(v[1] for v in agg.values())
+    print("| kernel | launches | total ms | ms/launch | share |")
+    print("|---|---:|---:|---:|---:|")
+    for k, (n, ms) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"| `{k}` | {n} | {ms:.2f} | {ms / n:.4f} | {ms / tot:.3f} |")
+    print(f"\ntotal {tot:.1f} ms over {sum(v[0] for v in agg.values())} launches (serialised, cold cache)")
+
+
+def report(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, u = rows[0], rows[1]
+    for v in rows[2:]:
+        d = dict(zip(h, zip(u, v)))
+        print(f"### `{d.get('Kernel Name', ('', '?'))[1][:120]}`\n")
+        print("| metric | unit | value |")
+        print("|---|---|---:|")
+        for k in KEYS:
+            if k in d:
+                print(f"| {k} | {d[k][0]} | {d[k][1]} |")
+        print()
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2])
+    else:
+        for p in sys.argv[2:]:
+            report(p)
