@@ -202,6 +202,8 @@ def main():
         cfg = S.config(args.config, iters=args.iters)
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if cfg.name == "c5":
+        return run_slabs(args, cfg)
 
     import torch
     import paper_1404_5344_b200 as P
@@ -341,6 +343,114 @@ def main():
         }
         print(json.dumps(line), flush=True)
     st.destroy()
+    md.destroy()
+    D.barrier()
+    return 0
+
+
+def run_slabs(args, cfg):
+    """c5 (BASELINE.json configs[4]): one 8192^2 scene cut into N row slabs, one per GPU, with
+    the per-trial 6-row ghost exchange and band-partial all-gather over NCCL (strong scaling:
+    the scene is fixed).  A step = reset from f + `iters` iterations."""
+    import torch
+    import foe_synth as S
+    import paper_1404_5344_b200 as P
+    from paper_1404_5344_b200 import dist as D
+
+    rank, ws, local = D.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    d = S.make_inputs(cfg)
+    f_full = d["f"][0]
+    Hg, W = f_full.shape
+    r0, r1 = D.slab_rows(Hg, ws, rank)
+    lam = tuple(d["lambdas"][0])
+    md = P.foe_model_create(d["filters"], d["theta"], lam=lam, device=local)
+    # setup: L_init (R-10) on the whole scene, identical on every rank (deterministic kernels)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    fw = torch.as_tensor(f_full[None], device=dev)
+    v0 = torch.as_tensor(S.lipschitz_start_vector(1, Hg, W), device=dev)
+    rho, L0 = P.foe_estimate_lipschitz(md, fw, v0, 25)
+    lipschitz_ms = 1e3 * (time.perf_counter() - t0)
+    del fw, v0
+    L0 = float(L0[0])
+    comm = P.foe_comm_create(D.share_bytes(P.foe_comm_unique_id() if rank == 0 else None), ws, rank, local)
+    f_dev = torch.as_tensor(np.ascontiguousarray(f_full[r0:r1]), device=dev)
+    cfgc = P.ipiano_config_default(max_iters=cfg.iters, record_trace=0)
+    sl = P.ipiano_slabs_create(md, f_dev, Hg, lam=lam, lipschitz_init=L0, cfg=cfgc, comm=comm)
+    member = P.ipiano_slabs_member(sl, 0)
+    u_dev = torch.empty((r1 - r0, W), dtype=torch.float32, device=dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        P.ipiano_slabs_reset(sl, f_dev, L0)
+        P.ipiano_slabs_solve(sl)
+        P.ipiano_slabs_get_iterate(sl, want_w=False, u_out=u_dev)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    P.ipiano_profile(member, True)
+    P.ipiano_profile_read(member)
+    sampler = ClockSampler(smi_index(local)) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    D.barrier()
+    torch.cuda.synchronize()
+    launches0 = P.foe_kernel_launches()
+    step_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    launches = P.foe_kernel_launches() - launches0
+    D.barrier()
+    clocks = sampler.stop() if sampler else None
+    k1_ms, k1_launches, _ = P.ipiano_profile_read(member)
+    cnt = P.ipiano_get_counters(member)
+    total_ms = D.max_over_ranks(sum(step_ms), dev)
+    mp_it_total = Hg * W * cfg.iters * args.steps / 1e6
+    value = mp_it_total / (total_ms / 1e3)
+    trials_per_step = float(cnt["trials"][0])
+    flops_px = 4.0 * cfg.n_filters * cfg.m * cfg.m
+    k1_flops = flops_px * (r1 - r0) * W * trials_per_step * args.steps
+    k1_tflops = k1_flops / (k1_ms / 1e3) / 1e12 if k1_ms > 0 else None
+    peaks, peak_src = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak = nsm * 128 * 2 * sm_max * 1e6 / 1e12
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "dtype_detail": "fp32 stencil (FFMA), fp64 iterate/prox/reductions", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: {cfg.description}", "H": Hg, "W": W,
+                       "filters": f"{cfg.n_filters}x{cfg.m}x{cfg.m}", "iters": cfg.iters,
+                       "slab_rows_per_gpu": r1 - r0,
+                       "l2": "inputs (8192^2 fp64 state, 1.6 GB) larger than L2; 256 MiB flush between steps",
+                       "parallelism": f"row slabs x{ws}: 6-row ghost exchange (ncclSend/Recv) + band all-gather per trial"},
+            "roofline": {"bound": "alu", "achieved": k1_tflops, "peak": fp32_peak, "unit": "TFLOP/s",
+                         "frac": (k1_tflops / fp32_peak) if k1_tflops else None, "traffic": args.traffic_bytes,
+                         "kernel": "k_prior_grad2 (K1, slab)",
+                         "peak_source": f"derived: {nsm} SMs x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz ({peak_src})",
+                         "k1_ms_per_launch": k1_ms / max(k1_launches, 1), "k1_launches": k1_launches,
+                         "k1_share_of_step": k1_ms / sum(step_ms) if step_ms else None},
+            "cpu_baseline": None, "e2e": None, "gpu_launches": int(launches), "clocks": clocks,
+            "trials_per_iter": trials_per_step / cfg.iters, "lipschitz_ms": lipschitz_ms,
+            "status": [int(cnt["status"][0])],
+        }
+        print(json.dumps(line), flush=True)
+    sl.destroy()
+    comm.destroy()
     md.destroy()
     D.barrier()
     return 0

@@ -222,6 +222,57 @@ foe_status ipiano_run(const foe_model* model, const float* f, int B, int H, int 
                       const ipiano_config* cfg, float* u_out, void* trace, size_t trace_bytes,
                       void* stream);
 
+/* ------------------------------------------------------------------ row slabs (multi-GPU) */
+
+/* One periodic scene split into equal row slabs (BASELINE.json configs[4]):
+ * per backtracking trial every slab computes w+ on its rows (K2), exchanges kHalo = 6 ghost
+ * rows (= m-1 for m <= 7: the energy needs +-3 rows, the gradient +-6) with its two ring
+ * neighbours, evaluates F and grad F on its rows (K1), and all slabs combine per-64-row-band
+ * partials of the test into one global array in a fixed order, so every slab takes the same
+ * decision and the result is bitwise independent of the number of slabs. */
+typedef struct foe_comm foe_comm;
+
+/* NCCL unique id (128 bytes) for foe_comm_create; call on one rank and broadcast the bytes
+ * (e.g. with torch.distributed).  libnccl.so.2 is resolved at run time (the copy already
+ * loaded by the process, else the system one); FOE_ERR_COMM if it cannot be loaded. */
+foe_status foe_comm_unique_id(void* id_out);
+/* Creates this rank's NCCL communicator (one process per GPU; collective over the nranks
+ * processes).  cuda_device must be the device of the models used with it. */
+foe_status foe_comm_create(const void* id, int nranks, int rank, int cuda_device, foe_comm** out);
+void foe_comm_destroy(foe_comm* comm);
+
+typedef struct ipiano_slabs ipiano_slabs;
+
+/* Creates the slab decomposition of ONE scene of H_global x W pixels and initialises it
+ * (a1 on every slab, ghost rows exchanged, F(w^0), grad F(w^0)).
+ *   comm == NULL: all `nslabs` slabs live in this process on the model's device (ghost rows
+ *       and band partials move by device copies); f = the whole scene, device fp32
+ *       [H_global][W].
+ *   comm != NULL: this process owns slab comm->rank only (nslabs is taken from comm);
+ *       f = that slab, device fp32 [H_global/nranks][W] = scene rows
+ *       [rank H_global/nranks, (rank+1) H_global/nranks).
+ *   lambda        host fp64 [2] or NULL (-> the model's)
+ *   lipschitz_init  L_0 > 0, identical on every rank
+ * Requires H_global a multiple of 64 * nslabs (whole 64-row bands per slab), W a multiple
+ * of 32.  Errors: FOE_ERR_INVALID_ARGUMENT, FOE_ERR_CUDA, FOE_ERR_OUT_OF_MEMORY,
+ * FOE_ERR_COMM (NCCL failure). */
+foe_status ipiano_slabs_create(const foe_model* model, const float* f, int H_global, int W, int nslabs,
+                               const double* lambda, double lipschitz_init, const ipiano_config* cfg,
+                               const foe_comm* comm, void* stream, ipiano_slabs** out);
+/* Re-initialises from new observations f (same layout as in create). */
+foe_status ipiano_slabs_reset(ipiano_slabs* slabs, const float* f, double lipschitz_init, void* stream);
+/* Runs max_iters accepted iterations (all ranks must call it; trial rounds in CUDA-graph
+ * chunks, one host synchronisation per chunk).  FOE_ERR_COMM if slabs disagree. */
+foe_status ipiano_slabs_solve(ipiano_slabs* slabs, void* stream);
+/* u = e^w (and/or w) of the slabs owned by this process: the whole scene when comm == NULL,
+ * this rank's slab otherwise (device, [rows][W]). */
+foe_status ipiano_slabs_get_iterate(const ipiano_slabs* slabs, double* w_out, float* u_out, void* stream);
+/* The per-slab iPiano state j of this process (for ipiano_get_counters / ipiano_get_trace /
+ * ipiano_profile / ipiano_profile_read; every slab holds the same control block and trace).
+ * The returned state is owned by `slabs`: do not destroy it. */
+foe_status ipiano_slabs_member(const ipiano_slabs* slabs, int j, ipiano_state** out);
+void ipiano_slabs_destroy(ipiano_slabs* slabs);
+
 #ifdef __cplusplus
 }
 #endif

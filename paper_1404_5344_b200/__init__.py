@@ -6,9 +6,9 @@ only for device memory, streams and torch.distributed process groups.
 """
 from . import _lib
 from .foe import *  # noqa: F401,F403
-from .foe import EXPORTED, FoeError, IPianoConfig, Model, State, lib
+from .foe import EXPORTED, Comm, FoeError, IPianoConfig, Model, Slabs, State, lib
 
-__all__ = list(EXPORTED) + ["FoeError", "IPianoConfig", "Model", "State", "lib", "build"]
+__all__ = list(EXPORTED) + ["Comm", "FoeError", "IPianoConfig", "Model", "Slabs", "State", "lib", "build"]
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

@@ -610,6 +610,7 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
     a3.trace = st->trace;
     a3.ne = st->ntiles * st->groups;
     a3.nblk = st->nblk2;
+    a3.estride = 1;
     a3.sp = st->sp;
     foe::k_decide<<<st->B, kThreads, 0, s>>>(a3);
     count_launch(1);
@@ -708,13 +709,13 @@ foe_status state_init(ipiano_state* st, const float* f, const double* lipschitz_
     if (st->cfg.record_trace)
         CK(cudaMemsetAsync(st->trace, 0, sizeof(double) * B * (st->cfg.max_iters + 1) * 8, st->s));
     foe::k_init<<<dim3(st->nblk2, B), kThreads, 0, st->s>>>(f, st->ft, st->w, n, st->ppart, st->nblk2, st->ctl,
-                                                             st->HW, kPxt2);
+                                                             st->HW, kPxt2, nullptr, 0);
     count_launch(1);
     CKL("k_init");
     const K1Args a1 = state_k1_args(st, 1);
     k1_dispatch(st->model->m, false, a1, *st->model->tp, *st->model->tp2, dim3(st->ntiles * st->groups, B), st->s);
     CKL("k_prior_grad (init)");
-    foe::k_init_finalize<<<B, kThreads, 0, st->s>>>(st->ctl, st->epart, st->ntiles * st->groups, st->ppart,
+    foe::k_init_finalize<<<B, kThreads, 0, st->s>>>(st->ctl, st->epart, st->ntiles * st->groups, 1, st->ppart,
                                                     st->nblk2, st->trace, st->cfg.max_iters, st->cfg.record_trace);
     count_launch(1);
     CKL("k_init_finalize");
@@ -993,6 +994,523 @@ foe_status ipiano_run(const foe_model* md, const float* f, int B, int H, int W, 
     if (du) CK(cudaFreeAsync(du, s));
     CK(cudaStreamSynchronize(s));
     return r != FOE_OK ? r : r2;
+}
+
+}  // extern "C"
+
+// ============================================================================ row slabs
+//
+// One periodic scene cut into `nslabs` equal row slabs (BASELINE.json
+// configs[4]).  Per trial round every slab runs
+//   A  K2 on its rows (w+ of its first/last kHalo rows also packed into halo_send)
+//   X  halo exchange: top ghost rows <- the slab above's last kHalo rows, bottom ghost rows
+//      <- the slab below's first kHalo rows (ring: slab 0's top comes from slab G-1)
+//   B  K1 on its rows, reading the ghost rows (energy over owned responses, g+ on owned px)
+//   R  per-band (64-row) partials of K1 and K2 into its part of the global band array
+//   Y  gather of the band arrays (NCCL all-gather; in-process slabs share the array)
+//   C  K3 on the global band array: every slab takes the identical decision.
+// Bands are a fixed partition of the scene and every reduction has a fixed order, so the
+// iterate and the trace are bitwise identical for any number of slabs.
+
+#include <dlfcn.h>
+#include <nccl.h>
+
+namespace {
+
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+// NCCL is resolved at run time (the copy torch already loaded, else the system one), so that
+// libfoe itself loads without it; only the multi-process slab path needs it.
+const NcclApi& nccl_api() {
+    static NcclApi api;
+    static bool tried = false;
+    static std::atomic<int> lock{0};
+    while (lock.exchange(1)) {}
+    if (!tried) {
+        tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+            api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+            api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+            api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+            api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+            api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+            api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+            api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+            api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+            api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.GroupStart && api.GroupEnd &&
+                     api.Send && api.Recv && api.AllGather && api.GetErrorString;
+        }
+    }
+    lock.store(0);
+    return api;
+}
+
+foe_status nccl_fail(ncclResult_t r, const char* what, int line) {
+    const NcclApi& api = nccl_api();
+    return fail(FOE_ERR_COMM, "%s failed: %s (foe_api.cu:%d)", what,
+                api.GetErrorString ? api.GetErrorString(r) : "?", line);
+}
+#define CKN(call)                                                         \
+    do {                                                                  \
+        ncclResult_t r_ = (call);                                         \
+        if (r_ != ncclSuccess) return nccl_fail(r_, #call, __LINE__);     \
+    } while (0)
+
+}  // namespace
+
+struct foe_comm {
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0, dev = 0;
+};
+
+struct ipiano_slabs {
+    const foe_model* model = nullptr;
+    const foe_comm* comm = nullptr;        // nullptr: all slabs in this process
+    int nslabs = 1, first = 0;             // global slab index of members[0]
+    int Hs = 0, W = 0, Hg = 0;             // slab rows, columns, scene rows
+    int nb_local = 0, nb_global = 0, e_per_band = 0, bpb = 0;
+    std::vector<ipiano_state*> members;    // slabs owned by this process, in ring order
+    double* band_all = nullptr;            // [nb_global][kNumPart]
+    double* halo = nullptr;                // [members][2][kHalo][W] received ghost rows
+    double* halo_send = nullptr;           // [members][2][kHalo][W] own boundary rows
+    cudaStream_t s = nullptr;
+    cudaEvent_t sync_ev = nullptr;
+    cudaGraphExec_t graph = nullptr;
+    bool use_graph = true;
+};
+
+namespace {
+
+size_t halo_elems(const ipiano_slabs* g) { return (size_t)2 * foe::kHalo * g->W; }
+
+// A (K2 + pack) for member j
+foe_status slab_k2(ipiano_slabs* g, int j) {
+    ipiano_state* st = g->members[j];
+    foe::K2Args a2{};
+    a2.w = st->w;
+    a2.w_slot_stride = st->HW;
+    a2.g = st->g;
+    a2.g_group_stride = st->HW;
+    a2.g_slot_stride = a2.g_group_stride * st->groups;
+    a2.ft = st->ft;
+    a2.ppart = st->ppart;
+    a2.ctl = st->ctl;
+    a2.sp = st->sp;
+    a2.groups = st->groups;
+    a2.nblk = st->nblk2;
+    a2.HW = st->HW;
+    a2.halo_send = g->halo_send + j * halo_elems(g);
+    a2.halo_px = (size_t)foe::kHalo * g->W;
+    foe::k_inertial_prox<kPxt2><<<dim3(st->nblk2, 1), kThreads, 0, g->s>>>(a2);
+    count_launch(1);
+    CKL("k_inertial_prox (slab)");
+    return FOE_OK;
+}
+
+// X: ghost rows.  Top ghost of slab i = last kHalo rows of slab i-1; bottom ghost = first
+// kHalo rows of slab i+1 (periodic ring).
+foe_status slab_exchange(ipiano_slabs* g) {
+    const size_t hp = (size_t)foe::kHalo * g->W;
+    if (g->comm == nullptr) {
+        const int n = (int)g->members.size();
+        for (int j = 0; j < n; ++j) {
+            const int up = (j + n - 1) % n, dn = (j + 1) % n;
+            double* dst = g->halo + j * halo_elems(g);
+            CK(cudaMemcpyAsync(dst, g->halo_send + up * halo_elems(g) + hp, hp * sizeof(double),
+                               cudaMemcpyDeviceToDevice, g->s));
+            CK(cudaMemcpyAsync(dst + hp, g->halo_send + dn * halo_elems(g), hp * sizeof(double),
+                               cudaMemcpyDeviceToDevice, g->s));
+        }
+        return FOE_OK;
+    }
+    const NcclApi& api = nccl_api();
+    const int R = g->comm->nranks, r = g->comm->rank;
+    const int up = (r + R - 1) % R, dn = (r + 1) % R;
+    // One fixed posting order on every rank, so that two messages between the same pair of
+    // ranks (G = 2, or G = 1 to itself) match: send up, recv down, send down, recv up.
+    CKN(api.GroupStart());
+    CKN(api.Send(g->halo_send, hp, ncclFloat64, up, g->comm->comm, g->s));          // my top rows
+    CKN(api.Recv(g->halo + hp, hp, ncclFloat64, dn, g->comm->comm, g->s));          // below's top rows
+    CKN(api.Send(g->halo_send + hp, hp, ncclFloat64, dn, g->comm->comm, g->s));     // my bottom rows
+    CKN(api.Recv(g->halo, hp, ncclFloat64, up, g->comm->comm, g->s));               // above's bottom rows
+    CKN(api.GroupEnd());
+    return FOE_OK;
+}
+
+K1Args slab_k1_args(ipiano_slabs* g, int j, int which_cur) {
+    ipiano_state* st = g->members[j];
+    K1Args a = state_k1_args(st, which_cur);
+    a.w_slot_stride = st->HW;
+    a.g_group_stride = st->HW;
+    a.g_slot_stride = a.g_group_stride * st->groups;
+    a.halo = g->halo + j * halo_elems(g);
+    return a;
+}
+
+// R + Y: band partials of every member into the global array, then the all-gather.
+foe_status slab_bands(ipiano_slabs* g) {
+    for (size_t j = 0; j < g->members.size(); ++j) {
+        ipiano_state* st = g->members[j];
+        double* out = g->band_all + (size_t)(g->first + (int)j) * g->nb_local * foe::kNumPart;
+        foe::k_band_reduce<<<g->nb_local, kThreads, 0, g->s>>>(st->epart, g->e_per_band, st->ppart, g->bpb, out);
+        count_launch(1);
+        CKL("k_band_reduce");
+    }
+    if (g->comm != nullptr && g->comm->nranks > 1) {
+        const NcclApi& api = nccl_api();
+        const size_t cnt = (size_t)g->nb_local * foe::kNumPart;
+        CKN(api.AllGather(g->band_all + (size_t)g->comm->rank * cnt, g->band_all, cnt, ncclFloat64, g->comm->comm,
+                          g->s));
+    }
+    return FOE_OK;
+}
+
+foe_status slab_round(ipiano_slabs* g, bool timed) {
+    foe_status r;
+    for (size_t j = 0; j < g->members.size(); ++j)
+        if ((r = slab_k2(g, (int)j)) != FOE_OK) return r;
+    if ((r = slab_exchange(g)) != FOE_OK) return r;
+    for (size_t j = 0; j < g->members.size(); ++j) {
+        ipiano_state* st = g->members[j];
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (timed) {
+            e0 = pool_event(st);
+            e1 = pool_event(st);
+            CK(cudaEventRecord(e0, g->s));
+        }
+        k1_dispatch(st->model->m, false, slab_k1_args(g, (int)j, 0), *st->model->tp, *st->model->tp2,
+                    dim3(st->ntiles * st->groups, 1), g->s);
+        CKL("k_prior_grad (slab)");
+        if (timed) {
+            CK(cudaEventRecord(e1, g->s));
+            st->ev_live.emplace_back(e0, e1);
+            st->k1_launches += 1;
+        }
+    }
+    if ((r = slab_bands(g)) != FOE_OK) return r;
+    for (size_t j = 0; j < g->members.size(); ++j) {
+        ipiano_state* st = g->members[j];
+        foe::K3Args a3{};
+        a3.ctl = st->ctl;
+        a3.epart = g->band_all + 7;
+        a3.estride = foe::kNumPart;
+        a3.ppart = g->band_all;
+        a3.trace = st->trace;
+        a3.ne = g->nb_global;
+        a3.nblk = g->nb_global;
+        a3.sp = st->sp;
+        foe::k_decide<<<1, kThreads, 0, g->s>>>(a3);
+        count_launch(1);
+        CKL("k_decide (slab)");
+        st->total_launches += 4;
+    }
+    return FOE_OK;
+}
+
+foe_status slab_init(ipiano_slabs* g, const float* f, double L_init, cudaStream_t user) {
+    CK(cudaEventRecord(g->sync_ev, user));
+    CK(cudaStreamWaitEvent(g->s, g->sync_ev, 0));
+    const size_t HWs = (size_t)g->Hs * g->W;
+    for (size_t j = 0; j < g->members.size(); ++j) {
+        ipiano_state* st = g->members[j];
+        ImgCtl& c = st->hctl[0];
+        std::memset(&c, 0, sizeof(c));
+        c.L = L_init;
+        c.lam1 = st->lam[0];
+        c.lam2 = st->lam[1];
+        c.cur = 0; c.prev = 1; c.cand = 2;
+        c.gcur = 0; c.gcand = 1;
+        c.active = 1;
+        CK(cudaMemcpyAsync(st->ctl, st->hctl, sizeof(ImgCtl), cudaMemcpyHostToDevice, g->s));
+        if (st->cfg.record_trace)
+            CK(cudaMemsetAsync(st->trace, 0, sizeof(double) * (st->cfg.max_iters + 1) * 8, g->s));
+        foe::k_init<<<dim3(st->nblk2, 1), kThreads, 0, g->s>>>(f + j * HWs, st->ft, st->w, HWs, st->ppart, st->nblk2,
+                                                                st->ctl, HWs, kPxt2, g->halo_send + j * halo_elems(g),
+                                                                (size_t)foe::kHalo * g->W);
+        count_launch(1);
+        CKL("k_init (slab)");
+    }
+    foe_status r = slab_exchange(g);
+    if (r != FOE_OK) return r;
+    for (size_t j = 0; j < g->members.size(); ++j) {
+        ipiano_state* st = g->members[j];
+        k1_dispatch(st->model->m, false, slab_k1_args(g, (int)j, 1), *st->model->tp, *st->model->tp2,
+                    dim3(st->ntiles * st->groups, 1), g->s);
+        CKL("k_prior_grad (slab init)");
+    }
+    if ((r = slab_bands(g)) != FOE_OK) return r;
+    for (size_t j = 0; j < g->members.size(); ++j) {
+        ipiano_state* st = g->members[j];
+        foe::k_init_finalize<<<1, kThreads, 0, g->s>>>(st->ctl, g->band_all + 7, g->nb_global, foe::kNumPart,
+                                                        g->band_all, g->nb_global, st->trace, st->cfg.max_iters,
+                                                        st->cfg.record_trace);
+        count_launch(1);
+        CKL("k_init_finalize (slab)");
+        foe::k_set_target<<<1, 128, 0, g->s>>>(st->ctl, 1, 0);
+        count_launch(1);
+        CKL("k_set_target (slab)");
+    }
+    CK(cudaEventRecord(g->sync_ev, g->s));
+    CK(cudaStreamWaitEvent(user, g->sync_ev, 0));
+    return FOE_OK;
+}
+
+foe_status slab_sync(ipiano_slabs* g) {
+    for (ipiano_state* st : g->members)
+        CK(cudaMemcpyAsync(st->hctl, st->ctl, sizeof(ImgCtl), cudaMemcpyDeviceToHost, g->s));
+    CK(cudaStreamSynchronize(g->s));
+    for (ipiano_state* st : g->members) {
+        for (auto& pr : st->ev_live) {
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) st->k1_ms += ms;
+            st->ev_pool.push_back(pr.first);
+            st->ev_pool.push_back(pr.second);
+        }
+        st->ev_live.clear();
+    }
+    return FOE_OK;
+}
+
+foe_status slab_ensure_graph(ipiano_slabs* g) {
+    if (g->graph) return FOE_OK;
+    cudaGraph_t gr = nullptr;
+    CK(cudaStreamBeginCapture(g->s, cudaStreamCaptureModeThreadLocal));
+    foe_status r = FOE_OK;
+    t_capturing = true;
+    std::vector<long long> tl;
+    for (ipiano_state* st : g->members) tl.push_back(st->total_launches);
+    for (int i = 0; i < kGraphRounds && r == FOE_OK; ++i) r = slab_round(g, false);
+    t_capturing = false;
+    for (size_t j = 0; j < g->members.size(); ++j) g->members[j]->total_launches = tl[j];
+    cudaError_t e = cudaStreamEndCapture(g->s, &gr);
+    if (r != FOE_OK) { if (gr) cudaGraphDestroy(gr); return r; }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamEndCapture (slabs)", __LINE__);
+    e = cudaGraphInstantiate(&g->graph, gr, 0);
+    cudaGraphDestroy(gr);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGraphInstantiate (slabs)", __LINE__);
+    return FOE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+foe_status foe_comm_unique_id(void* id_out) {
+    if (!id_out) return fail(FOE_ERR_INVALID_ARGUMENT, "id_out is NULL");
+    const NcclApi& api = nccl_api();
+    if (!api.ok) return fail(FOE_ERR_COMM, "libnccl.so.2 could not be loaded");
+    ncclUniqueId id;
+    CKN(api.GetUniqueId(&id));
+    std::memcpy(id_out, &id, sizeof(id));
+    return FOE_OK;
+}
+
+foe_status foe_comm_create(const void* id, int nranks, int rank, int cuda_device, foe_comm** out) {
+    if (!out) return fail(FOE_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (!id) return fail(FOE_ERR_INVALID_ARGUMENT, "id is NULL");
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(FOE_ERR_INVALID_ARGUMENT, "rank=%d outside [0, nranks=%d)", rank, nranks);
+    const NcclApi& api = nccl_api();
+    if (!api.ok) return fail(FOE_ERR_COMM, "libnccl.so.2 could not be loaded");
+    CK(cudaSetDevice(cuda_device));
+    foe_comm* c = new (std::nothrow) foe_comm();
+    if (!c) return fail(FOE_ERR_OUT_OF_MEMORY, "host allocation");
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclResult_t r = api.CommInitRank(&c->comm, nranks, uid, rank);
+    if (r != ncclSuccess) { delete c; return nccl_fail(r, "ncclCommInitRank", __LINE__); }
+    c->nranks = nranks;
+    c->rank = rank;
+    c->dev = cuda_device;
+    *out = c;
+    return FOE_OK;
+}
+
+void foe_comm_destroy(foe_comm* c) {
+    if (!c) return;
+    const NcclApi& api = nccl_api();
+    if (c->comm && api.ok) api.CommDestroy(c->comm);
+    delete c;
+}
+
+void ipiano_slabs_destroy(ipiano_slabs* g) {
+    if (!g) return;
+    cudaSetDevice(g->model->dev);
+    if (g->s) cudaStreamSynchronize(g->s);
+    for (ipiano_state* st : g->members) {
+        st->s = nullptr;  // the group's stream
+        ipiano_state_destroy(st);
+    }
+    if (g->graph) cudaGraphExecDestroy(g->graph);
+    cudaFree(g->band_all);
+    cudaFree(g->halo);
+    cudaFree(g->halo_send);
+    if (g->sync_ev) cudaEventDestroy(g->sync_ev);
+    if (g->s) cudaStreamDestroy(g->s);
+    delete g;
+}
+
+foe_status ipiano_slabs_create(const foe_model* md, const float* f, int H_global, int W, int nslabs,
+                               const double* lambda, double lipschitz_init, const ipiano_config* cfg_in,
+                               const foe_comm* comm, void* stream, ipiano_slabs** out) {
+    if (!out) return fail(FOE_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (!md) return fail(FOE_ERR_INVALID_ARGUMENT, "model is NULL");
+    if (!f) return fail(FOE_ERR_INVALID_ARGUMENT, "f is NULL");
+    if (comm) nslabs = comm->nranks;
+    if (comm && comm->dev != md->dev)
+        return fail(FOE_ERR_INVALID_ARGUMENT, "comm is on cuda:%d, the model on cuda:%d", comm->dev, md->dev);
+    if (nslabs < 1) return fail(FOE_ERR_INVALID_ARGUMENT, "nslabs=%d must be >= 1", nslabs);
+    if (H_global % (nslabs * foe::kBandRows) != 0)
+        return fail(FOE_ERR_INVALID_ARGUMENT, "H_global=%d must be a multiple of %d x nslabs=%d (64-row bands per slab)",
+                    H_global, foe::kBandRows, nslabs);
+    if (W % 32 != 0 || W < md->m)
+        return fail(FOE_ERR_INVALID_ARGUMENT, "W=%d must be a multiple of 32 and >= m", W);
+    if (!(lipschitz_init > 0.0) || !std::isfinite(lipschitz_init))
+        return fail(FOE_ERR_INVALID_ARGUMENT, "lipschitz_init=%g must be > 0", lipschitz_init);
+    CK(cudaSetDevice(md->dev));
+    ipiano_slabs* g = new (std::nothrow) ipiano_slabs();
+    if (!g) return fail(FOE_ERR_OUT_OF_MEMORY, "host allocation");
+    auto cleanup = [&](foe_status s) { ipiano_slabs_destroy(g); return s; };
+    g->model = md;
+    g->comm = comm;
+    g->nslabs = nslabs;
+    g->first = comm ? comm->rank : 0;
+    g->Hs = H_global / nslabs;
+    g->W = W;
+    g->Hg = H_global;
+    const int nmem = comm ? 1 : nslabs;
+    const int tiles_x = div_up(W, kTile);
+    const int groups = choose_groups(md, tiles_x * div_up(H_global, kTile), 1, cfg_in ? cfg_in->filter_groups : 0);
+    g->nb_local = g->Hs / foe::kBandRows;
+    g->nb_global = H_global / foe::kBandRows;
+    g->e_per_band = tiles_x * groups;
+    g->bpb = foe::kBandRows * W / (kThreads * kPxt2);
+    CK(cudaStreamCreateWithFlags(&g->s, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&g->sync_ev, cudaEventDisableTiming));
+    const size_t he = halo_elems(g);
+    if (cudaMalloc((void**)&g->band_all, sizeof(double) * g->nb_global * foe::kNumPart) != cudaSuccess ||
+        cudaMalloc((void**)&g->halo, sizeof(double) * he * nmem) != cudaSuccess ||
+        cudaMalloc((void**)&g->halo_send, sizeof(double) * he * nmem) != cudaSuccess)
+        return cleanup(cuda_fail(cudaErrorMemoryAllocation, "cudaMalloc (slabs)", __LINE__));
+    cudaMemset(g->band_all, 0, sizeof(double) * g->nb_global * foe::kNumPart);
+    ipiano_config cfg;
+    if (cfg_in) cfg = *cfg_in; else ipiano_config_default(&cfg);
+    cfg.filter_groups = groups;
+    // members: per-slab iPiano states of one image (B = 1) sharing the group's stream.
+    // ipiano_state_create evaluates w^0 with periodic wrap; slab_init below redoes it with halos.
+    const size_t HWs = (size_t)g->Hs * W;
+    for (int j = 0; j < nmem; ++j) {
+        ipiano_state* st = nullptr;
+        foe_status r = ipiano_state_create(md, f + (size_t)j * HWs, 1, g->Hs, W, lambda, &lipschitz_init, &cfg,
+                                           stream, &st);
+        if (r != FOE_OK) return cleanup(r);
+        cudaStreamSynchronize(st->s);
+        cudaStreamDestroy(st->s);
+        st->s = g->s;
+        g->members.push_back(st);
+    }
+    foe_status r = slab_init(g, f, lipschitz_init, (cudaStream_t)stream);
+    if (r != FOE_OK) return cleanup(r);
+    *out = g;
+    return FOE_OK;
+}
+
+foe_status ipiano_slabs_reset(ipiano_slabs* g, const float* f, double lipschitz_init, void* stream) {
+    if (!g || !f) return fail(FOE_ERR_INVALID_ARGUMENT, "slabs or f is NULL");
+    if (!(lipschitz_init > 0.0) || !std::isfinite(lipschitz_init))
+        return fail(FOE_ERR_INVALID_ARGUMENT, "lipschitz_init=%g must be > 0", lipschitz_init);
+    CK(cudaSetDevice(g->model->dev));
+    return slab_init(g, f, lipschitz_init, (cudaStream_t)stream);
+}
+
+foe_status ipiano_slabs_solve(ipiano_slabs* g, void* stream) {
+    if (!g) return fail(FOE_ERR_INVALID_ARGUMENT, "slabs is NULL");
+    CK(cudaSetDevice(g->model->dev));
+    cudaStream_t user = (cudaStream_t)stream;
+    CK(cudaEventRecord(g->sync_ev, user));
+    CK(cudaStreamWaitEvent(g->s, g->sync_ev, 0));
+    const int max_iters = g->members[0]->cfg.max_iters;
+    for (ipiano_state* st : g->members) {
+        foe::k_set_target<<<1, 128, 0, g->s>>>(st->ctl, 1, max_iters);
+        count_launch(1);
+    }
+    CKL("k_set_target (slabs)");
+    foe_status r = slab_sync(g);
+    if (r != FOE_OK) return r;
+    const bool timed = g->members[0]->profile;
+    const long long max_rounds = (long long)max_iters * (g->members[0]->cfg.max_backtracks + 2) + 8;
+    long long done = 0;
+    for (;;) {
+        const ImgCtl& c = g->members[0]->hctl[0];   // identical on every slab
+        if (!c.active || done > max_rounds) break;
+        const int rounds = std::max(1, max_iters - c.n);
+        if (timed || !g->use_graph) {
+            for (int i = 0; i < rounds; ++i)
+                if ((r = slab_round(g, timed)) != FOE_OK) return r;
+            done += rounds;
+        } else {
+            if ((r = slab_ensure_graph(g)) != FOE_OK) return r;
+            const int reps = div_up(rounds, kGraphRounds);
+            for (int i = 0; i < reps; ++i) {
+                CK(cudaGraphLaunch(g->graph, g->s));
+                count_launch(4LL * kGraphRounds * (long long)g->members.size());
+                for (ipiano_state* st : g->members) st->total_launches += 4LL * kGraphRounds;
+            }
+            done += (long long)reps * kGraphRounds;
+        }
+        if ((r = slab_sync(g)) != FOE_OK) return r;
+    }
+    for (size_t j = 1; j < g->members.size(); ++j)
+        if (std::memcmp(&g->members[j]->hctl[0], &g->members[0]->hctl[0], sizeof(ImgCtl)) != 0)
+            return fail(FOE_ERR_COMM, "slab %d diverged from slab 0 (control blocks differ)", (int)j);
+    CK(cudaEventRecord(g->sync_ev, g->s));
+    CK(cudaStreamWaitEvent(user, g->sync_ev, 0));
+    return first_image_error(g->members[0]);
+}
+
+foe_status ipiano_slabs_get_iterate(const ipiano_slabs* g, double* w_out, float* u_out, void* stream) {
+    if (!g) return fail(FOE_ERR_INVALID_ARGUMENT, "slabs is NULL");
+    CK(cudaSetDevice(g->model->dev));
+    ipiano_slabs* gg = const_cast<ipiano_slabs*>(g);
+    cudaStream_t user = (cudaStream_t)stream;
+    CK(cudaEventRecord(gg->sync_ev, user));
+    CK(cudaStreamWaitEvent(gg->s, gg->sync_ev, 0));
+    const size_t HWs = (size_t)g->Hs * g->W;
+    for (size_t j = 0; j < g->members.size(); ++j) {
+        const ipiano_state* st = g->members[j];
+        const int gx = std::max(1, std::min(div_up((long long)HWs, 256), 4 * g->model->nsm));
+        foe::k_iterate_out<<<dim3(gx, 1), 256, 0, gg->s>>>(st->ctl, st->w, HWs, w_out ? w_out + j * HWs : nullptr,
+                                                            u_out ? u_out + j * HWs : nullptr, HWs);
+        count_launch(1);
+        CKL("k_iterate_out (slabs)");
+    }
+    CK(cudaEventRecord(gg->sync_ev, gg->s));
+    CK(cudaStreamWaitEvent(user, gg->sync_ev, 0));
+    return FOE_OK;
+}
+
+foe_status ipiano_slabs_member(const ipiano_slabs* g, int j, ipiano_state** out) {
+    if (!g || !out) return fail(FOE_ERR_INVALID_ARGUMENT, "slabs or out is NULL");
+    if (j < 0 || j >= (int)g->members.size())
+        return fail(FOE_ERR_INVALID_ARGUMENT, "member %d outside [0,%d)", j, (int)g->members.size());
+    *out = g->members[j];
+    return FOE_OK;
 }
 
 }  // extern "C"

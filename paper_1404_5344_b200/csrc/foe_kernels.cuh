@@ -28,6 +28,8 @@ constexpr int kMaxTaps = 3136;
 constexpr int kThreads = 256;
 constexpr int kTile = 64;  // output tile side of K1
 constexpr int kNumPart = 8;  // K2 block partials
+constexpr int kHalo = 6;     // ghost rows per side of a row slab (2C for m <= 7)
+constexpr int kBandRows = 64; // rows per band of the slab-invariant partial reduction (= kTile)
 
 // Filter taps, resident in the kernel-parameter constant bank.
 struct TapParams {
@@ -69,6 +71,10 @@ struct K1Args {
     const ImgCtl* ctl;      // nullable
     int which_cur;          // 1: evaluate at ctl.cur -> ctl.gcur; 0: ctl.cand -> ctl.gcand
     int H, W, tiles_x, ntiles, groups, nf, nchunks;
+    // Row slab: rows y < 0 come from halo row kHalo + y, rows y >= H from
+    // halo row kHalo + (y - H) ([2][kHalo][W] fp64, filled by the halo exchange); nullptr =
+    // periodic wrap inside the image (single-GPU scene).
+    const double* halo;
     // HVP only
     const double* v;        // [B][H][W]
     const float* gw;        // [B][H][W] gradient at w
@@ -478,14 +484,21 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
     const int ck0 = (grp * args.nchunks) / args.groups;
     const int ck1 = ((grp + 1) * args.nchunks) / args.groups;
 
-    // (a2) stage u - c on the tile + 2C halo (fp64 exp, one rounding to fp32)
-    const int yc = wrap_idx(y0 + kTile / 2, H), xc = wrap_idx(x0 + kTile / 2, W);
+    // (a2) stage u - c on the tile + 2C halo (fp64 exp, one rounding to fp32); c = e^w at a
+    // pixel inside the tile (so a row slab and the whole scene use the same c)
+    const int yc = min(y0 + kTile / 2, H - 1), xc = min(x0 + kTile / 2, W - 1);
     const float cst = (float)exp(w[(size_t)yc * W + xc]);
     const double cstd = (double)cst;
+    const double* halo = args.halo;
     for (int idx = threadIdx.x; idx < G::UY * G::UX; idx += kThreads) {
         const int uy = idx / G::UX, ux = idx - uy * G::UX;
-        const int gy = wrap_idx(y0 - 2 * C + uy, H), gx = wrap_idx(x0 - 2 * C + ux, W);
-        us[uy * G::UP + ux] = (float)(exp(w[(size_t)gy * W + gx]) - cstd);
+        const int y = y0 - 2 * C + uy, gx = wrap_idx(x0 - 2 * C + ux, W);
+        const double* src;
+        if (halo == nullptr) src = w + (size_t)wrap_idx(y, H) * W;
+        else if (y < 0) src = halo + (size_t)(kHalo + y) * W;
+        else if (y >= H) src = halo + (size_t)(kHalo + y - H) * W;
+        else src = w + (size_t)y * W;
+        us[uy * G::UP + ux] = (float)(exp(src[gx]) - cstd);
     }
     __syncthreads();
 
@@ -665,6 +678,10 @@ struct K2Args {
     SolverParams sp;
     int groups, nblk;
     size_t HW;
+    // Row slab: w+ of the first and last kHalo rows is also written to halo_send
+    // ([2][kHalo][W], the rows the ring neighbours need); nullptr = no slab.
+    double* halo_send;
+    size_t halo_px;        // kHalo * W
 };
 
 template <int PXT>
@@ -695,6 +712,10 @@ k_inertial_prox(const K2Args a) {  // (3 CTAs/SM: <= 80 registers)
         double z, em, ep;
         const int it = prox_newton(what, f, alpha, l1, l2, a.sp.newton_tol, a.sp.newton_cap, z, em, ep);
         wn[p] = z;
+        if (a.halo_send != nullptr) {
+            if (p < a.halo_px) a.halo_send[p] = z;
+            else if (p >= a.HW - a.halo_px) a.halo_send[p - (a.HW - 2 * a.halo_px)] = z;
+        }
         const double d = z - wv;
         gd += gv * d;
         dd += d * d;
@@ -734,10 +755,10 @@ k_inertial_prox(const K2Args a) {  // (3 CTAs/SM: <= 80 registers)
 // ---------------------------------------------------------------------------------
 struct K3Args {
     ImgCtl* ctl;
-    const double* epart;  // [B][ne]
+    const double* epart;  // [B][ne] (element i at epart[(b ne + i) estride])
     const double* ppart;  // [B][nblk][kNumPart]
     double* trace;        // [B][max_iters+1][8]
-    int ne, nblk;
+    int ne, nblk, estride;
     SolverParams sp;
 };
 
@@ -749,7 +770,7 @@ __global__ void __launch_bounds__(kThreads) k_decide(const K3Args a) {
     ImgCtl& c = a.ctl[b];
     if (!c.active) return;
     double e = 0.0;
-    for (int i = threadIdx.x; i < a.ne; i += kThreads) e += a.epart[(size_t)b * a.ne + i];
+    for (int i = threadIdx.x; i < a.ne; i += kThreads) e += a.epart[((size_t)b * a.ne + i) * a.estride];
     double s[7] = {0, 0, 0, 0, 0, 0, 0};
     for (int i = threadIdx.x; i < a.nblk; i += kThreads) {
         const double* p = a.ppart + ((size_t)b * a.nblk + i) * kNumPart;
@@ -806,7 +827,7 @@ __global__ void __launch_bounds__(kThreads) k_decide(const K3Args a) {
 // partials of G(w^0) (slot 2 of ppart).
 __global__ void __launch_bounds__(kThreads)
 k_init(const float* f, float* ft, double* w, size_t w_slot_stride, double* ppart, int nblk,
-       const ImgCtl* ctl, size_t HW, int pxt) {
+       const ImgCtl* ctl, size_t HW, int pxt, double* halo_send, size_t halo_px) {
     __shared__ double red[32];
     const int b = blockIdx.y;
     const double l1 = ctl[b].lam1, l2 = ctl[b].lam2;
@@ -822,6 +843,10 @@ k_init(const float* f, float* ft, double* w, size_t w_slot_stride, double* ppart
         const double z = log(fd);
         w[gi] = z;
         w[w_slot_stride + gi] = z;
+        if (halo_send != nullptr) {   // row slab (B = 1): rows the ring neighbours need
+            if (p < halo_px) halo_send[p] = z;
+            else if (p >= HW - halo_px) halo_send[p - (HW - 2 * halo_px)] = z;
+        }
         const double f2 = fd * fd;
         G += 0.5 * l1 * (2.0 * z + f2 * exp(-2.0 * z)) + 0.5 * l2 * (exp(2.0 * z) - 2.0 * f2 * z);
     }
@@ -835,12 +860,12 @@ k_init(const float* f, float* ft, double* w, size_t w_slot_stride, double* ppart
 
 // F(w^0), G(w^0) -> ctl, trace row 0.
 __global__ void __launch_bounds__(kThreads)
-k_init_finalize(ImgCtl* ctl, const double* epart, int ne, const double* ppart, int nblk,
+k_init_finalize(ImgCtl* ctl, const double* epart, int ne, int estride, const double* ppart, int nblk,
                 double* trace, int max_iters, int record) {
     __shared__ double red[32];
     const int b = blockIdx.x;
     double e = 0.0, g = 0.0;
-    for (int i = threadIdx.x; i < ne; i += kThreads) e += epart[(size_t)b * ne + i];
+    for (int i = threadIdx.x; i < ne; i += kThreads) e += epart[((size_t)b * ne + i) * estride];
     for (int i = threadIdx.x; i < nblk; i += kThreads) g += ppart[((size_t)b * nblk + i) * kNumPart + 2];
     const double F = block_sum_d(e, red);
     const double G = block_sum_d(g, red);
@@ -874,6 +899,34 @@ k_reduce_rows(const double* part, int nblk, int stride, int K, double* out) {
         s = block_sum_d(s, red);
         if (threadIdx.x == 0) out[(size_t)b * K + k] = s;
     }
+}
+
+// Row slab (B = 1): per-band partials of one slab, band k = slab rows [64k, 64k+64) = tile row
+// k = K2 blocks [k bpb, (k+1) bpb).  out[k][0..6] = the K2 partials of the band (sums; slots
+// 4/5 max), out[k][7] = the band's K1 energy partials.  Bands are a fixed global partition of
+// the scene, so the decision's sums do not depend on how many slabs it is cut into.
+__global__ void __launch_bounds__(kThreads)
+k_band_reduce(const double* epart, int e_per_band, const double* ppart, int bpb, double* out) {
+    __shared__ double red[32];
+    const int k = blockIdx.x;
+    double e = 0.0;
+    for (int i = threadIdx.x; i < e_per_band; i += kThreads) e += epart[(size_t)k * e_per_band + i];
+    double s[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int i = threadIdx.x; i < bpb; i += kThreads) {
+        const double* p = ppart + ((size_t)k * bpb + i) * kNumPart;
+        s[0] += p[0]; s[1] += p[1]; s[2] += p[2]; s[3] += p[3];
+        s[4] = fmax(s[4], p[4]); s[5] = fmax(s[5], p[5]); s[6] += p[6];
+    }
+    double r[8];
+    r[0] = block_sum_d(s[0], red);
+    r[1] = block_sum_d(s[1], red);
+    r[2] = block_sum_d(s[2], red);
+    r[3] = block_sum_d(s[3], red);
+    r[4] = block_max_d(s[4], red);
+    r[5] = block_max_d(s[5], red);
+    r[6] = block_sum_d(s[6], red);
+    r[7] = block_sum_d(e, red);
+    if (threadIdx.x < 8) out[(size_t)k * kNumPart + threadIdx.x] = r[threadIdx.x];
 }
 
 // data energy partials of a given w (foe_energy_grad): part[b][blk][0]

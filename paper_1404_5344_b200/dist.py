@@ -68,3 +68,34 @@ def barrier():
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():
         dist.barrier()
+
+
+# ------------------------------------------------------------------ row slabs (c5)
+
+def slab_rows(H_global: int, world_size: int, rank: int, band: int = 64) -> tuple:
+    """Rows [r0, r1) of rank's slab: equal slabs of whole 64-row bands (include/foe.h
+    ipiano_slabs_create), ranks in ring order top to bottom."""
+    if H_global % (band * world_size):
+        raise ValueError(f"H_global={H_global} is not a multiple of {band} x {world_size}")
+    rows = H_global // world_size
+    return rank * rows, (rank + 1) * rows
+
+
+def ring_neighbours(rank: int, world_size: int) -> tuple:
+    """(up, down): the slabs above and below in the periodic ring."""
+    return (rank - 1) % world_size, (rank + 1) % world_size
+
+
+# The posting order of the ghost-row exchange (foe_api.cu slab_exchange): the same on every
+# rank, so that two messages between one pair of ranks (2 ranks, or 1 rank with itself) match.
+HALO_POSTING_ORDER = (("send", "up", "top_rows"), ("recv", "down", "bottom_ghost"),
+                      ("send", "down", "bottom_rows"), ("recv", "up", "top_ghost"))
+
+
+def share_bytes(payload, src: int = 0) -> bytes:
+    """Broadcast a small byte string (e.g. the NCCL unique id) from rank src to all ranks."""
+    import torch.distributed as dist
+    obj = [payload]
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.broadcast_object_list(obj, src=src)
+    return obj[0]

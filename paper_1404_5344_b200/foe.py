@@ -29,6 +29,8 @@ EXPORTED = (
     "ipiano_state_create", "ipiano_state_reset", "ipiano_step", "ipiano_solve", "ipiano_get_iterate",
     "ipiano_get_counters", "ipiano_get_trace", "ipiano_profile", "ipiano_profile_read",
     "ipiano_state_destroy", "ipiano_run",
+    "foe_comm_unique_id", "foe_comm_create", "foe_comm_destroy", "ipiano_slabs_create", "ipiano_slabs_reset",
+    "ipiano_slabs_solve", "ipiano_slabs_get_iterate", "ipiano_slabs_member", "ipiano_slabs_destroy",
 )
 
 
@@ -90,6 +92,18 @@ def lib():
     L.ipiano_state_destroy.restype = None
     L.ipiano_run.argtypes = [_vp, _vp, C.c_int, C.c_int, C.c_int, _dp, _dp, C.POINTER(IPianoConfig),
                              _vp, _vp, C.c_size_t, _vp]
+    L.foe_comm_unique_id.argtypes = [_vp]
+    L.foe_comm_create.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]
+    L.foe_comm_destroy.argtypes = [_vp]
+    L.foe_comm_destroy.restype = None
+    L.ipiano_slabs_create.argtypes = [_vp, _vp, C.c_int, C.c_int, C.c_int, _dp, C.c_double,
+                                      C.POINTER(IPianoConfig), _vp, _vp, C.POINTER(_vp)]
+    L.ipiano_slabs_reset.argtypes = [_vp, _vp, C.c_double, _vp]
+    L.ipiano_slabs_solve.argtypes = [_vp, _vp]
+    L.ipiano_slabs_get_iterate.argtypes = [_vp, _vp, _vp, _vp]
+    L.ipiano_slabs_member.argtypes = [_vp, C.c_int, C.POINTER(_vp)]
+    L.ipiano_slabs_destroy.argtypes = [_vp]
+    L.ipiano_slabs_destroy.restype = None
     _configured = L
     return L
 
@@ -407,3 +421,134 @@ def ipiano_run(model: Model, f, lam_per_image=None, lipschitz_init=None, cfg: Op
                             trace.nbytes if want_trace else 0, _stream(stream)))
     del keep
     return u_out, trace
+
+
+# ------------------------------------------------------------------ row slabs (multi-GPU)
+
+class Comm:
+    """foe_comm handle: this rank's NCCL communicator for the row-slab halo exchange."""
+
+    def __init__(self, handle, nranks: int, rank: int, device: int):
+        self._h = handle
+        self.nranks, self.rank, self.device = nranks, rank, device
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise FoeError(1, "comm destroyed")
+        return self._h
+
+    def destroy(self):
+        if self._h is not None:
+            lib().foe_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def foe_comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().foe_comm_unique_id(C.cast(buf, _vp)))
+    return buf.raw
+
+
+def foe_comm_create(unique_id: bytes, nranks: int, rank: int, device: int) -> Comm:
+    if len(unique_id) != 128:
+        raise ValueError("unique_id must be the 128 bytes of foe_comm_unique_id")
+    buf = C.create_string_buffer(bytes(unique_id), 128)
+    h = C.c_void_p()
+    _check(lib().foe_comm_create(C.cast(buf, _vp), int(nranks), int(rank), int(device), C.byref(h)))
+    return Comm(h, nranks, rank, device)
+
+
+def foe_comm_destroy(comm: Comm):
+    comm.destroy()
+
+
+class Slabs:
+    """ipiano_slabs handle: one scene cut into row slabs (all in-process, or this rank's)."""
+
+    def __init__(self, handle, model: Model, rows: int, W: int, H_global: int, nmembers: int,
+                 cfg: IPianoConfig, comm: Optional[Comm]):
+        self._h = handle
+        self.model, self.rows, self.W, self.H_global = model, rows, W, H_global
+        self.nmembers, self.cfg, self.comm = nmembers, cfg, comm
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise FoeError(1, "slabs destroyed")
+        return self._h
+
+    def destroy(self):
+        if self._h is not None:
+            lib().ipiano_slabs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def ipiano_slabs_create(model: Model, f, H_global: int, nslabs: int = 1, lam=None, lipschitz_init=None,
+                        cfg: Optional[IPianoConfig] = None, comm: Optional[Comm] = None, stream=None) -> Slabs:
+    """Row-slab decomposition of one H_global x W scene.  comm=None: ``f`` is the whole scene
+    [H_global][W] and all ``nslabs`` slabs run in this process; else ``f`` is this rank's slab."""
+    torch = _torch()
+    if f.dim() != 2:
+        raise ValueError("f must be [rows][W]")
+    rows, W = int(f.shape[0]), int(f.shape[1])
+    cfg = cfg if cfg is not None else ipiano_config_default()
+    lam_arr, lam_p = _host_d(lam, 2, "lam")
+    if lipschitz_init is None:
+        raise ValueError("lipschitz_init is required (see foe_estimate_lipschitz)")
+    h = C.c_void_p()
+    _check(lib().ipiano_slabs_create(model.handle, _dev_ptr(f, torch.float32, "f", device=model.device),
+                                     int(H_global), W, int(nslabs), lam_p, float(lipschitz_init), C.byref(cfg),
+                                     comm.handle if comm is not None else None, _stream(stream), C.byref(h)))
+    return Slabs(h, model, rows, W, int(H_global), 1 if comm is not None else int(nslabs), cfg, comm)
+
+
+def ipiano_slabs_reset(slabs: Slabs, f, lipschitz_init: float, stream=None):
+    torch = _torch()
+    _check(lib().ipiano_slabs_reset(slabs.handle, _dev_ptr(f, torch.float32, "f", (slabs.rows, slabs.W),
+                                                           slabs.model.device), float(lipschitz_init),
+                                    _stream(stream)))
+
+
+def ipiano_slabs_solve(slabs: Slabs, stream=None):
+    _check(lib().ipiano_slabs_solve(slabs.handle, _stream(stream)))
+
+
+def ipiano_slabs_get_iterate(slabs: Slabs, want_w=True, want_u=True, stream=None, u_out=None):
+    """(w fp64, u fp32) device tensors [rows][W] of the slabs owned by this process."""
+    torch = _torch()
+    dev = torch.device("cuda", slabs.model.device)
+    shp = (slabs.rows, slabs.W)
+    w = torch.empty(shp, dtype=torch.float64, device=dev) if want_w else None
+    u = u_out if u_out is not None else (torch.empty(shp, dtype=torch.float32, device=dev) if want_u else None)
+    if u is not None:
+        _dev_ptr(u, torch.float32, "u_out", shp, slabs.model.device)
+    _check(lib().ipiano_slabs_get_iterate(slabs.handle, C.c_void_p(w.data_ptr()) if w is not None else None,
+                                          C.c_void_p(u.data_ptr()) if u is not None else None, _stream(stream)))
+    return w, u
+
+
+def ipiano_slabs_member(slabs: Slabs, j: int = 0) -> State:
+    """Non-owning State view of slab member j (counters, trace, profiling)."""
+    h = C.c_void_p()
+    _check(lib().ipiano_slabs_member(slabs.handle, int(j), C.byref(h)))
+    st = State(h, slabs.model, 1, slabs.rows // slabs.nmembers, slabs.W, slabs.cfg)
+    st._h_borrowed = h
+    st.destroy = lambda: None   # owned by the Slabs handle
+    return st
+
+
+def ipiano_slabs_destroy(slabs: Slabs):
+    slabs.destroy()
