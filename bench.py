@@ -37,6 +37,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "megapixel-iterations/s of iPiano (FoE grad+prox) and % of B200 FP32 peak"
+DTYPE_DETAIL = {1: "fp32 stencil (FFMA2), fp64 iterate/prox/reductions",
+                2: "fp32-accurate stencil on tensor cores (TF32 x3 hi/lo split, fp32 accumulate), "
+                   "fp64 iterate/prox/reductions"}
 UNIT = "MP-it/s"
 
 
@@ -51,7 +54,8 @@ def parse_args():
     ap.add_argument("--iters", type=int, default=0, help="override iteration count (quick runs only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-iters", type=int, default=4, help="oracle sample: iterations on one image")
+    ap.add_argument("--cpu-iters", type=int, default=60,
+                    help="oracle sample: iterations on one image (~10 s of host CPU work)")
     ap.add_argument("--traffic-bytes", type=float, default=None,
                     help="dram bytes per K1 launch from an ncu --set full capture (roofline.traffic)")
     return ap.parse_args()
@@ -179,6 +183,47 @@ def run_reference(args, cfg):
     return 0
 
 
+def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cfg):
+    """Roofline of the dominant kernel (the prior stencil, ~90% of the step).
+
+    achieved = ALGORITHMIC flops (4 N_f m^2 per pixel per evaluation) / the
+    kernel's event-timed duration.  K1 (FFMA2) is bound by the FP32 FMA pipes: peak = SMs x 128
+    lanes x 2 x sm_max_mhz.  K8 (tcgen05 TF32, 3 passes) runs on the tensor cores: peak = the
+    measured sustained bf16 GEMM rate x the nominal TF32/BF16 ratio (1.1/2.25) -- the kernel is
+    timed inside a long step; fp32_frac (against the FP32 FMA peak) is the BASELINE metric's
+    "% of B200 FP32 peak"."""
+    import torch
+    peaks, peak_src = measured_peaks()
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_peak = nsm * 128 * 2 * sm_max * 1e6 / 1e12
+    common = {"achieved": alg_tflops, "unit": "TFLOP/s", "traffic": args.traffic_bytes,
+              "fp32_peak": fp32_peak, "fp32_frac": (alg_tflops / fp32_peak) if alg_tflops else None,
+              "k_ms_per_launch": k_ms / max(k_launches, 1), "k_launches": k_launches,
+              "k_share_of_step": (k_ms / sum(step_ms)) if step_ms else None}
+    if stencil == 2:
+        bf16 = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
+        tf32_peak = bf16 * 1.1 / 2.25
+        m, nf = cfg.m, cfg.n_filters
+        kt, np_ = ((m * m + 7) // 8) * 8, ((nf + 15) // 16) * 16
+        c = (m - 1) // 2
+        ow = 128 - 2 * c
+        # executed tensor flops per output pixel: 3 passes x (fwd KT x NP + bwd NP x KT) x 2 per
+        # response pixel, x (64 + 2C) 128-lane response rows per 64 x OW output tile
+        exec_px = 3 * 2 * 2 * kt * np_ * (64 + 2 * c) * 128 / (64 * ow)
+        alg_px = 4.0 * nf * m * m
+        ex = alg_tflops * exec_px / alg_px if alg_tflops else None
+        return dict(common, bound="tensor", peak=tf32_peak, frac=(alg_tflops / tf32_peak) if alg_tflops else None,
+                    kernel="k_prior_grad_tc (K8: tcgen05 TF32 x3, TMEM accumulators)",
+                    peak_source=f"derived: measured sustained bf16 {bf16:.1f} TFLOP/s x 1.1/2.25 (nominal TF32/BF16), "
+                                f"{peak_src} MEASURED_PEAKS.json",
+                    tensor_executed_tflops=ex, tensor_executed_frac=(ex / tf32_peak) if ex else None)
+    return dict(common, bound="alu", peak=fp32_peak, frac=(alg_tflops / fp32_peak) if alg_tflops else None,
+                kernel="k_prior_grad2 (K1: FFMA2 fused FoE energy+gradient stencil)",
+                peak_source=f"derived: {nsm} SMs x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz "
+                            f"(sm_max_mhz, {peak_src} MEASURED_PEAKS.json) -- DESIGN.md")
+
+
 def config_block(cfg, n_gpus, images_per_gpu, px, args):
     iters = args.iters or cfg.iters
     return {
@@ -279,20 +324,8 @@ def main():
     flops_per_eval_px = 4.0 * cfg.n_filters * cfg.m * cfg.m
     k1_flops = flops_per_eval_px * H * W * trials_per_step * args.steps
     k1_tflops = k1_flops / (k1_ms / 1e3) / 1e12 if k1_ms > 0 else None
-    peaks, peak_src = measured_peaks()
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    fp32_peak = nsm * 128 * 2 * sm_max * 1e6 / 1e12
-    roofline = {
-        "bound": "alu", "achieved": k1_tflops, "peak": fp32_peak, "unit": "TFLOP/s",
-        "frac": (k1_tflops / fp32_peak) if k1_tflops else None,
-        "traffic": args.traffic_bytes,
-        "kernel": "k_prior_grad (K1, fused FoE energy+gradient stencil)",
-        "peak_source": f"derived: {nsm} SMs x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz "
-                       f"(sm_max_mhz, {peak_src} MEASURED_PEAKS.json) -- DESIGN.md",
-        "k1_ms_per_launch": k1_ms / max(k1_launches, 1), "k1_launches": k1_launches,
-        "k1_share_of_step": (k1_ms / sum(step_ms)) if step_ms else None,
-    }
+    roofline = roofline_entry(P.ipiano_state_stencil(st), k1_tflops, k1_ms, k1_launches, step_ms, args, dev, cfg)
+    fp32_peak = roofline["fp32_peak"]
 
     # ---- e2e: the public C-ABI call with host buffers (H2D of f and D2H of u inside)
     e2e = None
@@ -333,7 +366,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "dtype_detail": "fp32 stencil (FFMA), fp64 iterate/prox/reductions",
+            "dtype_detail": DTYPE_DETAIL[P.ipiano_state_stencil(st)],
             "data": "synthetic", "config": config_block(cfg, ws, B, H * W, args),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "trials_per_iter": trials_per_step / (B * cfg.iters),
@@ -423,27 +456,19 @@ def run_slabs(args, cfg):
     flops_px = 4.0 * cfg.n_filters * cfg.m * cfg.m
     k1_flops = flops_px * (r1 - r0) * W * trials_per_step * args.steps
     k1_tflops = k1_flops / (k1_ms / 1e3) / 1e12 if k1_ms > 0 else None
-    peaks, peak_src = measured_peaks()
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    fp32_peak = nsm * 128 * 2 * sm_max * 1e6 / 1e12
+    roof = roofline_entry(P.ipiano_state_stencil(member), k1_tflops, k1_ms, k1_launches, step_ms, args, dev, cfg)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "dtype_detail": "fp32 stencil (FFMA), fp64 iterate/prox/reductions", "data": "synthetic",
+            "dtype_detail": DTYPE_DETAIL[P.ipiano_state_stencil(member)], "data": "synthetic",
             "config": {"workload": f"{cfg.name}: {cfg.description}", "H": Hg, "W": W,
                        "filters": f"{cfg.n_filters}x{cfg.m}x{cfg.m}", "iters": cfg.iters,
                        "slab_rows_per_gpu": r1 - r0,
                        "l2": "inputs (8192^2 fp64 state, 1.6 GB) larger than L2; 256 MiB flush between steps",
                        "parallelism": f"row slabs x{ws}: 6-row ghost exchange (ncclSend/Recv) + band all-gather per trial"},
-            "roofline": {"bound": "alu", "achieved": k1_tflops, "peak": fp32_peak, "unit": "TFLOP/s",
-                         "frac": (k1_tflops / fp32_peak) if k1_tflops else None, "traffic": args.traffic_bytes,
-                         "kernel": "k_prior_grad2 (K1, slab)",
-                         "peak_source": f"derived: {nsm} SMs x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz ({peak_src})",
-                         "k1_ms_per_launch": k1_ms / max(k1_launches, 1), "k1_launches": k1_launches,
-                         "k1_share_of_step": k1_ms / sum(step_ms) if step_ms else None},
+            "roofline": roof,
             "cpu_baseline": None, "e2e": None, "gpu_launches": int(launches), "clocks": clocks,
             "trials_per_iter": trials_per_step / cfg.iters, "lipschitz_ms": lipschitz_ms,
             "status": [int(cnt["status"][0])],

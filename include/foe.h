@@ -62,6 +62,15 @@ typedef enum {
     FOE_DATA_NAKAGAMI = 1  /* Eq.(8): l2 forced to 0, l1 = lambda            */
 } foe_data_term;
 
+/* Kernel of the fused prior energy + gradient (rows a2-a7):
+ *   FOE_STENCIL_FFMA    K1: paired fp32 FMA (FFMA2) correlations out of shared memory
+ *   FOE_STENCIL_TENSOR  K8: tcgen05 tensor cores, TF32 with a 3-pass hi/lo split (fp32-level),
+ *                       m = 7 with N_f <= 48 or m = 5 with N_f <= 32 (else FOE_ERR_UNSUPPORTED)
+ *   FOE_STENCIL_AUTO    K8 where supported and the launch fills the GPU, else K1. */
+#define FOE_STENCIL_AUTO 0
+#define FOE_STENCIL_FFMA 1
+#define FOE_STENCIL_TENSOR 2
+
 /* Limits of this build (kernel-parameter-resident filter taps). */
 #define FOE_MAX_FILTERS 64
 #define FOE_MAX_TAPS 3136  /* n_filters * m * m */
@@ -97,6 +106,10 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
                             const double* lambda, double looks_L, foe_data_term term,
                             int cuda_device, foe_model** out);
 void foe_model_destroy(foe_model* model);
+/* Stencil used by foe_energy_grad with this model (default FOE_STENCIL_AUTO; a tuning and
+ * testing knob: do not change it while another thread uses the model).
+ * FOE_ERR_UNSUPPORTED if the bank has no tensor-core kernel and FOE_STENCIL_TENSOR is asked. */
+foe_status foe_model_set_stencil(foe_model* model, int stencil);
 
 /* ------------------------------------------------------------------ energy / gradient */
 
@@ -143,6 +156,7 @@ typedef struct {
     int record_trace;        /* 1: keep the per-iteration trace on device                             */
     int filter_groups;       /* 0 = automatic; else split the N_f filters over this many CTAs
                                 per tile (partial gradients summed in fixed order)                    */
+    int stencil;             /* prior energy+gradient kernel: FOE_STENCIL_AUTO / _FFMA / _TENSOR     */
 } ipiano_config;
 
 /* Fills the defaults above (graded policy). */
@@ -208,6 +222,9 @@ foe_status ipiano_get_trace(const ipiano_state* st, void* host_trace, size_t byt
 foe_status ipiano_profile(ipiano_state* st, int enable);
 foe_status ipiano_profile_read(ipiano_state* st, double* k1_ms, long long* k1_launches,
                                long long* total_launches);
+
+/* The stencil this state resolved to (FOE_STENCIL_FFMA or FOE_STENCIL_TENSOR). */
+int ipiano_state_stencil(const ipiano_state* st);
 
 void ipiano_state_destroy(ipiano_state* st);
 

@@ -15,6 +15,7 @@
 
 #include "foe.h"
 #include "foe_kernels.cuh"
+#include "foe_tc.cuh"
 
 using foe::ImgCtl;
 using foe::K1Args;
@@ -109,6 +110,22 @@ void k1_dispatch(int m, bool hvp, const K1Args& a, const TapParams& tp, const fo
     }
 }
 
+// K8 (tensor-core stencil): output tile rows (= the 64-row bands of the slab path)
+constexpr int kTcR = 64;
+template <int M, int NP>
+constexpr int tc_smem() { return foe::TcGeom<M, NP, kTcR>::SMEM_BYTES; }
+template <int M, int NP>
+cudaError_t tc_set_attr() {
+    return cudaFuncSetAttribute(foe::k_prior_grad_tc<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                tc_smem<M, NP>());
+}
+// the banks K8 has an instantiation for: (m, padded N_f)
+int tc_np(int m, int nf) {
+    if (m == 7 && nf <= 48) return 48;
+    if (m == 5 && nf <= 32) return 32;
+    return 0;
+}
+
 constexpr int kPxt2 = 8;  // pixels per thread of the pointwise kernels
 
 int div_up(long long a, long long b) { return (int)((a + b - 1) / b); }
@@ -123,6 +140,12 @@ struct foe_model {
     double lam[2] = {0, 0};
     TapParams* tp = nullptr;        // host copy, passed by value to the HVP stencil launches
     foe::TapParams2* tp2 = nullptr; // pair-interleaved taps of the paired-FMA stencil
+    // K8: B operand images (tf32 hi/lo, K-major canonical layout), sum k_i, theta_i ln 2
+    int tc_np = 0;                  // padded N_f of the K8 instantiation (0: no K8 for this bank)
+    float* tc_bimg = nullptr;
+    float* tc_sumk = nullptr;
+    float* tc_thl = nullptr;
+    int stencil = FOE_STENCIL_AUTO; // foe_energy_grad's choice
 };
 
 struct ipiano_state {
@@ -132,6 +155,7 @@ struct ipiano_state {
     ipiano_config cfg{};
     foe::SolverParams sp{};
     int tiles_x = 0, ntiles = 0, groups = 1, nchunks = 0, nblk2 = 0;
+    int kind = FOE_STENCIL_FFMA;  // resolved stencil of this state (K1 or K8)
     double* w = nullptr;      // [3][B][HW]
     float* g = nullptr;       // [2][groups][B][HW]
     float* ft = nullptr;      // [B][HW]
@@ -151,6 +175,55 @@ struct ipiano_state {
     double k1_ms = 0.0;
     long long k1_launches = 0, total_launches = 0;
 };
+
+namespace {
+
+float tf32_host(float x) {  // = cvt.rna.tf32.f32 (round to nearest, ties away from zero)
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & 0xFFFFE000u;
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+}
+
+// K8 operand images (foe_tc.cuh): Kf[t][i] = flipped tap t of filter i (K-major: [t/4][i][t%4]),
+// Kb[i][t] = 2 theta_i k_i[t] for t < NB ([i/4][t][i%4]); each as tf32 hi then lo = tf32(v - hi);
+// then the last tap of Kb (t = m*m - 1, done on CUDA cores) as a plain fp32 vector [NP].
+foe_status build_tc_images(foe_model* md) {
+    const int m = md->m, nf = md->nf, NP = md->tc_np;
+    const int KT = ((m * m + 7) / 8) * 8, NB = (m * m / 8) * 8;
+    const size_t BF = (size_t)KT * NP, BB = (size_t)NP * NB;
+    std::vector<float> img(2 * BF + 2 * BB + NP, 0.0f), sumk(NP, 0.0f), thl(NP, 0.0f);
+    for (int i = 0; i < nf; ++i) {
+        for (int t = 0; t < m * m; ++t) {
+            const float vf = md->tp->fwd[i * m * m + t], vb = md->tp->bwd[i * m * m + t];
+            const size_t of = (size_t)(t / 4) * NP * 4 + (size_t)i * 4 + t % 4;
+            const float fh = tf32_host(vf);
+            img[of] = fh;
+            img[BF + of] = tf32_host(vf - fh);
+            if (t < NB) {
+                const size_t ob = (size_t)(i / 4) * NB * 4 + (size_t)t * 4 + i % 4;
+                const float bh = tf32_host(vb);
+                img[2 * BF + ob] = bh;
+                img[2 * BF + BB + ob] = tf32_host(vb - bh);
+            } else {
+                img[2 * BF + 2 * BB + i] = vb;
+            }
+        }
+        sumk[i] = md->tp->sumk[i];
+        thl[i] = (float)md->tp->theta_ln2[i];
+    }
+    CK(cudaMalloc((void**)&md->tc_bimg, img.size() * sizeof(float)));
+    CK(cudaMalloc((void**)&md->tc_sumk, NP * sizeof(float)));
+    CK(cudaMalloc((void**)&md->tc_thl, NP * sizeof(float)));
+    CK(cudaMemcpy(md->tc_bimg, img.data(), img.size() * sizeof(float), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(md->tc_sumk, sumk.data(), NP * sizeof(float), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(md->tc_thl, thl.data(), NP * sizeof(float), cudaMemcpyHostToDevice));
+    return FOE_OK;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -225,6 +298,8 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
         return fail(FOE_ERR_CUDA, "libfoe is built for sm_100a (B200); device %d is sm_%d%d", cuda_device,
                     prop.major, prop.minor);
     CK(cudaSetDevice(cuda_device));
+    if (tc_np(m, n_filters) == 48) CK((tc_set_attr<7, 48>()));
+    if (tc_np(m, n_filters) == 32) CK((tc_set_attr<5, 32>()));
     switch (m) {
         case 7: CK((k2g_set_attr<7>())); CK((k1_set_attr<7, true>())); break;
         case 5: CK((k2g_set_attr<5>())); CK((k1_set_attr<5, true>())); break;
@@ -269,12 +344,31 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
         md->tp2->sumk[i] = md->tp->sumk[i];
         md->tp2->theta_ln2[i] = md->tp->theta_ln2[i];
     }
+    md->tc_np = tc_np(m, n_filters);
+    if (md->tc_np) {
+        foe_status r = build_tc_images(md);
+        if (r != FOE_OK) { foe_model_destroy(md); return r; }
+    }
     *out = md;
+    return FOE_OK;
+}
+
+foe_status foe_model_set_stencil(foe_model* model, int stencil) {
+    if (!model) return fail(FOE_ERR_INVALID_ARGUMENT, "model is NULL");
+    if (stencil < FOE_STENCIL_AUTO || stencil > FOE_STENCIL_TENSOR)
+        return fail(FOE_ERR_INVALID_ARGUMENT, "unknown stencil %d", stencil);
+    if (stencil == FOE_STENCIL_TENSOR && !model->tc_np)
+        return fail(FOE_ERR_UNSUPPORTED, "no tensor-core stencil for %d filters of %dx%d (m=7: N_f<=48, m=5: N_f<=32)",
+                    model->nf, model->m, model->m);
+    model->stencil = stencil;
     return FOE_OK;
 }
 
 void foe_model_destroy(foe_model* model) {
     if (!model) return;
+    if (model->tc_bimg) cudaFree(model->tc_bimg);
+    if (model->tc_sumk) cudaFree(model->tc_sumk);
+    if (model->tc_thl) cudaFree(model->tc_thl);
     delete model->tp;
     delete model->tp2;
     delete model;
@@ -301,6 +395,55 @@ int choose_groups(const foe_model* md, int ntiles, int B, int requested) {
         if (cost < best - 1e-9) { best = cost; bg = g; }
     }
     return bg;
+}
+
+// Stencil plan of one evaluation over B images of H x W: kernel, tiling and energy partials.
+// H_grid: rows that decide whether a K8 launch fills the GPU (the whole scene for slabs).
+struct Plan {
+    int kind = FOE_STENCIL_FFMA;
+    int tiles_x = 0, ntiles = 0, groups = 1;
+};
+Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref, int req_groups) {
+    Plan p;
+    const int ow = 128 - (md->m - 1);
+    bool tc = md->tc_np != 0 && pref != FOE_STENCIL_FFMA;
+    if (tc && pref == FOE_STENCIL_AUTO)
+        tc = (long long)div_up(W, ow) * div_up(H_grid, kTcR) * B >= 2LL * md->nsm;
+    if (tc) {
+        p.kind = FOE_STENCIL_TENSOR;
+        p.tiles_x = div_up(W, ow);
+        p.ntiles = p.tiles_x * div_up(H, kTcR);
+        p.groups = 1;
+    } else {
+        p.kind = FOE_STENCIL_FFMA;
+        p.tiles_x = div_up(W, kTile);
+        p.ntiles = p.tiles_x * div_up(H, kTile);
+        p.groups = choose_groups(md, p.tiles_x * div_up(H_grid, kTile), B, req_groups);
+    }
+    return p;
+}
+
+// Launch the prior energy+gradient evaluation `a` (tiling fields taken from the plan).
+foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStream_t s) {
+    if (kind == FOE_STENCIL_FFMA) {
+        k1_dispatch(md->m, false, a, *md->tp, *md->tp2, dim3(a.ntiles * a.groups, B), s);
+        CKL("k_prior_grad2");
+        return FOE_OK;
+    }
+    foe::TcArgs ta;
+    ta.k = a;
+    ta.k.groups = 1;
+    ta.bimg = md->tc_bimg;
+    ta.sumk = md->tc_sumk;
+    ta.theta_ln2 = md->tc_thl;
+    ta.tiles_x = a.tiles_x;
+    count_launch(1);
+    if (md->tc_np == 48)
+        foe::k_prior_grad_tc<7, 48, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<7, 48>(), s>>>(ta);
+    else
+        foe::k_prior_grad_tc<5, 32, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<5, 32>(), s>>>(ta);
+    CKL("k_prior_grad_tc");
+    return FOE_OK;
 }
 
 foe_status check_dims(const foe_model* md, int B, int H, int W) {
@@ -331,7 +474,7 @@ bool is_device_ptr(const void* p) {
 // the gradient planes gparts[groups][B][HW].
 foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int W, int groups,
                         double* epart, float* gparts, bool hvp, const double* v, const float* gw,
-                        cudaStream_t s) {
+                        cudaStream_t s, int kind = FOE_STENCIL_FFMA, int tiles_x_tc = 0, int ntiles_tc = 0) {
     K1Args a{};
     a.w = w;
     a.w_slot_stride = 0;
@@ -350,6 +493,14 @@ foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int 
     a.nchunks = div_up(md->nf, Tr<7>::NC);
     a.v = v;
     a.gw = gw;
+    if (!hvp) {
+        if (kind == FOE_STENCIL_TENSOR) {
+            a.tiles_x = tiles_x_tc;
+            a.ntiles = ntiles_tc;
+            a.groups = 1;
+        }
+        return launch_prior(md, kind, a, B, s);
+    }
     dim3 grid(a.ntiles * groups, B);
     k1_dispatch(md->m, hvp, a, *md->tp, *md->tp2, grid, s);
     CKL("k_prior_grad launch");
@@ -370,9 +521,9 @@ foe_status foe_energy_grad(const foe_model* md, const double* w, const float* f,
     CK(cudaSetDevice(md->dev));
     cudaStream_t s = (cudaStream_t)stream;
     const size_t HW = (size_t)H * W;
-    const int tiles = div_up(W, kTile) * div_up(H, kTile);
-    const int groups = choose_groups(md, tiles, B, 0);
-    const int ne = tiles * groups;
+    const Plan pl = plan_stencil(md, B, H, W, H, md->stencil, 0);
+    const int groups = pl.groups;
+    const int ne = pl.ntiles * pl.groups;
     double* epart = nullptr;
     float* gparts = nullptr;
     double* dred = nullptr;
@@ -383,7 +534,8 @@ foe_status foe_energy_grad(const foe_model* md, const double* w, const float* f,
     const bool direct = (groups == 1 && grad != nullptr);
     if (!direct) CK(cudaMallocAsync((void**)&gparts, sizeof(float) * groups * B * HW, s));
     CK(cudaMallocAsync((void**)&dred, sizeof(double) * B * 2, s));
-    st = run_k1_plain(md, w, B, H, W, groups, epart, direct ? grad : gparts, false, nullptr, nullptr, s);
+    st = run_k1_plain(md, w, B, H, W, groups, epart, direct ? grad : gparts, false, nullptr, nullptr, s, pl.kind,
+                      pl.tiles_x, pl.ntiles);
     if (st != FOE_OK) return st;
     if (grad && !direct) {
         const size_t n = (size_t)B * HW;
@@ -521,6 +673,7 @@ void ipiano_config_default(ipiano_config* c) {
     c->w_guard = 40.0;
     c->record_trace = 1;
     c->filter_groups = 0;
+    c->stencil = FOE_STENCIL_AUTO;
 }
 
 }  // extern "C"
@@ -596,8 +749,8 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
         e1 = pool_event(st);
         CK(cudaEventRecord(e0, s));
     }
-    k1_dispatch(st->model->m, false, a1, *st->model->tp, *st->model->tp2, dim3(st->ntiles * st->groups, st->B), s);
-    CKL("k_prior_grad");
+    foe_status rl = launch_prior(st->model, st->kind, a1, st->B, s);
+    if (rl != FOE_OK) return rl;
     if (timed) {
         CK(cudaEventRecord(e1, s));
         st->ev_live.emplace_back(e0, e1);
@@ -713,8 +866,8 @@ foe_status state_init(ipiano_state* st, const float* f, const double* lipschitz_
     count_launch(1);
     CKL("k_init");
     const K1Args a1 = state_k1_args(st, 1);
-    k1_dispatch(st->model->m, false, a1, *st->model->tp, *st->model->tp2, dim3(st->ntiles * st->groups, B), st->s);
-    CKL("k_prior_grad (init)");
+    foe_status rl = launch_prior(st->model, st->kind, a1, B, st->s);
+    if (rl != FOE_OK) return rl;
     foe::k_init_finalize<<<B, kThreads, 0, st->s>>>(st->ctl, st->epart, st->ntiles * st->groups, 1, st->ppart,
                                                     st->nblk2, st->trace, st->cfg.max_iters, st->cfg.record_trace);
     count_launch(1);
@@ -728,6 +881,8 @@ foe_status state_init(ipiano_state* st, const float* f, const double* lipschitz_
 }  // namespace
 
 extern "C" {
+
+int ipiano_state_stencil(const ipiano_state* st) { return st ? st->kind : -1; }
 
 void ipiano_state_destroy(ipiano_state* st) {
     if (!st) return;
@@ -791,10 +946,20 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     st->sp.newton_cap = cfg.newton_max_iters;
     st->sp.record_trace = cfg.record_trace;
     st->sp.max_iters = cfg.max_iters;
-    st->tiles_x = div_up(W, kTile);
-    st->ntiles = st->tiles_x * div_up(H, kTile);
+    if (cfg.stencil < FOE_STENCIL_AUTO || cfg.stencil > FOE_STENCIL_TENSOR) {
+        delete st;
+        return fail(FOE_ERR_INVALID_ARGUMENT, "unknown stencil %d", cfg.stencil);
+    }
+    if (cfg.stencil == FOE_STENCIL_TENSOR && !md->tc_np) {
+        delete st;
+        return fail(FOE_ERR_UNSUPPORTED, "no tensor-core stencil for %d filters of %dx%d", md->nf, md->m, md->m);
+    }
+    const Plan pl = plan_stencil(md, B, H, W, H, cfg.stencil, cfg.filter_groups);
+    st->kind = pl.kind;
+    st->tiles_x = pl.tiles_x;
+    st->ntiles = pl.ntiles;
     st->nchunks = div_up(md->nf, Tr<7>::NC);
-    st->groups = choose_groups(md, st->ntiles, B, cfg.filter_groups);
+    st->groups = pl.groups;
     st->nblk2 = div_up((long long)st->HW, (long long)kThreads * kPxt2);
     auto cleanup = [&](foe_status s) { ipiano_state_destroy(st); return s; };
 #define CKS(call)                                                                    \
@@ -1192,9 +1357,8 @@ foe_status slab_round(ipiano_slabs* g, bool timed) {
             e1 = pool_event(st);
             CK(cudaEventRecord(e0, g->s));
         }
-        k1_dispatch(st->model->m, false, slab_k1_args(g, (int)j, 0), *st->model->tp, *st->model->tp2,
-                    dim3(st->ntiles * st->groups, 1), g->s);
-        CKL("k_prior_grad (slab)");
+        foe_status rl = launch_prior(st->model, st->kind, slab_k1_args(g, (int)j, 0), 1, g->s);
+        if (rl != FOE_OK) return rl;
         if (timed) {
             CK(cudaEventRecord(e1, g->s));
             st->ev_live.emplace_back(e0, e1);
@@ -1248,9 +1412,8 @@ foe_status slab_init(ipiano_slabs* g, const float* f, double L_init, cudaStream_
     if (r != FOE_OK) return r;
     for (size_t j = 0; j < g->members.size(); ++j) {
         ipiano_state* st = g->members[j];
-        k1_dispatch(st->model->m, false, slab_k1_args(g, (int)j, 1), *st->model->tp, *st->model->tp2,
-                    dim3(st->ntiles * st->groups, 1), g->s);
-        CKL("k_prior_grad (slab init)");
+        foe_status rl = launch_prior(st->model, st->kind, slab_k1_args(g, (int)j, 1), 1, g->s);
+        if (rl != FOE_OK) return rl;
     }
     if ((r = slab_bands(g)) != FOE_OK) return r;
     for (size_t j = 0; j < g->members.size(); ++j) {
@@ -1395,11 +1558,17 @@ foe_status ipiano_slabs_create(const foe_model* md, const float* f, int H_global
     g->W = W;
     g->Hg = H_global;
     const int nmem = comm ? 1 : nslabs;
-    const int tiles_x = div_up(W, kTile);
-    const int groups = choose_groups(md, tiles_x * div_up(H_global, kTile), 1, cfg_in ? cfg_in->filter_groups : 0);
+    const int pref = cfg_in ? cfg_in->stencil : FOE_STENCIL_AUTO;
+    if (pref == FOE_STENCIL_TENSOR && !md->tc_np) {
+        delete g;
+        return fail(FOE_ERR_UNSUPPORTED, "no tensor-core stencil for %d filters of %dx%d", md->nf, md->m, md->m);
+    }
+    // one plan for the whole scene, so that every slab (and every slab count) runs the same kernel
+    const Plan pl = plan_stencil(md, 1, H_global / nslabs, W, H_global, pref, cfg_in ? cfg_in->filter_groups : 0);
+    const int groups = pl.groups;
     g->nb_local = g->Hs / foe::kBandRows;
     g->nb_global = H_global / foe::kBandRows;
-    g->e_per_band = tiles_x * groups;
+    g->e_per_band = pl.tiles_x * groups;   // K1 and K8 tiles are both 64 rows high: one tile row per band
     g->bpb = foe::kBandRows * W / (kThreads * kPxt2);
     CK(cudaStreamCreateWithFlags(&g->s, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g->sync_ev, cudaEventDisableTiming));
@@ -1412,6 +1581,7 @@ foe_status ipiano_slabs_create(const foe_model* md, const float* f, int H_global
     ipiano_config cfg;
     if (cfg_in) cfg = *cfg_in; else ipiano_config_default(&cfg);
     cfg.filter_groups = groups;
+    cfg.stencil = pl.kind;
     // members: per-slab iPiano states of one image (B = 1) sharing the group's stream.
     // ipiano_state_create evaluates w^0 with periodic wrap; slab_init below redoes it with halos.
     const size_t HWs = (size_t)g->Hs * W;

@@ -21,6 +21,7 @@ STATUS_NAMES = {
     7: "FOE_ERR_DOMAIN", 8: "FOE_ERR_COMM", 9: "FOE_ERR_UNSUPPORTED",
 }
 FOE_DATA_COMBINED, FOE_DATA_NAKAGAMI = 0, 1
+FOE_STENCIL_AUTO, FOE_STENCIL_FFMA, FOE_STENCIL_TENSOR = 0, 1, 2
 TRACE_FIELDS = ("F", "G", "H", "L", "trials", "margin", "newton", "relchg")
 
 EXPORTED = (
@@ -28,8 +29,8 @@ EXPORTED = (
     "foe_energy_grad", "foe_hvp", "foe_estimate_lipschitz", "ipiano_config_default",
     "ipiano_state_create", "ipiano_state_reset", "ipiano_step", "ipiano_solve", "ipiano_get_iterate",
     "ipiano_get_counters", "ipiano_get_trace", "ipiano_profile", "ipiano_profile_read",
-    "ipiano_state_destroy", "ipiano_run",
-    "foe_comm_unique_id", "foe_comm_create", "foe_comm_destroy", "ipiano_slabs_create", "ipiano_slabs_reset",
+    "ipiano_state_destroy", "ipiano_state_stencil", "ipiano_run",
+    "foe_model_set_stencil", "foe_comm_unique_id", "foe_comm_create", "foe_comm_destroy", "ipiano_slabs_create", "ipiano_slabs_reset",
     "ipiano_slabs_solve", "ipiano_slabs_get_iterate", "ipiano_slabs_member", "ipiano_slabs_destroy",
 )
 
@@ -47,6 +48,7 @@ class IPianoConfig(C.Structure):
         ("shrink", C.c_double), ("max_iters", C.c_int), ("max_backtracks", C.c_int),
         ("newton_max_iters", C.c_int), ("newton_tol", C.c_double), ("rel_change_tol", C.c_double),
         ("w_guard", C.c_double), ("record_trace", C.c_int), ("filter_groups", C.c_int),
+        ("stencil", C.c_int),
     ]
 
 
@@ -88,10 +90,13 @@ def lib():
     L.ipiano_get_trace.argtypes = [_vp, _vp, C.c_size_t]
     L.ipiano_profile.argtypes = [_vp, C.c_int]
     L.ipiano_profile_read.argtypes = [_vp, _dp, _llp, _llp]
+    L.ipiano_state_stencil.argtypes = [_vp]
+    L.ipiano_state_stencil.restype = C.c_int
     L.ipiano_state_destroy.argtypes = [_vp]
     L.ipiano_state_destroy.restype = None
     L.ipiano_run.argtypes = [_vp, _vp, C.c_int, C.c_int, C.c_int, _dp, _dp, C.POINTER(IPianoConfig),
                              _vp, _vp, C.c_size_t, _vp]
+    L.foe_model_set_stencil.argtypes = [_vp, C.c_int]
     L.foe_comm_unique_id.argtypes = [_vp]
     L.foe_comm_create.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]
     L.foe_comm_destroy.argtypes = [_vp]
@@ -221,6 +226,11 @@ def foe_model_create(filters, alphas, lam: Optional[Sequence[float]] = None, loo
 
 def foe_model_destroy(model: Model):
     model.destroy()
+
+
+def foe_model_set_stencil(model: Model, stencil: int):
+    """FOE_STENCIL_AUTO / _FFMA (K1) / _TENSOR (K8) for foe_energy_grad with this model."""
+    _check(lib().foe_model_set_stencil(model.handle, int(stencil)))
 
 
 # ----------------------------------------------------------------- energy/gradient
@@ -378,6 +388,11 @@ def ipiano_profile_read(state: State):
     ms = C.c_double(); n = C.c_longlong(); tot = C.c_longlong()
     _check(lib().ipiano_profile_read(state.handle, C.byref(ms), C.byref(n), C.byref(tot)))
     return ms.value, n.value, tot.value
+
+
+def ipiano_state_stencil(state: State) -> int:
+    """FOE_STENCIL_FFMA (K1) or FOE_STENCIL_TENSOR (K8): the prior kernel this state runs."""
+    return int(lib().ipiano_state_stencil(state.handle))
 
 
 def ipiano_state_destroy(state: State):
