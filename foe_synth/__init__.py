@@ -29,7 +29,7 @@ from typing import Dict, List, Optional, Sequence, Tuple
 import numpy as np
 
 __all__ = [
-    "LAMBDA_PRESETS", "POLICY", "Config", "CONFIGS", "config", "rng",
+    "LAMBDA_PRESETS", "IDIV_U_RMS", "idiv_lambda", "POLICY", "Config", "CONFIGS", "config", "rng",
     "piecewise_smooth_scene", "sar_like_scene", "add_speckle",
     "random_filter_bank", "dct_filter_bank", "lipschitz_start_vector",
     "make_inputs",
@@ -44,6 +44,17 @@ LAMBDA_PRESETS: Dict[int, Tuple[float, float]] = {
     5: (50.0, 0.15),
     8: (550.0, 0.02),
 }
+
+# Variant model (6) (I-divergence): the paper tuned lambda by hand and
+# prints none.  Reading R-18: lambda = lambda_1 / u_rms^2, which gives Eq.(5)
+# the curvature of model (8)'s data term at u = f = u_rms; u_rms = 120.4 is the clean RMS that
+# reproduces Table II's noisy PSNR row (reading R-14).
+IDIV_U_RMS = 120.4
+
+
+def idiv_lambda(L: int) -> float:
+    return LAMBDA_PRESETS[L][0] / (IDIV_U_RMS * IDIV_U_RMS)
+
 
 # iPiano step policy used for every graded configuration (reading R-9):
 # doubling backtracking, L never shrinks, beta = 0.4, safety 0.95

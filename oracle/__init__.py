@@ -96,6 +96,19 @@ def lib():
             L.orc_estimate_lipschitz.argtypes = [fp, C.c_int, C.c_int, dp, dp, C.c_int, C.c_int,
                                                  dp, C.c_int, dp]
             L.orc_estimate_lipschitz.restype = C.c_double
+            L.orc_idiv_energy.argtypes = [dp, dp, C.c_int, C.c_int, C.c_double]
+            L.orc_idiv_energy.restype = C.c_double
+            L.orc_idiv_prox_pixel.argtypes = [C.c_double] * 4
+            L.orc_idiv_prox_pixel.restype = C.c_double
+            L.orc_hvp_u.argtypes = [dp, dp, C.c_int, C.c_int, dp, dp, C.c_int, C.c_int, dp]
+            L.orc_ipiano_trial_u.argtypes = [dp, dp, dp, C.c_double, C.c_double, dp, C.c_int, C.c_int,
+                                             dp, dp, C.c_int, C.c_int, C.c_double,
+                                             C.POINTER(OrcCfg), dp, dp, dp, dp]
+            L.orc_ipiano_run_u.argtypes = [fp, C.c_int, C.c_int, dp, dp, C.c_int, C.c_int, C.c_double,
+                                           C.POINTER(OrcCfg), dp, dp, ip, ip]
+            L.orc_estimate_lipschitz_u.argtypes = [fp, C.c_int, C.c_int, dp, dp, C.c_int, C.c_int,
+                                                   dp, C.c_int, dp]
+            L.orc_estimate_lipschitz_u.restype = C.c_double
             L.orc_num_threads.restype = C.c_int
             _lib = L
     return _lib
@@ -256,6 +269,65 @@ def estimate_lipschitz(f, filters, theta, v0, iters=25):
     rho_hat = lib().orc_estimate_lipschitz(_ptr(f, C.c_float), H, W, _ptr(k), _ptr(th),
                                            k.shape[0], k.shape[1], _ptr(v0), int(iters),
                                            C.byref(Lp))
+    return rho_hat, Lp.value
+
+
+# ------------------------------------------------- variant model (6) in u (f2, I-divergence)
+
+def idiv_energy(u, ft, lam) -> float:
+    """D(u,f) = (lam/2) <u^2 - 2 f^2 log u, 1> (Eq.(5))."""
+    u, ft = _d(u), _d(ft)
+    return float(lib().orc_idiv_energy(_ptr(u), _ptr(ft), u.shape[0], u.shape[1], float(lam)))
+
+
+def idiv_prox_pixel(uhat, ft, tau, lam) -> float:
+    """Closed-form prox of tau D."""
+    return float(lib().orc_idiv_prox_pixel(float(uhat), float(ft), float(tau), float(lam)))
+
+
+def hvp_u(u, v, filters, theta) -> np.ndarray:
+    """Hess F(u) v = sum_i theta_i K_i^T [rho''(K_i u) (.) K_i v]."""
+    u, v, k, th = _d(u), _d(v), _d(filters), _d(theta)
+    out = np.empty_like(u)
+    lib().orc_hvp_u(_ptr(u), _ptr(v), u.shape[0], u.shape[1], _ptr(k), _ptr(th), k.shape[0], k.shape[1],
+                    _ptr(out))
+    return out
+
+
+def ipiano_trial_u(u, uprev, g, F, L, f, filters, theta, lam, cfg: OrcCfg):
+    """One iPiano trial of model (6) in u."""
+    u, uprev, g = _d(u), _d(uprev), _d(g)
+    ft = ftilde(f)
+    k, th = _d(filters), _d(theta)
+    uhat, uplus, gplus, out = np.empty_like(u), np.empty_like(u), np.empty_like(u), np.empty(8)
+    lib().orc_ipiano_trial_u(_ptr(u), _ptr(uprev), _ptr(g), float(F), float(L), _ptr(ft), u.shape[0],
+                             u.shape[1], _ptr(k), _ptr(th), k.shape[0], k.shape[1], float(lam), C.byref(cfg),
+                             _ptr(uhat), _ptr(uplus), _ptr(gplus), _ptr(out))
+    return dict(uhat=uhat, uplus=uplus, gplus=gplus, Fplus=out[0], gdelta=out[1], dd=out[2], Gplus=out[3],
+                margin=out[4], accepted=bool(out[5]), uu=out[7])
+
+
+def ipiano_run_u(f, filters, theta, lam, cfg: OrcCfg):
+    """Model (6) on one image; returns dict(u, trace, iters, trials, status)."""
+    f = np.ascontiguousarray(f, np.float32)
+    H, W = f.shape
+    k, th = _d(filters), _d(theta)
+    u = np.empty((H, W))
+    trace = np.zeros((cfg.max_iters + 1, TR_FIELDS))
+    it, tt = C.c_int(), C.c_int()
+    st = lib().orc_ipiano_run_u(_ptr(f, C.c_float), H, W, _ptr(k), _ptr(th), k.shape[0], k.shape[1],
+                                float(lam), C.byref(cfg), _ptr(u), _ptr(trace), C.byref(it), C.byref(tt))
+    return dict(u=u, trace=trace[: it.value + 1], iters=it.value, trials=tt.value, status=st)
+
+
+def estimate_lipschitz_u(f, filters, theta, v0, iters=25):
+    """Model (6): |Rayleigh quotient| of Hess F(u^0), u^0 = f~; (rho_hat, 2^ceil(log2 rho_hat))."""
+    f = np.ascontiguousarray(f, np.float32)
+    H, W = f.shape
+    k, th, v0 = _d(filters), _d(theta), _d(v0)
+    Lp = C.c_double()
+    rho_hat = lib().orc_estimate_lipschitz_u(_ptr(f, C.c_float), H, W, _ptr(k), _ptr(th), k.shape[0],
+                                             k.shape[1], _ptr(v0), int(iters), C.byref(Lp))
     return rho_hat, Lp.value
 
 

@@ -76,3 +76,17 @@ def prox_bisect(what, ft, tau, l1, l2, iters=200):
         else:
             lo = mid
     return 0.5 * (lo + hi)
+
+
+def hessian_u(u, filters, theta) -> np.ndarray:
+    """Dense Hessian of F(u) = E_FoE(u) (model (6)): sum_i theta_i K_i^T diag(rho''(K_i u)) K_i."""
+    u = np.asarray(u, np.float64)
+    H, W = u.shape
+    x = u.ravel()
+    M = np.zeros((H * W, H * W))
+    for k, th in zip(filters, theta):
+        K = conv_matrix(k, H, W)
+        r = K @ x
+        rpp = 2 * (1 - r * r) / (1 + r * r) ** 2
+        M += float(th) * (K.T @ (rpp[:, None] * K))
+    return M

@@ -18,6 +18,8 @@
  *                           G(w) = (l1/2)<2w + f^2 e^{-2w},1> + (l2/2)<e^{2w} - 2 f^2 w,1>
  *   PAPER.md:185-192 Eq.(9)  prox of G solved by Newton's method
  *   PAPER.md:162-166        iPiano: w+ = (I + a dG)^{-1}(w - a grad F(w) + b (w - w-))
+ *   PAPER.md:143-150, :194-204  variant model (6) in u: D = (lambda/2)<u^2 - 2f^2 log u,1>,
+ *                           closed-form prox (FOE_DATA_IDIV on the GPU side)
  *   SPEC.md:287              backtracking on the descent-lemma inequality
  *
  * Readings where the paper is silent are listed in DESIGN.md (R-1 .. R-17) and
@@ -455,6 +457,182 @@ double orc_estimate_lipschitz(const float* f, int H, int W, const double* k, con
     const double rho = fabs(rq);
     if (L_pow2) *L_pow2 = ldexp(1.0, (int)ceil(log2(rho)));
     free(w); free(v); free(h); free(t); free(rowbuf);
+    return rho;
+}
+
+/* -------------------------------------------------------------------------------- */
+/* Variant model (6) in u: I-divergence data term         */
+/* -------------------------------------------------------------------------------- */
+
+/* D(u,f) = (lambda/2) <u^2 - 2 f^2 log u, 1> (Eq.(5)); u > 0 (else NaN). */
+double orc_idiv_energy(const double* u, const double* ft, int H, int W, double lam)
+{
+    const size_t N = (size_t)H * W;
+    double* t = (double*)malloc(sizeof(double) * N);
+    double* rowbuf = (double*)malloc(sizeof(double) * (size_t)H);
+    for (size_t p = 0; p < N; ++p)
+        t[p] = u[p] > 0.0 ? 0.5 * lam * (u[p] * u[p] - 2.0 * ft[p] * ft[p] * log(u[p])) : NAN;
+    const double e = sum_rows(t, H, W, rowbuf);
+    free(t); free(rowbuf);
+    return e;
+}
+
+/* (I + tau dG)^{-1}(uhat), pointwise closed form:
+ *   u_p = (uhat_p + sqrt(uhat_p^2 + 4 (1 + tau lam) tau lam f_p^2)) / (2 (1 + tau lam)). */
+double orc_idiv_prox_pixel(double uhat, double ft, double tau, double lam)
+{
+    const double tl = tau * lam;
+    return (uhat + sqrt(uhat * uhat + 4.0 * (1.0 + tl) * tl * ft * ft)) / (2.0 * (1.0 + tl));
+}
+
+/* Hessian-vector product of F(u) = E_FoE(u): sum_i theta_i K_i^T [rho''(K_i u) (.) K_i v] */
+int orc_hvp_u(const double* u, const double* v, int H, int W, const double* k,
+              const double* theta, int nf, int m, double* hv)
+{
+    const size_t N = (size_t)H * W;
+    double* r = (double*)malloc(sizeof(double) * N);
+    double* t = (double*)malloc(sizeof(double) * N);
+    double* q = (double*)malloc(sizeof(double) * N);
+    memset(hv, 0, sizeof(double) * N);
+    for (int i = 0; i < nf; ++i) {
+        const double* ki = k + (size_t)i * m * m;
+        orc_conv(u, H, W, ki, m, r);                          /* K_i u  */
+        orc_conv(v, H, W, ki, m, t);                          /* K_i v  */
+        for (size_t p = 0; p < N; ++p) t[p] *= orc_rho_second(r[p]);
+        orc_conv_adj(t, H, W, ki, m, q);
+        for (size_t p = 0; p < N; ++p) hv[p] += theta[i] * q[p];
+    }
+    free(r); free(t); free(q);
+    return ORC_OK;
+}
+
+/* One iPiano trial of model (6) in u, as orc_ipiano_trial
+ * with grad_u F, the closed-form prox and D of Eq.(5).  out[8] as orc_ipiano_trial
+ * (out[6] = 0: no Newton). */
+int orc_ipiano_trial_u(const double* u, const double* uprev, const double* g, double F, double L,
+                       const double* ft, int H, int W, const double* k, const double* theta,
+                       int nf, int m, double lam, const orc_cfg* cfg,
+                       double* uhat_out, double* uplus, double* gplus, double* out)
+{
+    const size_t N = (size_t)H * W;
+    const double alpha = cfg->step_safety * 2.0 * (1.0 - cfg->beta) / L;
+    double* uhat = uhat_out ? uhat_out : (double*)malloc(sizeof(double) * N);
+    double* t = (double*)malloc(sizeof(double) * N);
+    double* rowbuf = (double*)malloc(sizeof(double) * (size_t)H);
+    for (size_t p = 0; p < N; ++p) {
+        uhat[p] = u[p] - alpha * g[p] + cfg->beta * (u[p] - uprev[p]);
+        uplus[p] = orc_idiv_prox_pixel(uhat[p], ft[p], alpha, lam);
+    }
+    double Fp = NAN;
+    orc_energy_grad_u(uplus, H, W, k, theta, nf, m, &Fp, gplus);
+    for (size_t p = 0; p < N; ++p) t[p] = g[p] * (uplus[p] - u[p]);
+    const double gd = sum_rows(t, H, W, rowbuf);
+    for (size_t p = 0; p < N; ++p) t[p] = (uplus[p] - u[p]) * (uplus[p] - u[p]);
+    const double dd = sum_rows(t, H, W, rowbuf);
+    for (size_t p = 0; p < N; ++p) t[p] = u[p] * u[p];
+    const double uu = sum_rows(t, H, W, rowbuf);
+    const double Gp = orc_idiv_energy(uplus, ft, H, W, lam);
+    const double margin = F + gd + 0.5 * L * dd - Fp;
+    const int ok = isfinite(Fp) && isfinite(gd) && isfinite(dd) && isfinite(Gp) && margin >= 0.0;
+    if (out) {
+        out[0] = Fp; out[1] = gd; out[2] = dd; out[3] = Gp; out[4] = margin;
+        out[5] = ok ? 1.0 : 0.0; out[6] = 0.0; out[7] = uu;
+    }
+    if (!uhat_out) free(uhat);
+    free(t); free(rowbuf);
+    return ORC_OK;
+}
+
+/* Full run of model (6): u^0 = f~, u^{-1} = u^0 [R-8], L = L_init; the
+ * same backtracking, acceptance, trace and stopping rules as orc_ipiano_run_ex.  The
+ * guard [R-11] becomes: an accepted iterate must be finite and positive. */
+int orc_ipiano_run_u(const float* f, int H, int W, const double* k, const double* theta,
+                     int nf, int m, double lam, const orc_cfg* cfg,
+                     double* u_out, double* trace, int* iters_run, int* total_trials)
+{
+    const size_t N = (size_t)H * W;
+    double* ft = (double*)malloc(sizeof(double) * N);
+    double* u = (double*)malloc(sizeof(double) * N);
+    double* up = (double*)malloc(sizeof(double) * N);
+    double* un = (double*)malloc(sizeof(double) * N);
+    double* g = (double*)malloc(sizeof(double) * N);
+    double* gn = (double*)malloc(sizeof(double) * N);
+    int st = ORC_OK, n = 0, trials_total = 0;
+    for (size_t p = 0; p < N; ++p) {
+        ft[p] = fmax((double)f[p], 1.0);                  /* f~ = max(f,1)   [R-4] */
+        u[p] = ft[p];                                     /* u^0 = f~ */
+        up[p] = u[p];                                     /* u^{-1} = u^0    [R-8] */
+    }
+    double F;
+    orc_energy_grad_u(u, H, W, k, theta, nf, m, &F, g);
+    double L = cfg->lipschitz_init;
+    if (trace) {
+        double* r0 = trace;
+        r0[TR_F] = F; r0[TR_G] = orc_idiv_energy(u, ft, H, W, lam); r0[TR_H] = F + r0[TR_G];
+        r0[TR_L] = L; r0[TR_TRIALS] = 0; r0[TR_MARGIN] = 0; r0[TR_NEWTON] = 0; r0[TR_RELCHG] = 0;
+    }
+    if (!isfinite(F)) st = ORC_ERR_NONFINITE;
+    while (st == ORC_OK && n < cfg->max_iters) {
+        int trials = 0;
+        double out[8];
+        for (;;) {
+            ++trials; ++trials_total;
+            orc_ipiano_trial_u(u, up, g, F, L, ft, H, W, k, theta, nf, m, lam, cfg, NULL, un, gn, out);
+            if (out[5] != 0.0) break;
+            if (trials > cfg->max_backtracks) { st = ORC_ERR_BACKTRACK; break; }
+            L *= cfg->backtrack_factor;                   /* double L_n */
+        }
+        if (st != ORC_OK) break;
+        for (size_t p = 0; p < N; ++p)
+            if (!(un[p] > 0.0) || !isfinite(un[p])) { st = isfinite(un[p]) ? ORC_ERR_DOMAIN : ORC_ERR_NONFINITE; break; }
+        double* tmp = up; up = u; u = un; un = tmp;
+        tmp = g; g = gn; gn = tmp;
+        F = out[0];
+        ++n;
+        const double relchg = sqrt(out[2]) / fmax(sqrt(out[7]), 1.0);
+        if (trace) {
+            double* r = trace + (size_t)n * TR_FIELDS;
+            r[TR_F] = F; r[TR_G] = out[3]; r[TR_H] = F + out[3]; r[TR_L] = L;
+            r[TR_TRIALS] = trials; r[TR_MARGIN] = out[4]; r[TR_NEWTON] = 0;
+            r[TR_RELCHG] = relchg;
+        }
+        L *= cfg->shrink;                                 /* [R-9] */
+        if (cfg->rel_change_tol > 0.0 && relchg < cfg->rel_change_tol) break;
+    }
+    memcpy(u_out, u, sizeof(double) * N);
+    if (iters_run) *iters_run = n;
+    if (total_trials) *total_trials = trials_total;
+    free(ft); free(u); free(up); free(un); free(g); free(gn);
+    return st;
+}
+
+/* Lipschitz estimate of model (6) [R-10 applied in u]: power iteration on the Hessian of
+ * F(u) at u^0 = f~. */
+double orc_estimate_lipschitz_u(const float* f, int H, int W, const double* k, const double* theta,
+                                int nf, int m, const double* v0, int iters, double* L_pow2)
+{
+    const size_t N = (size_t)H * W;
+    double* u = (double*)malloc(sizeof(double) * N);
+    double* v = (double*)malloc(sizeof(double) * N);
+    double* h = (double*)malloc(sizeof(double) * N);
+    double* t = (double*)malloc(sizeof(double) * N);
+    double* rowbuf = (double*)malloc(sizeof(double) * (size_t)H);
+    for (size_t p = 0; p < N; ++p) u[p] = fmax((double)f[p], 1.0);
+    for (size_t p = 0; p < N; ++p) t[p] = v0[p] * v0[p];
+    double nv = sqrt(sum_rows(t, H, W, rowbuf));
+    for (size_t p = 0; p < N; ++p) v[p] = v0[p] / nv;
+    double rq = 0.0;
+    for (int it = 0; it < iters; ++it) {
+        orc_hvp_u(u, v, H, W, k, theta, nf, m, h);
+        for (size_t p = 0; p < N; ++p) t[p] = v[p] * h[p];
+        rq = sum_rows(t, H, W, rowbuf);
+        for (size_t p = 0; p < N; ++p) t[p] = h[p] * h[p];
+        const double nh = sqrt(sum_rows(t, H, W, rowbuf));
+        for (size_t p = 0; p < N; ++p) v[p] = h[p] / nh;
+    }
+    const double rho = fabs(rq);
+    if (L_pow2) *L_pow2 = ldexp(1.0, (int)ceil(log2(rho)));
+    free(u); free(v); free(h); free(t); free(rowbuf);
     return rho;
 }
 
