@@ -179,7 +179,7 @@ def run_reference(args, cfg):
                          "sample": r["sample"]},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -239,7 +239,31 @@ def config_block(cfg, n_gpus, images_per_gpu, px, args):
 
 # ------------------------------------------------------------------------------ main
 
+_JSON_OUT = None
+
+
+def emit(line: dict):
+    """The one JSON line of this run, on the process's real stdout."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
+def _isolate_stdout():
+    """Send everything else written to fd 1 (NCCL's version banner, library prints) to stderr,
+    so that stdout carries exactly the one JSON line the driver parses."""
+    global _JSON_OUT
+    try:
+        sys.stdout.flush()
+        real = os.dup(1)
+        os.dup2(2, 1)
+        _JSON_OUT = os.fdopen(real, "w")
+    except OSError:
+        _JSON_OUT = None
+
+
 def main():
+    _isolate_stdout()
     args = parse_args()
     import foe_synth as S
     cfg = S.config(args.config)
@@ -374,7 +398,7 @@ def main():
                              / fp32_peak / ws,
             "lipschitz_ms": lipschitz_ms, "status": [int(s) for s in set(cnt["status"].tolist())],
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     st.destroy()
     md.destroy()
     D.barrier()
@@ -473,7 +497,7 @@ def run_slabs(args, cfg):
             "trials_per_iter": trials_per_step / cfg.iters, "lipschitz_ms": lipschitz_ms,
             "status": [int(cnt["status"][0])],
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     sl.destroy()
     comm.destroy()
     md.destroy()

@@ -59,7 +59,11 @@ typedef enum {
 
 typedef enum {
     FOE_DATA_COMBINED = 0, /* Eq.(10): l1, l2 as given                                         */
-    FOE_DATA_NAKAGAMI = 1  /* Eq.(8): l2 forced to 0, l1 = lambda            */
+    FOE_DATA_NAKAGAMI = 1, /* Eq.(8): l2 forced to 0, l1 = lambda            */
+    FOE_DATA_IDIV = 2      /* model (6): iterate u (not w = log u),
+                              D(u,f) = (lambda/2)<u^2 - 2 f^2 log u, 1>, lambda = lambda[0]
+                              (lambda[1] ignored; no preset: the paper prints none), grad_u F
+                              without W, closed-form prox; u^0 = max(f,1)       */
 } foe_data_term;
 
 /* Kernel of the fused prior energy + gradient (rows a2-a7):
@@ -96,7 +100,8 @@ typedef struct foe_model foe_model;
  *            L=1 (160,0.004); L=5 (50,0.15))
  *   looks_L  number of looks L; required (1, 3, 5 or 8) iff lambda == NULL, else informational
  *            (L is folded into lambda, R-5)
- *   term     FOE_DATA_COMBINED or FOE_DATA_NAKAGAMI
+ *   term     FOE_DATA_COMBINED, FOE_DATA_NAKAGAMI or FOE_DATA_IDIV.  For FOE_DATA_IDIV every
+ *            "w" below is the iterate u itself (device fp64), and lambda must be given
  *   cuda_device  CUDA ordinal the model's kernels run on
  * Errors: FOE_ERR_INVALID_ARGUMENT (m even/< 3, n_filters < 1 or > FOE_MAX_FILTERS,
  * n_filters*m*m > FOE_MAX_TAPS, theta_i <= 0 or non-finite (message names filter i),
@@ -228,7 +233,11 @@ int ipiano_state_stencil(const ipiano_state* st);
 
 void ipiano_state_destroy(ipiano_state* st);
 
-/* One-shot convenience: state_create + solve + get_iterate + get_trace + destroy.
+/* One-shot convenience: state_create + solve + get_iterate + get_trace + destroy.  The model
+ * keeps one solver workspace (state + host-I/O staging buffers) for repeated calls of the same
+ * B, H, W and configuration, so that a call after the first does no device allocation (a call
+ * concurrent with another on the same model uses a private workspace); foe_model_destroy
+ * frees it.
  *   f      fp32 [B][H][W], host OR device (detected); host buffers are copied in/out on
  *          `stream` inside the call
  *   u_out  fp32 [B][H][W] = e^w, host or device

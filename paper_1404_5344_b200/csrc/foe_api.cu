@@ -5,6 +5,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -146,6 +147,13 @@ struct foe_model {
     float* tc_sumk = nullptr;
     float* tc_thl = nullptr;
     int stencil = FOE_STENCIL_AUTO; // foe_energy_grad's choice
+    // ipiano_run's reusable workspace (one solver state + host-I/O staging buffers), kept for
+    // repeated calls of the same shape and configuration; guarded by run_mu (a concurrent call
+    // falls back to a private workspace)
+    mutable std::mutex run_mu;
+    mutable ipiano_state* run_state = nullptr;
+    mutable float* io_buf = nullptr;   // [2][n] device staging of host f and u
+    mutable size_t io_n = 0;
 };
 
 struct ipiano_state {
@@ -153,6 +161,7 @@ struct ipiano_state {
     int B = 0, H = 0, W = 0;
     size_t HW = 0;
     ipiano_config cfg{};
+    ipiano_config cfg_in{};   // the configuration as the caller passed it (ipiano_run's cache key)
     foe::SolverParams sp{};
     int tiles_x = 0, ntiles = 0, groups = 1, nchunks = 0, nblk2 = 0;
     int kind = FOE_STENCIL_FFMA;  // resolved stencil of this state (K1 or K8)
@@ -262,8 +271,10 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
         return fail(FOE_ERR_INVALID_ARGUMENT, "n_filters=%d outside [1,%d]", n_filters, foe::kMaxFilters);
     if ((long long)n_filters * m * m > foe::kMaxTaps)
         return fail(FOE_ERR_INVALID_ARGUMENT, "n_filters*m*m=%d exceeds %d", n_filters * m * m, foe::kMaxTaps);
-    if (term != FOE_DATA_COMBINED && term != FOE_DATA_NAKAGAMI)
+    if (term != FOE_DATA_COMBINED && term != FOE_DATA_NAKAGAMI && term != FOE_DATA_IDIV)
         return fail(FOE_ERR_INVALID_ARGUMENT, "unknown data term %d", (int)term);
+    if (term == FOE_DATA_IDIV && !lambda)
+        return fail(FOE_ERR_INVALID_ARGUMENT, "FOE_DATA_IDIV needs an explicit lambda (PAPER.md:231 prints none)");
     for (int i = 0; i < n_filters; ++i) {
         if (!(alphas[i] > 0.0f) || !std::isfinite(alphas[i]))
             return fail(FOE_ERR_INVALID_ARGUMENT, "non-positive weight at filter %d (theta=%g)", i, (double)alphas[i]);
@@ -283,7 +294,7 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
         else if (looks_L == 5) { lam[0] = 50; lam[1] = 0.15; }
         else return fail(FOE_ERR_INVALID_ARGUMENT, "lambda is NULL and looks_L=%g has no preset (1,3,5,8)", looks_L);
     }
-    if (term == FOE_DATA_NAKAGAMI) lam[1] = 0.0;
+    if (term == FOE_DATA_NAKAGAMI || term == FOE_DATA_IDIV) lam[1] = 0.0;
     if (!(lam[0] >= 0) || !(lam[1] >= 0) || !std::isfinite(lam[0]) || !std::isfinite(lam[1]) ||
         (lam[0] == 0 && lam[1] == 0))
         return fail(FOE_ERR_INVALID_ARGUMENT, "lambda=(%g,%g) must be finite, >= 0 and not both 0", lam[0], lam[1]);
@@ -366,6 +377,8 @@ foe_status foe_model_set_stencil(foe_model* model, int stencil) {
 
 void foe_model_destroy(foe_model* model) {
     if (!model) return;
+    if (model->run_state) ipiano_state_destroy(model->run_state);
+    if (model->io_buf) cudaFree(model->io_buf);
     if (model->tc_bimg) cudaFree(model->tc_bimg);
     if (model->tc_sumk) cudaFree(model->tc_sumk);
     if (model->tc_thl) cudaFree(model->tc_thl);
@@ -493,6 +506,7 @@ foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int 
     a.nchunks = div_up(md->nf, Tr<7>::NC);
     a.v = v;
     a.gw = gw;
+    a.udom = md->term == FOE_DATA_IDIV;
     if (!hvp) {
         if (kind == FOE_STENCIL_TENSOR) {
             a.tiles_x = tiles_x_tc;
@@ -550,12 +564,13 @@ foe_status foe_energy_grad(const foe_model* md, const double* w, const float* f,
         std::vector<double> lam(2 * (size_t)B);
         for (int b = 0; b < B; ++b) {
             lam[2 * b] = lambda_per_image ? lambda_per_image[2 * b] : md->lam[0];
-            lam[2 * b + 1] = md->term == FOE_DATA_NAKAGAMI ? 0.0 : (lambda_per_image ? lambda_per_image[2 * b + 1] : md->lam[1]);
+            lam[2 * b + 1] = md->term != FOE_DATA_COMBINED ? 0.0 : (lambda_per_image ? lambda_per_image[2 * b + 1] : md->lam[1]);
         }
         CK(cudaMallocAsync((void**)&dlam, sizeof(double) * 2 * B, s));
         CK(cudaMallocAsync((void**)&dpart, sizeof(double) * B * nblk, s));
         CK(cudaMemcpyAsync(dlam, lam.data(), sizeof(double) * 2 * B, cudaMemcpyHostToDevice, s));
-        foe::k_data_energy<<<dim3(nblk, B), kThreads, 0, s>>>(w, f, dlam, dpart, nblk, HW, kPxt2);
+        foe::k_data_energy<<<dim3(nblk, B), kThreads, 0, s>>>(w, f, dlam, dpart, nblk, HW, kPxt2,
+                                                               md->term == FOE_DATA_IDIV);
         count_launch(1);
         CKL("k_data_energy");
         foe::k_reduce_rows<<<B, kThreads, 0, s>>>(dpart, nblk, 1, 1, dred + B);
@@ -622,7 +637,7 @@ foe_status foe_estimate_lipschitz(const foe_model* md, const float* f, int B, in
     CK(cudaMallocAsync((void**)&part, sizeof(double) * B * nblk * 3, s));
     CK(cudaMallocAsync((void**)&sums, sizeof(double) * B * 3, s));
     const int eb = div_up((long long)n, 256);
-    foe::k_log_ftilde<<<eb, 256, 0, s>>>(f, w0, n);
+    foe::k_log_ftilde<<<eb, 256, 0, s>>>(f, w0, n, md->term == FOE_DATA_IDIV);
     count_launch(1);
     CKL("k_log_ftilde");
     // v <- v0 / ||v0||
@@ -710,6 +725,7 @@ K1Args state_k1_args(const ipiano_state* st, int which_cur) {
     a.groups = st->groups;
     a.nf = st->model->nf;
     a.nchunks = st->nchunks;
+    a.udom = st->model->term == FOE_DATA_IDIV;
     return a;
 }
 
@@ -739,6 +755,7 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
     a2.groups = st->groups;
     a2.nblk = st->nblk2;
     a2.HW = st->HW;
+    a2.idiv = st->model->term == FOE_DATA_IDIV;
     foe::k_inertial_prox<kPxt2><<<dim3(st->nblk2, st->B), kThreads, 0, s>>>(a2);
     count_launch(1);
     CKL("k_inertial_prox");
@@ -862,7 +879,8 @@ foe_status state_init(ipiano_state* st, const float* f, const double* lipschitz_
     if (st->cfg.record_trace)
         CK(cudaMemsetAsync(st->trace, 0, sizeof(double) * B * (st->cfg.max_iters + 1) * 8, st->s));
     foe::k_init<<<dim3(st->nblk2, B), kThreads, 0, st->s>>>(f, st->ft, st->w, n, st->ppart, st->nblk2, st->ctl,
-                                                             st->HW, kPxt2, nullptr, 0);
+                                                             st->HW, kPxt2, nullptr, 0,
+                                                             st->model->term == FOE_DATA_IDIV);
     count_launch(1);
     CKL("k_init");
     const K1Args a1 = state_k1_args(st, 1);
@@ -982,12 +1000,26 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     st->lam.resize(2 * (size_t)B);
     for (int b = 0; b < B; ++b) {
         st->lam[2 * b] = lambda_per_image ? lambda_per_image[2 * b] : md->lam[0];
-        st->lam[2 * b + 1] = md->term == FOE_DATA_NAKAGAMI ? 0.0 : (lambda_per_image ? lambda_per_image[2 * b + 1] : md->lam[1]);
+        st->lam[2 * b + 1] = md->term != FOE_DATA_COMBINED ? 0.0 : (lambda_per_image ? lambda_per_image[2 * b + 1] : md->lam[1]);
     }
     rs = state_init(st, f, lipschitz_init, (cudaStream_t)stream);
     if (rs != FOE_OK) return cleanup(rs);
 #undef CKS
     *out = st;
+    return FOE_OK;
+}
+
+// replace the per-image lambdas of an existing state (validated like ipiano_state_create)
+static foe_status set_state_lambdas(ipiano_state* st, const double* lambda_per_image) {
+    const foe_model* md = st->model;
+    for (int b = 0; b < st->B; ++b) {
+        const double l1 = lambda_per_image ? lambda_per_image[2 * b] : md->lam[0];
+        const double l2 = md->term != FOE_DATA_COMBINED ? 0.0 : (lambda_per_image ? lambda_per_image[2 * b + 1] : md->lam[1]);
+        if (!(l1 >= 0) || !(l2 >= 0) || !std::isfinite(l1) || !std::isfinite(l2) || (l1 == 0 && l2 == 0))
+            return fail(FOE_ERR_INVALID_ARGUMENT, "lambda of image %d = (%g,%g) invalid", b, l1, l2);
+        st->lam[2 * b] = l1;
+        st->lam[2 * b + 1] = l2;
+    }
     return FOE_OK;
 }
 
@@ -1074,7 +1106,7 @@ foe_status ipiano_get_iterate(const ipiano_state* st, double* w_out, float* u_ou
     if (w_out || u_out) {
         const int gx = std::max(1, std::min(div_up((long long)st->HW, 256), 4 * st->model->nsm));
         foe::k_iterate_out<<<dim3(gx, st->B), 256, 0, s->s>>>(st->ctl, st->w, (size_t)st->B * st->HW, w_out,
-                                                              u_out, st->HW);
+                                                              u_out, st->HW, st->model->term == FOE_DATA_IDIV);
         CKL("k_iterate_out");
         count_launch(1);
     }
@@ -1132,31 +1164,65 @@ foe_status ipiano_run(const foe_model* md, const float* f, int B, int H, int W, 
     foe_status r = check_dims(md, B, H, W);
     if (r != FOE_OK) return r;
     if (!f || !u_out) return fail(FOE_ERR_INVALID_ARGUMENT, "f and u_out must be non-NULL");
+    if (!lipschitz_init) return fail(FOE_ERR_INVALID_ARGUMENT, "lipschitz_init is NULL");
     CK(cudaSetDevice(md->dev));
     cudaStream_t s = (cudaStream_t)stream;
     const size_t n = (size_t)B * H * W;
     const bool f_dev = is_device_ptr(f), u_dev = is_device_ptr(u_out);
+    ipiano_config c;
+    if (cfg) c = *cfg; else ipiano_config_default(&c);
+    std::unique_lock<std::mutex> lk(md->run_mu, std::try_to_lock);
+    const bool cached = lk.owns_lock();
+    // staging buffers for host I/O
     float* df = nullptr;
     float* du = nullptr;
-    if (!f_dev) {
-        CK(cudaMallocAsync((void**)&df, sizeof(float) * n, s));
-        CK(cudaMemcpyAsync(df, f, sizeof(float) * n, cudaMemcpyHostToDevice, s));
+    if (!f_dev || !u_dev) {
+        if (cached) {
+            if (md->io_n < n) {
+                if (md->io_buf) cudaFree(md->io_buf);
+                md->io_buf = nullptr;
+                md->io_n = 0;
+                CK(cudaMalloc((void**)&md->io_buf, sizeof(float) * 2 * n));
+                md->io_n = n;
+            }
+            df = md->io_buf;
+            du = md->io_buf + md->io_n;
+        } else {
+            CK(cudaMallocAsync((void**)&df, sizeof(float) * 2 * n, s));
+            du = df + n;
+        }
     }
-    if (!u_dev) CK(cudaMallocAsync((void**)&du, sizeof(float) * n, s));
+    if (!f_dev) CK(cudaMemcpyAsync(df, f, sizeof(float) * n, cudaMemcpyHostToDevice, s));
+    const float* fd = f_dev ? f : df;
+    // the solver state: reuse the cached one when shape and configuration match
     ipiano_state* st = nullptr;
-    r = ipiano_state_create(md, f_dev ? f : df, B, H, W, lambda_per_image, lipschitz_init, cfg, stream, &st);
+    bool own = true;
+    if (cached && md->run_state && md->run_state->B == B && md->run_state->H == H && md->run_state->W == W &&
+        std::memcmp(&md->run_state->cfg_in, &c, sizeof(c)) == 0) {
+        st = md->run_state;
+        own = false;
+        r = set_state_lambdas(st, lambda_per_image);
+        if (r == FOE_OK) r = ipiano_state_reset(st, fd, lipschitz_init, stream);
+    } else {
+        r = ipiano_state_create(md, fd, B, H, W, lambda_per_image, lipschitz_init, &c, stream, &st);
+        if (r == FOE_OK) st->cfg_in = c;
+        if (r == FOE_OK && cached) {
+            if (md->run_state) ipiano_state_destroy(md->run_state);
+            md->run_state = st;
+            own = false;
+        }
+    }
     if (r == FOE_OK) r = ipiano_solve(st, stream);
     foe_status r2 = FOE_OK;
     if (st) {
         const std::string keep = g_err;
         r2 = ipiano_get_iterate(st, nullptr, u_dev ? u_out : du, stream);
         if (r2 == FOE_OK && trace) r2 = ipiano_get_trace(st, trace, trace_bytes);
-        ipiano_state_destroy(st);
+        if (own) ipiano_state_destroy(st);
         if (r != FOE_OK) g_err = keep;
     }
     if (!u_dev && r2 == FOE_OK) CK(cudaMemcpyAsync(u_out, du, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
-    if (df) CK(cudaFreeAsync(df, s));
-    if (du) CK(cudaFreeAsync(du, s));
+    if (df && !cached) CK(cudaFreeAsync(df, s));
     CK(cudaStreamSynchronize(s));
     return r != FOE_OK ? r : r2;
 }
@@ -1280,6 +1346,7 @@ foe_status slab_k2(ipiano_slabs* g, int j) {
     a2.HW = st->HW;
     a2.halo_send = g->halo_send + j * halo_elems(g);
     a2.halo_px = (size_t)foe::kHalo * g->W;
+    a2.idiv = st->model->term == FOE_DATA_IDIV;
     foe::k_inertial_prox<kPxt2><<<dim3(st->nblk2, 1), kThreads, 0, g->s>>>(a2);
     count_launch(1);
     CKL("k_inertial_prox (slab)");
@@ -1404,7 +1471,7 @@ foe_status slab_init(ipiano_slabs* g, const float* f, double L_init, cudaStream_
             CK(cudaMemsetAsync(st->trace, 0, sizeof(double) * (st->cfg.max_iters + 1) * 8, g->s));
         foe::k_init<<<dim3(st->nblk2, 1), kThreads, 0, g->s>>>(f + j * HWs, st->ft, st->w, HWs, st->ppart, st->nblk2,
                                                                 st->ctl, HWs, kPxt2, g->halo_send + j * halo_elems(g),
-                                                                (size_t)foe::kHalo * g->W);
+                                                                (size_t)foe::kHalo * g->W, st->model->term == FOE_DATA_IDIV);
         count_launch(1);
         CKL("k_init (slab)");
     }
@@ -1666,7 +1733,8 @@ foe_status ipiano_slabs_get_iterate(const ipiano_slabs* g, double* w_out, float*
         const ipiano_state* st = g->members[j];
         const int gx = std::max(1, std::min(div_up((long long)HWs, 256), 4 * g->model->nsm));
         foe::k_iterate_out<<<dim3(gx, 1), 256, 0, gg->s>>>(st->ctl, st->w, HWs, w_out ? w_out + j * HWs : nullptr,
-                                                            u_out ? u_out + j * HWs : nullptr, HWs);
+                                                            u_out ? u_out + j * HWs : nullptr, HWs,
+                                                            st->model->term == FOE_DATA_IDIV);
         count_launch(1);
         CKL("k_iterate_out (slabs)");
     }

@@ -75,6 +75,9 @@ struct K1Args {
     // halo row kHalo + (y - H) ([2][kHalo][W] fp64, filled by the halo exchange); nullptr =
     // periodic wrap inside the image (single-GPU scene).
     const double* halo;
+    // Data model of the iterate: 0 = w-domain (models (8)/(10): u = e^w, grad_w F = u (.) s),
+    // 1 = u-domain (model (6): the iterate is u, grad_u F = s)
+    int udom;
     // HVP only
     const double* v;        // [B][H][W]
     const float* gw;        // [B][H][W] gradient at w
@@ -220,15 +223,17 @@ k_prior_grad(const K1Args args, const __grid_constant__ TapParams tp) {
 
     // (a2) stage u - c on the tile + 2C halo, with c = e^w at the tile centre (fp64 exp).
     const int yc = wrap_idx(y0 + kTile / 2, H), xc = wrap_idx(x0 + kTile / 2, W);
-    const float cst = (float)exp(w[(size_t)yc * W + xc]);
+    const bool udom = args.udom != 0;
+    const float cst = (float)(udom ? w[(size_t)yc * W + xc] : exp(w[(size_t)yc * W + xc]));
     const double cstd = (double)cst;
     for (int idx = threadIdx.x; idx < G::UY * G::UX; idx += kThreads) {
         const int uy = idx / G::UX, ux = idx - uy * G::UX;
         const int gy = wrap_idx(y0 - 2 * C + uy, H), gx = wrap_idx(x0 - 2 * C + ux, W);
         const size_t gi = (size_t)gy * W + gx;
-        const double u = exp(w[gi]);
+        const double u = udom ? w[gi] : exp(w[gi]);
         us[uy * G::UP + ux] = (float)(u - cstd);
-        if (HVP) uvs[uy * G::UP + ux] = (float)(u * vv[gi]);
+        // HVP in w: u (.) v is the direction of u; in u the direction is v itself
+        if (HVP) uvs[uy * G::UP + ux] = (float)(udom ? vv[gi] : u * vv[gi]);
     }
     __syncthreads();
 
@@ -335,7 +340,9 @@ k_prior_grad(const K1Args args, const __grid_constant__ TapParams tp) {
             const float u = us[(oy + 2 * C) * G::UP + ox + 2 * C] + cst;
             float val;
             if (!HVP) {
-                val = u * acc[o][x];
+                val = udom ? acc[o][x] : u * acc[o][x];
+            } else if (udom) {
+                val = acc[o][x];                  // Hess F(u) v = sum theta K^T [rho'' (.) K v]
             } else {
                 const size_t gi = (size_t)gy * W + gx;
                 val = (float)(vv[gi] * (double)args.gw[(size_t)b * HW + gi] + (double)(u * acc[o][x]));
@@ -398,9 +405,10 @@ struct G2 {
     static constexpr int SMEM_BYTES = UY * UP * 4 + NCP * RY * PP * 8;
 };
 
-// acc[o][x] += u[(o+a)][x+b] * (kA, kB)[a][b]   (FFMA2 with a broadcast scalar)
+// acc[o][x] += (u[(o+a)][x+b] - sub) * (kA, kB)[a][b]   (FFMA2 with a broadcast scalar; `sub`
+// is the item's own DC shift, restored by the caller as sub * sum k)
 template <int M, int S, int NV>
-__device__ __forceinline__ void corr_fwd2(const float* __restrict__ in, int pitch,
+__device__ __forceinline__ void corr_fwd2(const float* __restrict__ in, int pitch, float sub,
                                           const float2* __restrict__ taps, float2 (&acc)[S][4]) {
 #pragma unroll
     for (int i = 0; i < S + M - 1; ++i) {
@@ -409,7 +417,9 @@ __device__ __forceinline__ void corr_fwd2(const float* __restrict__ in, int pitc
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
             const float4 t = rp[v];
-            row[4 * v + 0] = t.x; row[4 * v + 1] = t.y; row[4 * v + 2] = t.z; row[4 * v + 3] = t.w;
+            const float2 lo = __fadd2_rn(make_float2(t.x, t.y), make_float2(-sub, -sub));
+            const float2 hi = __fadd2_rn(make_float2(t.z, t.w), make_float2(-sub, -sub));
+            row[4 * v + 0] = lo.x; row[4 * v + 1] = lo.y; row[4 * v + 2] = hi.x; row[4 * v + 3] = hi.y;
         }
 #pragma unroll
         for (int a = 0; a < M; ++a) {
@@ -487,7 +497,8 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
     // (a2) stage u - c on the tile + 2C halo (fp64 exp, one rounding to fp32); c = e^w at a
     // pixel inside the tile (so a row slab and the whole scene use the same c)
     const int yc = min(y0 + kTile / 2, H - 1), xc = min(x0 + kTile / 2, W - 1);
-    const float cst = (float)exp(w[(size_t)yc * W + xc]);
+    const bool udom = args.udom != 0;
+    const float cst = (float)(udom ? w[(size_t)yc * W + xc] : exp(w[(size_t)yc * W + xc]));
     const double cstd = (double)cst;
     const double* halo = args.halo;
     for (int idx = threadIdx.x; idx < G::UY * G::UX; idx += kThreads) {
@@ -498,7 +509,7 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
         else if (y < 0) src = halo + (size_t)(kHalo + y) * W;
         else if (y >= H) src = halo + (size_t)(kHalo + y - H) * W;
         else src = w + (size_t)y * W;
-        us[uy * G::UP + ux] = (float)(exp(src[gx]) - cstd);
+        us[uy * G::UP + ux] = (float)((udom ? src[gx] : exp(src[gx])) - cstd);
     }
     __syncthreads();
 
@@ -518,6 +529,10 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
             if (rok && tcx >= 0 && tcx < kTile && x0 + tcx < W) own |= 1u << (o * 4 + x);
         }
     }
+    // the item's own DC shift: u at the centre of its response block (second-level shift on
+    // top of the tile's c; local differences keep the FFMA accumulation accurate on rough images)
+    const float isub = fwd_on ? us[(fseg * SF + SF / 2 + C) * G::UP + fstrip * 4 + 2 + C] : 0.f;
+    const float icst = cst + isub;
     const int bstrip = tid % G::NBSTRIP, bseg = tid / G::NBSTRIP;
     float2 bacc[G::SB][G::CWB];
 #pragma unroll
@@ -533,14 +548,15 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
         for (int p = 0; p < ncp; ++p) {
             const int pi = pbase + p;
             if (fwd_on) {
-                // r = c sum(k) + K(u - c): the DC restore is the accumulator's initial value
-                const float2 cs = make_float2(cst * tp.sumk[2 * pi], cst * tp.sumk[2 * pi + 1]);
+                // r = (c + isub) sum(k) + K(u - c - isub): the DC restore is the accumulator's
+                // initial value
+                const float2 cs = make_float2(icst * tp.sumk[2 * pi], icst * tp.sumk[2 * pi + 1]);
                 float2 r[SF][4];
 #pragma unroll
                 for (int o = 0; o < SF; ++o)
 #pragma unroll
                     for (int x = 0; x < 4; ++x) r[o][x] = cs;
-                corr_fwd2<M, SF, G::NVF>(us + fseg * SF * G::UP + fstrip * 4, G::UP, &tp.fwd[pi * M * M], r);
+                corr_fwd2<M, SF, G::NVF>(us + fseg * SF * G::UP + fstrip * 4, G::UP, isub, &tp.fwd[pi * M * M], r);
                 float2 el = make_float2(0.f, 0.f);
                 float2* pdst = ps + (size_t)p * G::RY * G::PP + (size_t)(fseg * SF) * G::PP + fstrip * 4;
 #pragma unroll
@@ -583,7 +599,7 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
             const int ox = bstrip * G::CWB + x;
             const int gx = x0 + ox;
             if (gx >= W) continue;
-            const float u = us[(oy + 2 * C) * G::UP + ox + 2 * C] + cst;
+            const float u = udom ? 1.0f : us[(oy + 2 * C) * G::UP + ox + 2 * C] + cst;   // W = diag(e^w)
             gout[(size_t)gy * W + gx] = u * (bacc[o][x].x + bacc[o][x].y);
         }
     }
@@ -611,6 +627,65 @@ __device__ __forceinline__ double exp_small(double x) {
 }
 __device__ __forceinline__ double exp_near0(double x) { return fabs(x) <= 0.0625 ? exp_small(x) : exp(x); }
 
+// e^{x} and e^{-x} together for |x| <= 1/16: even and odd Taylor parts C = cosh x, S = sinh x
+// (terms to x^10, remainder < 1e-20 relative), e^{+-x} = C +- S -- half the work of two exp_small
+__device__ __forceinline__ void exp_pm_small(double x, double& ep, double& em) {
+    const double x2 = x * x;
+    double c = 2.7557319223985891e-07;             // 1/10!
+    c = fma(c, x2, 2.4801587301587302e-05);        // 1/8!
+    c = fma(c, x2, 1.3888888888888889e-03);        // 1/6!
+    c = fma(c, x2, 4.1666666666666664e-02);        // 1/4!
+    c = fma(c, x2, 0.5);
+    c = fma(c, x2, 1.0);
+    double sh = 2.7557319223985893e-06;            // 1/9!
+    sh = fma(sh, x2, 1.9841269841269841e-04);      // 1/7!
+    sh = fma(sh, x2, 8.3333333333333332e-03);      // 1/5!
+    sh = fma(sh, x2, 1.6666666666666666e-01);      // 1/3!
+    sh = fma(sh, x2, 1.0);
+    sh *= x;
+    ep = c + sh;
+    em = c - sh;
+}
+
+// e^{2a} and e^{-2a} from one range reduction (|2a| <= 700): 2a = n ln2 + r, |r| <= ln2/2;
+// cosh/sinh Taylor parts of r to r^16 (remainder < 1e-19 relative), scaled by 2^{+-n}
+__device__ __forceinline__ void exp2a_pm(double a, double& ep, double& em) {
+    const double x = 2.0 * a;
+    const double n = rint(x * 1.4426950408889634);                   // x / ln 2
+    const double r = fma(-n, 2.3190468138462996e-17, fma(-n, 6.9314718055994529e-01, x));   // x - n ln2
+    const double r2 = r * r;
+    double c = 4.7794773323873853e-14;             // 1/16!
+    c = fma(c, r2, 1.1470745597729725e-11);        // 1/14!
+    c = fma(c, r2, 2.0876756987868100e-09);        // 1/12!
+    c = fma(c, r2, 2.7557319223985891e-07);        // 1/10!
+    c = fma(c, r2, 2.4801587301587302e-05);        // 1/8!
+    c = fma(c, r2, 1.3888888888888889e-03);        // 1/6!
+    c = fma(c, r2, 4.1666666666666664e-02);        // 1/4!
+    c = fma(c, r2, 0.5);
+    c = fma(c, r2, 1.0);
+    double sh = 7.6471637318198164e-13;            // 1/15!
+    sh = fma(sh, r2, 1.6059043836821613e-10);      // 1/13!
+    sh = fma(sh, r2, 2.5052108385441720e-08);      // 1/11!
+    sh = fma(sh, r2, 2.7557319223985893e-06);      // 1/9!
+    sh = fma(sh, r2, 1.9841269841269841e-04);      // 1/7!
+    sh = fma(sh, r2, 8.3333333333333332e-03);      // 1/5!
+    sh = fma(sh, r2, 1.6666666666666666e-01);      // 1/3!
+    sh = fma(sh, r2, 1.0);
+    sh *= r;
+    const int ni = (int)n;
+    ep = (c + sh) * __hiloint2double((ni + 1023) << 20, 0);
+    em = (c - sh) * __hiloint2double((1023 - ni) << 20, 0);
+}
+
+// 1/b to full fp64 precision: MUFU reciprocal seed + two Newton steps (b finite, nonzero)
+__device__ __forceinline__ double rcp_f64(double b) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
+    y = fma(y, fma(-b, y, 1.0), y);
+    y = fma(y, fma(-b, y, 1.0), y);
+    return y;
+}
+
 // Root of phi(z) = z - what + tau [l1 (1 - f^2 e^{-2z}) + l2 (e^{2z} - f^2)],
 // solved for the increment d = z - what:
 //   phi(d) = d + tau(l1 - l2 f^2) - A e^{-2d} + Bc e^{2d},  A = tau l1 f^2 e^{-2 what},
@@ -626,19 +701,25 @@ __device__ __forceinline__ int prox_newton(double what, double ft, double tau, d
                                            double l2, double tol, int cap, double& z_out,
                                            double& em_out, double& ep_out) {
     const double f2 = ft * ft;
-    const double Em = exp(-2.0 * what);
-    const double Ep = 1.0 / Em;
+    double Em, Ep;
+    if (fabs(what) <= 340.0) {
+        exp2a_pm(what, Ep, Em);                    // e^{2 what}, e^{-2 what}
+    } else {
+        Em = exp(-2.0 * what);
+        Ep = 1.0 / Em;
+    }
     const double A = tau * l1 * f2 * Em, Bc = tau * l2 * Ep, c0 = tau * (l1 - l2 * f2);
-    {
+    if (isfinite(A) && isfinite(Bc)) {
         const double phi0 = c0 - A + Bc;
         if (fabs(phi0) <= tol) { z_out = what; em_out = Em; ep_out = Ep; return 0; }
-        const double d1 = -phi0 / (1.0 + 2.0 * (A + Bc));
+        const double d1 = -phi0 * rcp_f64(1.0 + 2.0 * (A + Bc));
         if (fabs(d1) <= 0.03125) {
-            const double ep2 = exp_small(2.0 * d1), em2 = exp_small(-2.0 * d1);
+            double ep2, em2;
+            exp_pm_small(2.0 * d1, ep2, em2);
             const double phi = d1 + c0 - A * em2 + Bc * ep2;
             if (fabs(phi) <= tol) { z_out = what + d1; em_out = Em * em2; ep_out = Ep * ep2; return 1; }
             const double dphi = 1.0 + 2.0 * (A * em2 + Bc * ep2);
-            const double st = phi / dphi;
+            const double st = phi * rcp_f64(dphi);
             if ((dphi - 1.0) * st * st <= 0.25 * tol && fabs(st) <= 1e-6) {
                 const double e = -2.0 * st;                              // e^{+-e}, |e| <= 2e-6
                 z_out = what + (d1 - st);
@@ -682,6 +763,7 @@ struct K2Args {
     // ([2][kHalo][W], the rows the ring neighbours need); nullptr = no slab.
     double* halo_send;
     size_t halo_px;        // kHalo * W
+    int idiv;              // model (6) in u: closed-form prox of (lam/2)(u^2 - 2 f^2 log u), lam = lam1
 };
 
 template <int PXT>
@@ -710,7 +792,15 @@ k_inertial_prox(const K2Args a) {  // (3 CTAs/SM: <= 80 registers)
         const double what = wv - alpha * gv + beta * (wv - wp[p]);
         const double f = (double)ft[p];
         double z, em, ep;
-        const int it = prox_newton(what, f, alpha, l1, l2, a.sp.newton_tol, a.sp.newton_cap, z, em, ep);
+        int it;
+        if (a.idiv) {
+            // u = (u^ + sqrt(u^2 + 4 (1 + tau lam) tau lam f^2)) / (2 (1 + tau lam))
+            const double tl = alpha * l1;
+            z = (what + sqrt(fma(what, what, 4.0 * (1.0 + tl) * tl * f * f))) / (2.0 * (1.0 + tl));
+            em = 0.0; ep = 0.0; it = 0;
+        } else {
+            it = prox_newton(what, f, alpha, l1, l2, a.sp.newton_tol, a.sp.newton_cap, z, em, ep);
+        }
         wn[p] = z;
         if (a.halo_send != nullptr) {
             if (p < a.halo_px) a.halo_send[p] = z;
@@ -720,9 +810,14 @@ k_inertial_prox(const K2Args a) {  // (3 CTAs/SM: <= 80 registers)
         gd += gv * d;
         dd += d * d;
         const double f2 = f * f;
-        Gp += 0.5 * l1 * (2.0 * z + f2 * em) + 0.5 * l2 * (ep - 2.0 * f2 * z);
+        if (a.idiv) {
+            Gp += 0.5 * l1 * (z * z - 2.0 * f2 * log(z));                 // Eq.(5)
+            wmax = fmax(wmax, z > 0.0 ? 0.0 : INFINITY);                  // the iterate must stay > 0
+        } else {
+            Gp += 0.5 * l1 * (2.0 * z + f2 * em) + 0.5 * l2 * (ep - 2.0 * f2 * z);
+            wmax = fmax(wmax, fabs(z));
+        }
         ww += wv * wv;
-        wmax = fmax(wmax, fabs(z));
         if (it < 0) fail += 1.0; else nit = fmax(nit, (double)it);
         if (!(z == z)) wmax = INFINITY;
     }
@@ -827,7 +922,7 @@ __global__ void __launch_bounds__(kThreads) k_decide(const K3Args a) {
 // partials of G(w^0) (slot 2 of ppart).
 __global__ void __launch_bounds__(kThreads)
 k_init(const float* f, float* ft, double* w, size_t w_slot_stride, double* ppart, int nblk,
-       const ImgCtl* ctl, size_t HW, int pxt, double* halo_send, size_t halo_px) {
+       const ImgCtl* ctl, size_t HW, int pxt, double* halo_send, size_t halo_px, int idiv) {
     __shared__ double red[32];
     const int b = blockIdx.y;
     const double l1 = ctl[b].lam1, l2 = ctl[b].lam2;
@@ -840,7 +935,7 @@ k_init(const float* f, float* ft, double* w, size_t w_slot_stride, double* ppart
         const float fv = fmaxf(f[gi], 1.0f);
         ft[gi] = fv;
         const double fd = (double)fv;
-        const double z = log(fd);
+        const double z = idiv ? fd : log(fd);          // u^0 = f~ (model (6)) or w^0 = log f~
         w[gi] = z;
         w[w_slot_stride + gi] = z;
         if (halo_send != nullptr) {   // row slab (B = 1): rows the ring neighbours need
@@ -848,7 +943,8 @@ k_init(const float* f, float* ft, double* w, size_t w_slot_stride, double* ppart
             else if (p >= HW - halo_px) halo_send[p - (HW - 2 * halo_px)] = z;
         }
         const double f2 = fd * fd;
-        G += 0.5 * l1 * (2.0 * z + f2 * exp(-2.0 * z)) + 0.5 * l2 * (exp(2.0 * z) - 2.0 * f2 * z);
+        G += idiv ? 0.5 * l1 * (z * z - 2.0 * f2 * log(z))
+                  : 0.5 * l1 * (2.0 * z + f2 * exp(-2.0 * z)) + 0.5 * l2 * (exp(2.0 * z) - 2.0 * f2 * z);
     }
     const double s = block_sum_d(G, red);
     if (threadIdx.x == 0) {
@@ -931,7 +1027,8 @@ k_band_reduce(const double* epart, int e_per_band, const double* ppart, int bpb,
 
 // data energy partials of a given w (foe_energy_grad): part[b][blk][0]
 __global__ void __launch_bounds__(kThreads)
-k_data_energy(const double* w, const float* f, const double* lam, double* part, int nblk, size_t HW, int pxt) {
+k_data_energy(const double* w, const float* f, const double* lam, double* part, int nblk, size_t HW, int pxt,
+              int idiv) {
     __shared__ double red[32];
     const int b = blockIdx.y;
     const double l1 = lam[2 * b], l2 = lam[2 * b + 1];
@@ -944,7 +1041,8 @@ k_data_energy(const double* w, const float* f, const double* lam, double* part, 
         const double fd = (double)fmaxf(f[gi], 1.0f);
         const double z = w[gi];
         const double f2 = fd * fd;
-        G += 0.5 * l1 * (2.0 * z + f2 * exp(-2.0 * z)) + 0.5 * l2 * (exp(2.0 * z) - 2.0 * f2 * z);
+        G += idiv ? 0.5 * l1 * (z * z - 2.0 * f2 * log(z))
+                  : 0.5 * l1 * (2.0 * z + f2 * exp(-2.0 * z)) + 0.5 * l2 * (exp(2.0 * z) - 2.0 * f2 * z);
     }
     const double s = block_sum_d(G, red);
     if (threadIdx.x == 0) part[(size_t)b * nblk + blockIdx.x] = s;
@@ -990,20 +1088,20 @@ __global__ void k_normalize(const T* src, double* v, const double* sums, int K, 
     v[i] = (double)src[i] / sqrt(sums[(size_t)b * K + k]);
 }
 
-__global__ void k_log_ftilde(const float* f, double* w, size_t n) {
+__global__ void k_log_ftilde(const float* f, double* w, size_t n, int idiv) {
     const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) w[i] = log((double)fmaxf(f[i], 1.0f));
+    if (i < n) w[i] = idiv ? (double)fmaxf(f[i], 1.0f) : log((double)fmaxf(f[i], 1.0f));
 }
 
 // a13: u = e^w of each image's current slot (and/or a copy of w)
 __global__ void k_iterate_out(const ImgCtl* ctl, const double* w, size_t slot_stride, double* w_out,
-                              float* u_out, size_t HW) {
+                              float* u_out, size_t HW, int udom) {
     const int b = blockIdx.y;
     const double* src = w + (size_t)ctl[b].cur * slot_stride + (size_t)b * HW;
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += (size_t)gridDim.x * blockDim.x) {
         const double v = src[i];
         if (w_out) w_out[(size_t)b * HW + i] = v;
-        if (u_out) u_out[(size_t)b * HW + i] = (float)exp(v);
+        if (u_out) u_out[(size_t)b * HW + i] = (float)(udom ? v : exp(v));
     }
 }
 

@@ -194,8 +194,9 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta) {
     // u - c = c (e^{w - w_c} - 1) with c = e^{w_c} at a pixel of the tile: one fp64 exp per CTA,
     // then fp32 expm1 of the small fp64 difference -- accurate relative to u - c (what the
     // stencil needs), and far cheaper than K1's fp64 exp per staged pixel
+    const bool udom = args.udom != 0;
     const double wc = w[(size_t)yc * W + xc];
-    const float cst = (float)exp(wc);
+    const float cst = (float)(udom ? wc : exp(wc));
     if (t < NP) {
         css[t] = __ldg(ta.sumk + t);
         ths[t] = __ldg(ta.theta_ln2 + t);
@@ -209,7 +210,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta) {
         else if (y < 0) src = halo + (size_t)(kHalo + y) * W;
         else if (y >= H) src = halo + (size_t)(kHalo + y - H) * W;
         else src = w + (size_t)y * W;
-        us[uy * G::UP + ux] = cst * expm1f((float)(src[gx] - wc));
+        us[uy * G::UP + ux] = udom ? (float)(src[gx] - (double)cst) : cst * expm1f((float)(src[gx] - wc));
     }
     tc::fence_proxy_async_smem();
     tc::fence_before_sync();
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta) {
                 const int o = jz - 2 * C;
                 if (o >= 0 && o < R && out_col && y0 + o < H) {
                     const float s_tot = acc[A1 - 1] + hand[(o & 7) * L + l];
-                    const float u = us[(o + 2 * C) * G::UP + l + 2 * C] + cst;
+                    const float u = udom ? 1.0f : us[(o + 2 * C) * G::UP + l + 2 * C] + cst;   // W = diag(e^w)
                     gout[(size_t)(y0 + o) * W + x0 + l] = u * s_tot;
                 }
 #pragma unroll

@@ -20,7 +20,7 @@ STATUS_NAMES = {
     4: "FOE_ERR_NONFINITE", 5: "FOE_ERR_BACKTRACK_LIMIT", 6: "FOE_ERR_PROX_NO_CONVERGENCE",
     7: "FOE_ERR_DOMAIN", 8: "FOE_ERR_COMM", 9: "FOE_ERR_UNSUPPORTED",
 }
-FOE_DATA_COMBINED, FOE_DATA_NAKAGAMI = 0, 1
+FOE_DATA_COMBINED, FOE_DATA_NAKAGAMI, FOE_DATA_IDIV = 0, 1, 2
 FOE_STENCIL_AUTO, FOE_STENCIL_FFMA, FOE_STENCIL_TENSOR = 0, 1, 2
 TRACE_FIELDS = ("F", "G", "H", "L", "trials", "margin", "newton", "relchg")
 

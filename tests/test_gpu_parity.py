@@ -316,3 +316,27 @@ def test_c4_bench_launch_configuration_two_iterations():
         l1, l2 = d["lambdas"][b]
         ref = oracle.ipiano_run(d["f"][b], d["filters"], d["theta"], l1, l2, oracle.make_cfg(L0[b], 2))
         assert rel_l2(u[b], ref["u"]) <= 1e-5
+
+
+def test_ipiano_run_workspace_reuse_is_exact():
+    """ipiano_run keeps one workspace per model: a repeated call with new inputs and lambdas
+    (host buffers, then device buffers) gives bit-identical results to a fresh state."""
+    cfg = S.config("c2", H=96, W=80, iters=8, B=2)
+    d = S.make_inputs(cfg, images=[0, 1])
+    md = _model(d["filters"], d["theta"], lam=tuple(d["lambdas"][0]))
+    L0 = np.array([2.0 ** 18, 2.0 ** 17])
+    c = P.ipiano_config_default(max_iters=cfg.iters)
+    outs = []
+    for scale, lam in ((1.0, d["lambdas"]), (1.3, d["lambdas"][::-1].copy())):
+        f = (d["f"] * scale).astype(np.float32)
+        u_h, tr_h = P.ipiano_run(md, f, lam, L0, c)                       # host in/out (cached)
+        u_d, tr_d = P.ipiano_run(md, _cuda(f, torch.float32), lam, L0, c)  # device in/out (cached)
+        st = P.ipiano_state_create(md, _cuda(f, torch.float32), lam, L0, c)   # fresh state
+        P.ipiano_solve(st)
+        _, u_f = P.ipiano_get_iterate(st, want_w=False)
+        tr_f = P.ipiano_get_trace(st)
+        np.testing.assert_array_equal(u_h, u_f.cpu().numpy())
+        np.testing.assert_array_equal(u_d.cpu().numpy(), u_f.cpu().numpy())
+        np.testing.assert_array_equal(tr_h, tr_f)
+        outs.append(u_h)
+    assert not np.array_equal(outs[0], outs[1])
