@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -116,9 +117,22 @@ constexpr int kTcR = 64;
 template <int M, int NP>
 constexpr int tc_smem() { return foe::TcGeom<M, NP, kTcR>::SMEM_BYTES; }
 template <int M, int NP>
+constexpr int tc4_smem() { return foe::Tc4Geom<M, NP, kTcR>::SMEM_BYTES; }
+template <int M, int NP>
 cudaError_t tc_set_attr() {
-    return cudaFuncSetAttribute(foe::k_prior_grad_tc<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                tc_smem<M, NP>());
+    cudaError_t e = cudaFuncSetAttribute(foe::k_prior_grad_tc<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         tc_smem<M, NP>());
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(foe::k_prior_grad_tc4<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                tc4_smem<M, NP>());
+}
+// K8 variant: 3 = two lock-step CTAs per SM (default; 1.90 ms vs 1.96 ms per c4 launch under
+// ncu), 4 = warp-specialised single-CTA pipeline (FOE_K8_VARIANT=4, experimental)
+int tc_variant() {
+    const char* e = std::getenv("FOE_K8_VARIANT");   // read per launch (A/B in one process)
+    if (e && e[0] == '4') return 4;
+    if (e && e[0] == 'k' && e[1] >= '1' && e[1] <= '4') return 40 + (e[1] - '0');   // profiling knockouts
+    return 3;
 }
 // the banks K8 has an instantiation for: (m, padded N_f)
 int tc_np(int m, int nf) {
@@ -146,6 +160,7 @@ struct foe_model {
     float* tc_bimg = nullptr;
     float* tc_sumk = nullptr;
     float* tc_thl = nullptr;
+    foe::TcConst* tc_const = nullptr;  // per-filter epilogue constants, passed by value to K8
     int stencil = FOE_STENCIL_AUTO; // foe_energy_grad's choice
     // ipiano_run's reusable workspace (one solver state + host-I/O staging buffers), kept for
     // repeated calls of the same shape and configuration; guarded by run_mu (a concurrent call
@@ -222,6 +237,14 @@ foe_status build_tc_images(foe_model* md) {
         }
         sumk[i] = md->tp->sumk[i];
         thl[i] = (float)md->tp->theta_ln2[i];
+    }
+    md->tc_const = new (std::nothrow) foe::TcConst();
+    if (!md->tc_const) return fail(FOE_ERR_OUT_OF_MEMORY, "host allocation");
+    std::memset(md->tc_const, 0, sizeof(foe::TcConst));
+    for (int i = 0; i < nf; ++i) {
+        md->tc_const->sumk[i] = sumk[i];
+        md->tc_const->thl[i] = thl[i];
+        md->tc_const->kbl[i] = img[2 * BF + 2 * BB + i];
     }
     CK(cudaMalloc((void**)&md->tc_bimg, img.size() * sizeof(float)));
     CK(cudaMalloc((void**)&md->tc_sumk, NP * sizeof(float)));
@@ -382,6 +405,7 @@ void foe_model_destroy(foe_model* model) {
     if (model->tc_bimg) cudaFree(model->tc_bimg);
     if (model->tc_sumk) cudaFree(model->tc_sumk);
     if (model->tc_thl) cudaFree(model->tc_thl);
+    delete model->tc_const;
     delete model->tp;
     delete model->tp2;
     delete model;
@@ -451,10 +475,32 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
     ta.theta_ln2 = md->tc_thl;
     ta.tiles_x = a.tiles_x;
     count_launch(1);
-    if (md->tc_np == 48)
-        foe::k_prior_grad_tc<7, 48, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<7, 48>(), s>>>(ta);
-    else
-        foe::k_prior_grad_tc<5, 32, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<5, 32>(), s>>>(ta);
+    constexpr int T4 = foe::Tc4Geom<7, 48, kTcR>::THREADS;
+    const int var = tc_variant();
+    if (var >= 41 && md->tc_np == 48) {   // profiling knockouts (FOE_K8_VARIANT=k1..k4), results invalid
+        static bool attr = false;
+        if (!attr) {
+            attr = true;
+            cudaFuncSetAttribute(foe::k_prior_grad_tc4<7, 48, kTcR, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc4_smem<7, 48>());
+            cudaFuncSetAttribute(foe::k_prior_grad_tc4<7, 48, kTcR, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc4_smem<7, 48>());
+            cudaFuncSetAttribute(foe::k_prior_grad_tc4<7, 48, kTcR, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc4_smem<7, 48>());
+            cudaFuncSetAttribute(foe::k_prior_grad_tc4<7, 48, kTcR, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc4_smem<7, 48>());
+        }
+        const dim3 gr(a.ntiles, B);
+        if (var == 41) foe::k_prior_grad_tc4<7, 48, kTcR, 1><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
+        if (var == 42) foe::k_prior_grad_tc4<7, 48, kTcR, 2><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
+        if (var == 43) foe::k_prior_grad_tc4<7, 48, kTcR, 3><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
+        if (var == 44) foe::k_prior_grad_tc4<7, 48, kTcR, 4><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
+    } else if (var >= 4) {
+        if (md->tc_np == 48)
+            foe::k_prior_grad_tc4<7, 48, kTcR><<<dim3(a.ntiles, B), T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
+        else
+            foe::k_prior_grad_tc4<5, 32, kTcR><<<dim3(a.ntiles, B), T4, tc4_smem<5, 32>(), s>>>(ta, *md->tc_const);
+    } else if (md->tc_np == 48) {
+        foe::k_prior_grad_tc<7, 48, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<7, 48>(), s>>>(ta, *md->tc_const);
+    } else {
+        foe::k_prior_grad_tc<5, 32, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<5, 32>(), s>>>(ta, *md->tc_const);
+    }
     CKL("k_prior_grad_tc");
     return FOE_OK;
 }

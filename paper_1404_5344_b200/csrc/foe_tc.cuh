@@ -75,6 +75,15 @@ struct TcGeom {
     static_assert(NP % 16 == 0 && KT % 8 == 0, "MMA shape");
 };
 
+// Per-filter constants of K8's epilogue, in the kernel-parameter constant bank (FFMA operands
+// straight from c[], no shared-memory loads): sum_t k_i (DC restore), theta_i ln 2 (energy),
+// and the last tap of Kb (the CUDA-core column of the backward GEMM); zero past N_f.
+struct TcConst {
+    float sumk[kMaxFilters];
+    float thl[kMaxFilters];
+    float kbl[kMaxFilters];
+};
+
 struct TcArgs {
     K1Args k;                 // image geometry, slots, control, outputs (as K1)
     const float* bimg;        // [B_FLOATS] B operand images (hi/lo), built at model creation
@@ -146,7 +155,7 @@ __device__ __forceinline__ void tc_z_to_smem(uint32_t t_z, float* zs, int l) {
 }
 
 template <int M, int NP, int R>
-__global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta) {
+__global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const __grid_constant__ TcConst cc) {
     using G = TcGeom<M, NP, R>;
     constexpr int C = G::C, KT = G::KT, TAPS = G::TAPS, L = G::LANES;
     extern __shared__ __align__(128) float sm[];
@@ -269,7 +278,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta) {
         tc::wait_st();
         tc::fence_before_sync();
         __syncthreads();
-        if (t == 0 && j < G::RR) {
+        if (warp == 0 && j < G::RR) {
             tc::fence_after_sync();
             // the small cross terms first, then hi.hi: the fp32 accumulator loses less of them
 #pragma unroll
@@ -277,16 +286,16 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta) {
                 const uint32_t off = (uint32_t)(s * 2 * NP * 16);
                 const uint64_t bh = tc::sdesc_kmajor(b_base + off, NP * 16, 128);
                 const uint64_t bl = tc::sdesc_kmajor(b_base + G::BF_FLOATS * 4 + off, NP * 16, 128);
-                tc::mma_tf32_ts(tb + G::COL_D, tb + G::COL_AHI + s * 8, bl, idf, s > 0);
-                tc::mma_tf32_ts(tb + G::COL_D, tb + G::COL_ALO + s * 8, bh, idf, 1);
+                tc::mma_tf32_ts_warp(tb + G::COL_D, tb + G::COL_AHI + s * 8, bl, idf, s > 0);
+                tc::mma_tf32_ts_warp(tb + G::COL_D, tb + G::COL_ALO + s * 8, bh, idf, 1);
             }
 #pragma unroll
             for (int s = 0; s < NC8; ++s) {
                 const uint32_t off = (uint32_t)(s * 2 * NP * 16);
                 const uint64_t bh = tc::sdesc_kmajor(b_base + off, NP * 16, 128);
-                tc::mma_tf32_ts(tb + G::COL_D, tb + G::COL_AHI + s * 8, bh, idf, 1);
+                tc::mma_tf32_ts_warp(tb + G::COL_D, tb + G::COL_AHI + s * 8, bh, idf, 1);
             }
-            tc::mma_commit(&mbar_f);
+            tc::mma_commit_warp(&mbar_f);
         }
         if (j > 0) {
             // col2im of row jz = j - 1: Z row jz feeds output rows o = jz - a at column ox = l:
@@ -337,14 +346,14 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta) {
             const bool own = col_own && (j >= C) && (j < C + R) && (y0 - C + j < H);
             float zl;
             const float el = wg == 0
-                ? tc_epilogue<0, HF8>(tl + G::COL_D, tl + G::COL_PHI, tl + G::COL_PLO, uq, css, ths, kbl, zl)
-                : tc_epilogue<HF8, NF8>(tl + G::COL_D, tl + G::COL_PHI, tl + G::COL_PLO, uq, css, ths, kbl, zl);
+                ? tc_epilogue<0, HF8>(tl + G::COL_D, tl + G::COL_PHI, tl + G::COL_PLO, uq, cc.sumk, cc.thl, cc.kbl, zl)
+                : tc_epilogue<HF8, NF8>(tl + G::COL_D, tl + G::COL_PHI, tl + G::COL_PLO, uq, cc.sumk, cc.thl, cc.kbl, zl);
             zls[(j & 1) * 2 * L + wg * L + l] = zl;
             if (own) e_acc += (double)el;
             tc::wait_st();
             tc::fence_before_sync();
             __syncthreads();
-            if (t == 0) {
+            if (warp == 0) {
                 tc::fence_after_sync();
 #pragma unroll
                 for (int s = 0; s < NF8; ++s) {
@@ -352,16 +361,16 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta) {
                     const uint64_t bh = tc::sdesc_kmajor(b_base + 2 * G::BF_FLOATS * 4 + off, G::NB * 16, 128);
                     const uint64_t bl = tc::sdesc_kmajor(b_base + (2 * G::BF_FLOATS + G::BB_FLOATS) * 4 + off,
                                                          G::NB * 16, 128);
-                    tc::mma_tf32_ts(tb + G::COL_Z, tb + G::COL_PHI + s * 8, bl, idb, s > 0);
-                    tc::mma_tf32_ts(tb + G::COL_Z, tb + G::COL_PLO + s * 8, bh, idb, 1);
+                    tc::mma_tf32_ts_warp(tb + G::COL_Z, tb + G::COL_PHI + s * 8, bl, idb, s > 0);
+                    tc::mma_tf32_ts_warp(tb + G::COL_Z, tb + G::COL_PLO + s * 8, bh, idb, 1);
                 }
 #pragma unroll
                 for (int s = 0; s < NF8; ++s) {
                     const uint32_t off = (uint32_t)(s * 2 * G::NB * 16);
                     const uint64_t bh = tc::sdesc_kmajor(b_base + 2 * G::BF_FLOATS * 4 + off, G::NB * 16, 128);
-                    tc::mma_tf32_ts(tb + G::COL_Z, tb + G::COL_PHI + s * 8, bh, idb, 1);
+                    tc::mma_tf32_ts_warp(tb + G::COL_Z, tb + G::COL_PHI + s * 8, bh, idb, 1);
                 }
-                tc::mma_commit(&mbar_b);
+                tc::mma_commit_warp(&mbar_b);
             }
         }
     }
@@ -371,6 +380,327 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta) {
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc<G::TCOLS>(tb);
+}
+
+}  // namespace foe
+
+namespace foe {
+
+// =============================================================================================
+// K8 v4: the same computation, warp-specialised so that the rows of a tile flow through a
+// pipeline instead of a lock-step loop (one CTA per SM, 512 TMEM columns):
+//
+//   IM  warps 0-7   im2col of row j into A[j%2]                    (waits A_empty: MMAf(j-2) done)
+//   MMA warp 20     MMAf(j): A[j%2] -> D[j%2]; MMAb(j-1): P -> Z(j-1) in D[(j-1)%2]
+//   EP  warps 8-15  rho, rho' of row j from D[j%2] -> P, last-tap partial -> TMEM (zl[j%2])
+//                   (waits D_full[j%2]; writes P after P_empty: MMAb(j-1) done)
+//   ZC  warps 16-19 Z(j) -> smem, col2im, g rows                   (waits Z_full[j%2])
+//
+// mbarriers: A_full[2] (8 IM warps), A_empty[2] / D_full[2] / Z_full[2] / P_empty (tcgen05
+// commits), P_full (8 EP warps), D_empty[2] (4 ZC warps).  Parity of the k-th completion of a
+// two-slot barrier is (k & 1) with k = j / 2; of a one-slot barrier, j & 1.
+// =============================================================================================
+// v4 epilogue math for one half of the filters (HALF), from the D row in TMEM
+template <int NP, int HALF>
+__device__ __forceinline__ void tc4_ep_half(uint32_t t_d, float uq, const TcConst& cc, float& el, float& zl,
+                                            float (&ph)[NP / 2], float (&pl)[NP / 2], bool knockout) {
+    constexpr int HF = NP / 2;
+    float r[HF];
+    tc::tmem_ld16(t_d + HALF * HF, *reinterpret_cast<float(*)[16]>(r));
+    if constexpr (HF > 16) tc::tmem_ld8(t_d + HALF * HF + 16, *reinterpret_cast<float(*)[8]>(r + 16));
+    tc::wait_ld();
+    el = 0.f;
+    zl = 0.f;
+#pragma unroll
+    for (int e = 0; e < HF; ++e) {
+        if (knockout) { ph[e] = r[e]; pl[e] = 0.f; continue; }
+        const int i = HALF * HF + e;
+        const float rv = fmaf(uq, cc.sumk[i], r[e]);
+        const float d = fmaf(rv, rv, 1.f);
+        el = fmaf(cc.thl[i], lg2_approx(d), el);
+        const float pv = rv * rcp_approx(d);
+        zl = fmaf(pv, cc.kbl[i], zl);
+        ph[e] = tc::tf32_hi(pv);
+        pl[e] = tc::tf32_hi(pv - ph[e]);
+    }
+}
+
+template <int M, int NP, int R>
+struct Tc4Geom {
+    using B = TcGeom<M, NP, R>;
+    static constexpr int KT = B::KT, NB = B::NB, TAPS = B::TAPS, LANES = 128;
+    // TMEM columns
+    static constexpr int ND = 3;                     // D / Z ring depth
+    static constexpr int COL_A0 = 0;                 // A[s]: hi [s*2KT, s*2KT+KT), lo [+KT, +2KT)
+    static constexpr int COL_D0 = 4 * KT;            // D[s] at COL_D0 + s*NP, s = j % ND (Z(j) reuses it)
+    static constexpr int COL_P = COL_D0 + ND * NP;   // P hi [COL_P, +NP), lo [+NP, +2NP)
+    static constexpr int COL_ZL = COL_P + 2 * NP;    // last-tap partials: [slot][half] (2 ND columns)
+    static constexpr int TCOLS_USED = COL_ZL + 2 * ND;
+    static_assert(TCOLS_USED <= 512, "TMEM budget");
+    // shared memory (floats): B images | u tile | Zs[2][TAPS][LANES] | sum k | theta ln2
+    static constexpr int SM_B = 0;
+    static constexpr int SM_U = B::B_FLOATS;
+    static constexpr int SM_Z = SM_U + B::UY * B::UP;
+    static constexpr int SM_CS = SM_Z + 2 * TAPS * LANES;
+    static constexpr int SM_TH = SM_CS + NP;
+    static constexpr int SM_FLOATS = SM_TH + NP;
+    static constexpr int SMEM_BYTES = SM_FLOATS * 4 + 64;
+    static constexpr int THREADS = 21 * 32;      // 8 IM + 8 EP + 4 ZC + 1 MMA warps
+};
+
+// KO (profiling only, never selected by the library's API): 0 = full kernel; 1/2/3/4 skip the
+// work of IM / EP / ZC / the MMAs (barriers kept) to find the pipeline's limiting role.
+template <int M, int NP, int R, int KO = 0>
+__global__ void __launch_bounds__(21 * 32, 1) k_prior_grad_tc4(const TcArgs ta, const __grid_constant__ TcConst cc) {
+    using G = TcGeom<M, NP, R>;
+    using G4 = Tc4Geom<M, NP, R>;
+    constexpr int C = G::C, KT = G::KT, TAPS = G::TAPS, L = G::LANES, NB = G::NB;
+    extern __shared__ __align__(128) float sm[];
+    float* bsm = sm + G4::SM_B;
+    float* us = sm + G4::SM_U;
+    float* zs = sm + G4::SM_Z;
+    float* css = sm + G4::SM_CS;
+    float* ths = sm + G4::SM_TH;
+    __shared__ uint32_t tbase_s;
+    constexpr int ND = G4::ND;
+    __shared__ __align__(8) uint64_t bar_afull[2], bar_aempty[2], bar_dfull[ND], bar_dempty[ND], bar_zfull[ND];
+    __shared__ __align__(8) uint64_t bar_pfull, bar_pempty;
+    __shared__ double red[32];
+
+    const K1Args& args = ta.k;
+    const int b = blockIdx.y;
+    int wslot = 0, gslot = 0;
+    if (args.ctl != nullptr) {
+        const ImgCtl& c = args.ctl[b];
+        if (!c.active) return;
+        wslot = args.which_cur ? c.cur : c.cand;
+        gslot = args.which_cur ? c.gcur : c.gcand;
+    }
+    const int H = args.H, W = args.W;
+    const size_t HW = (size_t)H * W;
+    const int tile = blockIdx.x;
+    const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
+    const int y0 = ty * R, x0 = tx * G::OW;
+    const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int l = (warp & 3) * 32 + lane;                       // TMEM lane = response pixel
+    const bool udom = args.udom != 0;
+
+    // ---- prologue (all warps): TMEM, barriers, B images, u tile ------------------------------
+    if (warp == 0) tc::tmem_alloc<512>(&tbase_s);
+    if (t == 0) {
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&bar_afull[s], 8);
+            tc::mbar_init(&bar_aempty[s], 1);
+        }
+        for (int s = 0; s < ND; ++s) {
+            tc::mbar_init(&bar_dfull[s], 1);
+            tc::mbar_init(&bar_dempty[s], 4);
+            tc::mbar_init(&bar_zfull[s], 1);
+        }
+        tc::mbar_init(&bar_pfull, 8);
+        tc::mbar_init(&bar_pempty, 1);
+        tc::mbar_fence_init();
+    }
+    {
+        const float4* src = reinterpret_cast<const float4*>(ta.bimg);
+        float4* dst = reinterpret_cast<float4*>(bsm);
+        for (int i = t; i < G::B_FLOATS / 4; i += G4::THREADS) dst[i] = __ldg(src + i);
+    }
+    const int yc = min(y0 + R / 2, H - 1), xc = min(x0 + G::OW / 2, W - 1);
+    const double wc = w[(size_t)yc * W + xc];
+    const float cst = (float)(udom ? wc : exp(wc));
+    if (t < NP) {
+        css[t] = __ldg(ta.sumk + t);
+        ths[t] = __ldg(ta.theta_ln2 + t);
+    }
+    const double* halo = args.halo;
+    for (int idx = t; idx < G::UY * G::UX; idx += G4::THREADS) {
+        const int uy = idx / G::UX, ux = idx - uy * G::UX;
+        const int y = y0 - 2 * C + uy, gx = wrap_idx(x0 - 2 * C + ux, W);
+        const double* src;
+        if (halo == nullptr) src = w + (size_t)wrap_idx(y, H) * W;
+        else if (y < 0) src = halo + (size_t)(kHalo + y) * W;
+        else if (y >= H) src = halo + (size_t)(kHalo + y - H) * W;
+        else src = w + (size_t)y * W;
+        us[uy * G::UP + ux] = udom ? (float)(src[gx] - (double)cst) : cst * expm1f((float)(src[gx] - wc));
+    }
+    tc::fence_proxy_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tb = tbase_s;
+    const uint32_t tl = tb + ((uint32_t)((warp & 3) * 32) << 16);
+    double e_acc = 0.0;
+
+    if (warp < 8) {
+        // ================================ IM: im2col ================================
+        // two warp groups: taps chunks [0, H8) and [H8, KT/8)
+        constexpr int H8 = (KT / 8 + 1) / 2;
+        const int ig = warp >> 2;
+#pragma unroll 1
+        for (int j = 0; j < G::RR; ++j) {
+            const int s = j & 1;
+            if (j >= 2) {
+                tc::mbar_wait(&bar_aempty[s], (uint32_t)(((j >> 1) - 1) & 1));
+                tc::fence_after_sync();
+            }
+            const float* up = us + j * G::UP + l;
+            const float vc = up[C * G::UP + C];
+            const uint32_t a_hi = tl + G4::COL_A0 + s * 2 * KT, a_lo = a_hi + KT;
+            if (KO != 1) {
+                if (ig == 0) tc_im2col<M, G::UP, 0, H8>(up, vc, a_hi, a_lo);
+                else tc_im2col<M, G::UP, H8, KT / 8>(up, vc, a_hi, a_lo);
+            }
+            tc::wait_st();
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&bar_afull[s]);
+        }
+    } else if (warp < 16) {
+        // ================================ EP: rho, rho' =============================
+        const int half = (warp - 8) >> 2;                   // filters [half*NP/2, (half+1)*NP/2)
+        const int lx = x0 - C + l;
+        const bool col_own = (l >= C) && (l < C + G::OW) && (lx < W);
+#pragma unroll 1
+        for (int j = 0; j < G::RR; ++j) {
+            const int s = j % ND;
+            tc::mbar_wait(&bar_dfull[s], (uint32_t)((j / ND) & 1));
+            tc::fence_after_sync();
+            const float uq = us[(j + C) * G::UP + l + C] + cst;   // window centre u_q (DC restore)
+            constexpr int HF = NP / 2;
+            float el, zl, ph[HF], pl[HF];
+            if (half == 0) tc4_ep_half<NP, 0>(tl + G4::COL_D0 + s * NP, uq, cc, el, zl, ph, pl, KO == 2);
+            else tc4_ep_half<NP, 1>(tl + G4::COL_D0 + s * NP, uq, cc, el, zl, ph, pl, KO == 2);
+            const bool own = col_own && (j >= C) && (j < C + R) && (y0 - C + j < H);
+            if (own) e_acc += (double)el;
+            if (j >= 1) {                                       // P is free once MMAb(j-1) is done
+                tc::mbar_wait(&bar_pempty, (uint32_t)((j - 1) & 1));
+                tc::fence_after_sync();
+            }
+#pragma unroll
+            for (int c8 = 0; c8 < HF / 8; ++c8) {
+                tc::tmem_st8(tl + G4::COL_P + half * HF + c8 * 8, *reinterpret_cast<float(*)[8]>(ph + c8 * 8));
+                tc::tmem_st8(tl + G4::COL_P + NP + half * HF + c8 * 8, *reinterpret_cast<float(*)[8]>(pl + c8 * 8));
+            }
+            tc::tmem_st1(tl + G4::COL_ZL + s * 2 + half, zl);
+            tc::wait_st();
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&bar_pfull);
+        }
+    } else if (warp < 20) {
+        // ================================ ZC: Z, col2im, g ==========================
+        float acc[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) acc[k] = 0.f;
+        float* gout = args.g + (size_t)gslot * args.g_slot_stride + (size_t)b * HW;
+        const bool out_col = (l < G::OW) && (x0 + l < W);
+#pragma unroll 1
+        for (int j = 0; j < G::RR; ++j) {
+            const int s = j % ND, zb = j & 1;
+            tc::mbar_wait(&bar_zfull[s], (uint32_t)((j / ND) & 1));
+            tc::fence_after_sync();
+            static_assert(NB == 48 || NB == 24 || NB == 8, "Z readout shapes");
+            float z[NB < 32 ? 32 : NB];
+            if constexpr (NB == 48) {
+                tc::tmem_ld32(tl + G4::COL_D0 + s * NP, z);
+                tc::tmem_ld16(tl + G4::COL_D0 + s * NP + 32, *reinterpret_cast<float(*)[16]>(z + 32));
+            } else if constexpr (NB == 24) {
+                tc::tmem_ld16(tl + G4::COL_D0 + s * NP, *reinterpret_cast<float(*)[16]>(z));
+                tc::tmem_ld8(tl + G4::COL_D0 + s * NP + 16, *reinterpret_cast<float(*)[8]>(z + 16));
+            } else {
+                tc::tmem_ld8(tl + G4::COL_D0 + s * NP, *reinterpret_cast<float(*)[8]>(z));
+            }
+            float zl0, zl1;
+            tc::tmem_ld2(tl + G4::COL_ZL + s * 2, zl0, zl1);
+            tc::wait_ld();
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&bar_dempty[s]);   // D[s] may take MMAf(j+2)
+            float* zr = zs + zb * TAPS * L;
+            if (KO == 3) { acc[0] += z[0] + zl0 + zl1; continue; }
+#pragma unroll
+            for (int k = 0; k < NB; ++k) zr[k * L + l] = z[k];
+            zr[NB * L + l] = zl0 + zl1;
+            tc::named_sync(1, 128);
+            // col2im of row j: output rows o = j - a; acc[a] holds row j - a (shifted each row)
+#pragma unroll
+            for (int a = 0; a < M; ++a) {
+                float sa = 0.f;
+#pragma unroll
+                for (int bb = 0; bb < M; ++bb) sa += zr[(a * M + bb) * L + l + bb];
+                acc[a] += sa;
+            }
+            const int o = j - 2 * C;
+            if (o >= 0 && o < R && out_col && y0 + o < H) {
+                const float u = udom ? 1.0f : us[(o + 2 * C) * G::UP + l + 2 * C] + cst;   // W = diag(e^w)
+                gout[(size_t)(y0 + o) * W + x0 + l] = u * acc[M - 1];
+            }
+#pragma unroll
+            for (int k = M - 1; k > 0; --k) acc[k] = acc[k - 1];
+            acc[0] = 0.f;
+        }
+    } else {
+        // ================================ MMA issuer (whole warp; one elected lane issues) ===
+        const uint32_t idf = tc::idesc_tf32(128, NP), idb = tc::idesc_tf32(128, NB);
+        const uint32_t b_base = tc::smem_u32(bsm);
+#pragma unroll 1
+        for (int j = 0; j <= G::RR; ++j) {
+            if (j < G::RR) {
+                const int s = j & 1, sd = j % ND;
+                tc::mbar_wait(&bar_afull[s], (uint32_t)((j >> 1) & 1));
+                if (j >= ND) tc::mbar_wait(&bar_dempty[sd], (uint32_t)(((j / ND) - 1) & 1));
+                tc::fence_after_sync();
+                const uint32_t a_hi = tb + G4::COL_A0 + s * 2 * KT, a_lo = a_hi + KT, d = tb + G4::COL_D0 + sd * NP;
+#pragma unroll
+                for (int k = 0; k < KT / 8; ++k) {
+                    const uint32_t off = (uint32_t)(k * 2 * NP * 16);
+                    const uint64_t bh = tc::sdesc_kmajor(b_base + off, NP * 16, 128);
+                    const uint64_t bl = tc::sdesc_kmajor(b_base + G::BF_FLOATS * 4 + off, NP * 16, 128);
+                    if (KO != 4) tc::mma_tf32_ts_warp(d, a_hi + k * 8, bl, idf, k > 0);
+                    if (KO != 4) tc::mma_tf32_ts_warp(d, a_lo + k * 8, bh, idf, 1);
+                }
+#pragma unroll
+                for (int k = 0; k < KT / 8; ++k) {
+                    const uint64_t bh = tc::sdesc_kmajor(b_base + (uint32_t)(k * 2 * NP * 16), NP * 16, 128);
+                    if (KO != 4) tc::mma_tf32_ts_warp(d, a_hi + k * 8, bh, idf, 1);
+                }
+                tc::mma_commit_warp(&bar_aempty[s]);
+                tc::mma_commit_warp(&bar_dfull[sd]);
+            }
+            if (j >= 1) {
+                const int jb = j - 1, s = jb % ND;
+                tc::mbar_wait(&bar_pfull, (uint32_t)(jb & 1));
+                tc::fence_after_sync();
+                const uint32_t z = tb + G4::COL_D0 + s * NP, p_hi = tb + G4::COL_P, p_lo = p_hi + NP;
+#pragma unroll
+                for (int k = 0; k < NP / 8; ++k) {
+                    const uint32_t off = (uint32_t)(k * 2 * NB * 16);
+                    const uint64_t bh = tc::sdesc_kmajor(b_base + 2 * G::BF_FLOATS * 4 + off, NB * 16, 128);
+                    const uint64_t bl = tc::sdesc_kmajor(b_base + (2 * G::BF_FLOATS + G::BB_FLOATS) * 4 + off,
+                                                         NB * 16, 128);
+                    if (KO != 4) tc::mma_tf32_ts_warp(z, p_hi + k * 8, bl, idb, k > 0);
+                    if (KO != 4) tc::mma_tf32_ts_warp(z, p_lo + k * 8, bh, idb, 1);
+                }
+#pragma unroll
+                for (int k = 0; k < NP / 8; ++k) {
+                    const uint64_t bh = tc::sdesc_kmajor(b_base + 2 * G::BF_FLOATS * 4 + (uint32_t)(k * 2 * NB * 16),
+                                                         NB * 16, 128);
+                    if (KO != 4) tc::mma_tf32_ts_warp(z, p_hi + k * 8, bh, idb, 1);
+                }
+                tc::mma_commit_warp(&bar_pempty);
+                tc::mma_commit_warp(&bar_zfull[s]);
+            }
+        }
+    }
+    // (a7) per-CTA energy partial (fixed order over all threads; only EP threads contribute)
+    __syncwarp();
+    const double e = block_sum_d(e_acc, red);
+    if (t == 0) args.epart[(size_t)b * args.ntiles * args.groups + blockIdx.x] = e;
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tb);
 }
 
 }  // namespace foe
