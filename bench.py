@@ -53,6 +53,7 @@ def parse_args():
     ap.add_argument("--images", type=int, default=0, help="images per GPU (default: the config's batch)")
     ap.add_argument("--iters", type=int, default=0, help="override iteration count (quick runs only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-p2p", action="store_true", help="c5: ghost rows over ncclSend/Recv instead of K2 peer stores")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=60,
                     help="oracle sample: iterations on one image (~10 s of host CPU work)")
@@ -436,6 +437,28 @@ def run_slabs(args, cfg):
     f_dev = torch.as_tensor(np.ascontiguousarray(f_full[r0:r1]), device=dev)
     cfgc = P.ipiano_config_default(max_iters=cfg.iters, record_trace=0)
     sl = P.ipiano_slabs_create(md, f_dev, Hg, lam=lam, lipschitz_init=L0, cfg=cfgc, comm=comm)
+    # fused ghost-row exchange: K2 stores straight into the ring neighbours' ghost rows (CUDA IPC
+    # over NVLink); the NCCL send/recv path stays if a mapping cannot be opened
+    exchange = "ncclSend/Recv"
+    if not args.no_p2p:
+        import torch.distributed as dist
+        h = P.ipiano_slabs_halo_handle(sl)
+        hs = [h]
+        if ws > 1:
+            hs = [None] * ws
+            dist.all_gather_object(hs, h)
+        up, dn = D.ring_neighbours(rank, ws)
+        ok = True
+        try:
+            P.ipiano_slabs_connect_peers(sl, hs[up], hs[dn])
+        except P.FoeError as e:
+            ok = False
+            print(f"[bench] fused exchange unavailable on rank {rank}: {e}", file=sys.stderr)
+        if D.all_true(ok):
+            exchange = "K2 peer stores (CUDA IPC/NVLink) + NCCL ordering all-reduce"
+        elif ok:
+            P.ipiano_slabs_disconnect_peers(sl)      # every rank must take the same path
+        P.ipiano_slabs_reset(sl, f_dev, L0)
     member = P.ipiano_slabs_member(sl, 0)
     u_dev = torch.empty((r1 - r0, W), dtype=torch.float32, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
@@ -491,7 +514,7 @@ def run_slabs(args, cfg):
                        "filters": f"{cfg.n_filters}x{cfg.m}x{cfg.m}", "iters": cfg.iters,
                        "slab_rows_per_gpu": r1 - r0,
                        "l2": "inputs (8192^2 fp64 state, 1.6 GB) larger than L2; 256 MiB flush between steps",
-                       "parallelism": f"row slabs x{ws}: 6-row ghost exchange (ncclSend/Recv) + band all-gather per trial"},
+                       "parallelism": f"row slabs x{ws}: 6-row ghost exchange ({exchange}) + band all-gather per trial"},
             "roofline": roof,
             "cpu_baseline": None, "e2e": None, "gpu_launches": int(launches), "clocks": clocks,
             "trials_per_iter": trials_per_step / cfg.iters, "lipschitz_ms": lipschitz_ms,

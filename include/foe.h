@@ -293,6 +293,20 @@ foe_status ipiano_slabs_solve(ipiano_slabs* slabs, void* stream);
 /* u = e^w (and/or w) of the slabs owned by this process: the whole scene when comm == NULL,
  * this rank's slab otherwise (device, [rows][W]). */
 foe_status ipiano_slabs_get_iterate(const ipiano_slabs* slabs, double* w_out, float* u_out, void* stream);
+/* Fused ghost-row exchange across processes (one GPU each, peer access over NVLink): K2 stores
+ * its boundary rows straight into the neighbours' ghost buffers through CUDA IPC mappings,
+ * replacing the ncclSend/ncclRecv step by a 1-element NCCL all-reduce that orders every rank's
+ * K2 before any rank's K1.  Each rank exports its handle (64 bytes), the ranks exchange them
+ * (e.g. torch.distributed.all_gather_object), and every rank connects its ring neighbours
+ * (up = rank-1, down = rank+1 mod nranks; its own handle where a neighbour is itself).
+ * In-process slabs (comm == NULL) always exchange this way (device pointers, no handles).
+ * FOE_ERR_COMM if a mapping cannot be opened (no peer access): keep the NCCL path then. */
+foe_status ipiano_slabs_halo_handle(const ipiano_slabs* slabs, void* handle_out);
+foe_status ipiano_slabs_connect_peers(ipiano_slabs* slabs, const void* up_handle, const void* down_handle);
+/* Back to the ncclSend/ncclRecv exchange (every rank must use the same path: when any rank
+ * fails to connect, all disconnect).  Re-initialise (ipiano_slabs_reset) after either call. */
+foe_status ipiano_slabs_disconnect_peers(ipiano_slabs* slabs);
+
 /* The per-slab iPiano state j of this process (for ipiano_get_counters / ipiano_get_trace /
  * ipiano_profile / ipiano_profile_read; every slab holds the same control block and trace).
  * The returned state is owned by `slabs`: do not destroy it. */

@@ -925,7 +925,7 @@ foe_status state_init(ipiano_state* st, const float* f, const double* lipschitz_
     if (st->cfg.record_trace)
         CK(cudaMemsetAsync(st->trace, 0, sizeof(double) * B * (st->cfg.max_iters + 1) * 8, st->s));
     foe::k_init<<<dim3(st->nblk2, B), kThreads, 0, st->s>>>(f, st->ft, st->w, n, st->ppart, st->nblk2, st->ctl,
-                                                             st->HW, kPxt2, nullptr, 0,
+                                                             st->HW, kPxt2, nullptr, nullptr, 0,
                                                              st->model->term == FOE_DATA_IDIV);
     count_launch(1);
     CKL("k_init");
@@ -1279,9 +1279,12 @@ foe_status ipiano_run(const foe_model* md, const float* f, int B, int H, int W, 
 //
 // One periodic scene cut into `nslabs` equal row slabs (BASELINE.json
 // configs[4]).  Per trial round every slab runs
-//   A  K2 on its rows (w+ of its first/last kHalo rows also packed into halo_send)
+//   A  K2 on its rows; w+ of its first/last kHalo rows is stored by K2 itself straight into the
+//      neighbours' ghost rows (in-process slabs, or peer GPUs through CUDA IPC mappings), or
+//      into a send buffer for NCCL
 //   X  halo exchange: top ghost rows <- the slab above's last kHalo rows, bottom ghost rows
-//      <- the slab below's first kHalo rows (ring: slab 0's top comes from slab G-1)
+//      <- the slab below's first kHalo rows (ring: slab 0's top comes from slab G-1) -- nothing
+//      to do in-process; a 1-element NCCL all-reduce (ordering) with peers; else ncclSend/Recv
 //   B  K1 on its rows, reading the ghost rows (energy over owned responses, g+ on owned px)
 //   R  per-band (64-row) partials of K1 and K2 into its part of the global band array
 //   Y  gather of the band arrays (NCCL all-gather; in-process slabs share the array)
@@ -1304,6 +1307,7 @@ struct NcclApi {
     ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -1327,9 +1331,10 @@ const NcclApi& nccl_api() {
             api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
             api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
             api.AllGather = (decltype(api.AllGather))dlsym(h, "ncclAllGather");
+            api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
             api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
             api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.GroupStart && api.GroupEnd &&
-                     api.Send && api.Recv && api.AllGather && api.GetErrorString;
+                     api.Send && api.Recv && api.AllGather && api.AllReduce && api.GetErrorString;
         }
     }
     lock.store(0);
@@ -1363,7 +1368,15 @@ struct ipiano_slabs {
     std::vector<ipiano_state*> members;    // slabs owned by this process, in ring order
     double* band_all = nullptr;            // [nb_global][kNumPart]
     double* halo = nullptr;                // [members][2][kHalo][W] received ghost rows
-    double* halo_send = nullptr;           // [members][2][kHalo][W] own boundary rows
+    double* halo_send = nullptr;           // [members][2][kHalo][W] own boundary rows (NCCL send path)
+    // fused exchange: K2 stores its boundary rows straight into the neighbours' ghost rows
+    // (in-process slabs always; across processes after ipiano_slabs_connect_peers, through
+    // CUDA IPC mappings of the neighbours' ghost buffers over NVLink)
+    bool p2p = false;
+    double* peer_up = nullptr;             // the slab above's ghost buffer (mapped), or own (1 rank)
+    double* peer_dn = nullptr;             // the slab below's ghost buffer
+    bool up_opened = false, dn_opened = false;
+    int* barrier_buf = nullptr;            // 1 int: the NCCL all-reduce that orders peer stores before K1
     cudaStream_t s = nullptr;
     cudaEvent_t sync_ev = nullptr;
     cudaGraphExec_t graph = nullptr;
@@ -1373,6 +1386,23 @@ struct ipiano_slabs {
 namespace {
 
 size_t halo_elems(const ipiano_slabs* g) { return (size_t)2 * foe::kHalo * g->W; }
+
+// Where member j's boundary rows go: top rows -> the slab above's bottom ghost rows, bottom rows
+// -> the slab below's top ghost rows (or this slab's send buffer on the NCCL send/recv path).
+void halo_dst(ipiano_slabs* g, int j, double*& up_dst, double*& dn_dst) {
+    const size_t he = halo_elems(g), hp = (size_t)foe::kHalo * g->W;
+    if (g->comm == nullptr) {
+        const int n = (int)g->members.size();
+        up_dst = g->halo + (size_t)((j + n - 1) % n) * he + hp;
+        dn_dst = g->halo + (size_t)((j + 1) % n) * he;
+    } else if (g->p2p) {
+        up_dst = g->peer_up + hp;
+        dn_dst = g->peer_dn;
+    } else {
+        up_dst = g->halo_send;
+        dn_dst = g->halo_send + hp;
+    }
+}
 
 // A (K2 + pack) for member j
 foe_status slab_k2(ipiano_slabs* g, int j) {
@@ -1390,7 +1420,8 @@ foe_status slab_k2(ipiano_slabs* g, int j) {
     a2.groups = st->groups;
     a2.nblk = st->nblk2;
     a2.HW = st->HW;
-    a2.halo_send = g->halo_send + j * halo_elems(g);
+    halo_dst(g, j, a2.halo_up, a2.halo_dn);
+    a2.halo_sys_fence = g->p2p && g->comm && g->comm->nranks > 1;
     a2.halo_px = (size_t)foe::kHalo * g->W;
     a2.idiv = st->model->term == FOE_DATA_IDIV;
     foe::k_inertial_prox<kPxt2><<<dim3(st->nblk2, 1), kThreads, 0, g->s>>>(a2);
@@ -1403,19 +1434,15 @@ foe_status slab_k2(ipiano_slabs* g, int j) {
 // kHalo rows of slab i+1 (periodic ring).
 foe_status slab_exchange(ipiano_slabs* g) {
     const size_t hp = (size_t)foe::kHalo * g->W;
-    if (g->comm == nullptr) {
-        const int n = (int)g->members.size();
-        for (int j = 0; j < n; ++j) {
-            const int up = (j + n - 1) % n, dn = (j + 1) % n;
-            double* dst = g->halo + j * halo_elems(g);
-            CK(cudaMemcpyAsync(dst, g->halo_send + up * halo_elems(g) + hp, hp * sizeof(double),
-                               cudaMemcpyDeviceToDevice, g->s));
-            CK(cudaMemcpyAsync(dst + hp, g->halo_send + dn * halo_elems(g), hp * sizeof(double),
-                               cudaMemcpyDeviceToDevice, g->s));
-        }
+    if (g->comm == nullptr) return FOE_OK;   // K2 stored the rows into the neighbours' ghost buffers
+    const NcclApi& api = nccl_api();
+    if (g->p2p) {
+        // the peers' K2 stored straight into our ghost rows; a 1-element all-reduce orders every
+        // rank's K2 (and its system-scope fence) before any rank's K1
+        if (g->comm->nranks > 1)
+            CKN(api.AllReduce(g->barrier_buf, g->barrier_buf, 1, ncclInt32, ncclSum, g->comm->comm, g->s));
         return FOE_OK;
     }
-    const NcclApi& api = nccl_api();
     const int R = g->comm->nranks, r = g->comm->rank;
     const int up = (r + R - 1) % R, dn = (r + 1) % R;
     // One fixed posting order on every rank, so that two messages between the same pair of
@@ -1515,8 +1542,10 @@ foe_status slab_init(ipiano_slabs* g, const float* f, double L_init, cudaStream_
         CK(cudaMemcpyAsync(st->ctl, st->hctl, sizeof(ImgCtl), cudaMemcpyHostToDevice, g->s));
         if (st->cfg.record_trace)
             CK(cudaMemsetAsync(st->trace, 0, sizeof(double) * (st->cfg.max_iters + 1) * 8, g->s));
+        double *up_dst, *dn_dst;
+        halo_dst(g, (int)j, up_dst, dn_dst);
         foe::k_init<<<dim3(st->nblk2, 1), kThreads, 0, g->s>>>(f + j * HWs, st->ft, st->w, HWs, st->ppart, st->nblk2,
-                                                                st->ctl, HWs, kPxt2, g->halo_send + j * halo_elems(g),
+                                                                st->ctl, HWs, kPxt2, up_dst, dn_dst,
                                                                 (size_t)foe::kHalo * g->W, st->model->term == FOE_DATA_IDIV);
         count_launch(1);
         CKL("k_init (slab)");
@@ -1636,6 +1665,9 @@ void ipiano_slabs_destroy(ipiano_slabs* g) {
     cudaFree(g->band_all);
     cudaFree(g->halo);
     cudaFree(g->halo_send);
+    if (g->up_opened) cudaIpcCloseMemHandle(g->peer_up);
+    if (g->dn_opened && g->peer_dn != g->peer_up) cudaIpcCloseMemHandle(g->peer_dn);
+    if (g->barrier_buf) cudaFree(g->barrier_buf);
     if (g->sync_ev) cudaEventDestroy(g->sync_ev);
     if (g->s) cudaStreamDestroy(g->s);
     delete g;
@@ -1786,6 +1818,64 @@ foe_status ipiano_slabs_get_iterate(const ipiano_slabs* g, double* w_out, float*
     }
     CK(cudaEventRecord(gg->sync_ev, gg->s));
     CK(cudaStreamWaitEvent(user, gg->sync_ev, 0));
+    return FOE_OK;
+}
+
+foe_status ipiano_slabs_halo_handle(const ipiano_slabs* g, void* handle_out) {
+    if (!g || !handle_out) return fail(FOE_ERR_INVALID_ARGUMENT, "slabs or handle_out is NULL");
+    if (!g->comm) return fail(FOE_ERR_INVALID_ARGUMENT, "in-process slabs exchange directly; no handle needed");
+    CK(cudaSetDevice(g->model->dev));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, g->halo));
+    std::memcpy(handle_out, &h, sizeof(h));
+    return FOE_OK;
+}
+
+foe_status ipiano_slabs_connect_peers(ipiano_slabs* g, const void* up_handle, const void* down_handle) {
+    if (!g || !up_handle || !down_handle) return fail(FOE_ERR_INVALID_ARGUMENT, "slabs or a handle is NULL");
+    if (!g->comm) return fail(FOE_ERR_INVALID_ARGUMENT, "in-process slabs exchange directly");
+    if (g->p2p) return fail(FOE_ERR_INVALID_ARGUMENT, "peers already connected");
+    CK(cudaSetDevice(g->model->dev));
+    const int R = g->comm->nranks, r = g->comm->rank;
+    const int up = (r + R - 1) % R, dn = (r + 1) % R;
+    auto open = [&](const void* hb, int peer, double*& ptr, bool& opened) -> foe_status {
+        if (peer == r) { ptr = g->halo; opened = false; return FOE_OK; }   // 1 rank: the ring is this slab
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, hb, sizeof(h));
+        void* p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(FOE_ERR_COMM, "cudaIpcOpenMemHandle of rank %d's ghost rows failed: %s", peer,
+                        cudaGetErrorString(e));
+        }
+        ptr = (double*)p;
+        opened = true;
+        return FOE_OK;
+    };
+    foe_status rs = open(up_handle, up, g->peer_up, g->up_opened);
+    if (rs != FOE_OK) return rs;
+    if (dn == up) { g->peer_dn = g->peer_up; g->dn_opened = g->up_opened; }
+    else if ((rs = open(down_handle, dn, g->peer_dn, g->dn_opened)) != FOE_OK) return rs;
+    if (!g->barrier_buf) {
+        CK(cudaMalloc((void**)&g->barrier_buf, sizeof(int)));
+        CK(cudaMemset(g->barrier_buf, 0, sizeof(int)));
+    }
+    g->p2p = true;
+    if (g->graph) { cudaGraphExecDestroy(g->graph); g->graph = nullptr; }   // recapture with the new path
+    return FOE_OK;
+}
+
+foe_status ipiano_slabs_disconnect_peers(ipiano_slabs* g) {
+    if (!g) return fail(FOE_ERR_INVALID_ARGUMENT, "slabs is NULL");
+    CK(cudaSetDevice(g->model->dev));
+    CK(cudaStreamSynchronize(g->s));
+    if (g->up_opened) cudaIpcCloseMemHandle(g->peer_up);
+    if (g->dn_opened && g->peer_dn != g->peer_up) cudaIpcCloseMemHandle(g->peer_dn);
+    g->peer_up = g->peer_dn = nullptr;
+    g->up_opened = g->dn_opened = false;
+    g->p2p = false;
+    if (g->graph) { cudaGraphExecDestroy(g->graph); g->graph = nullptr; }
     return FOE_OK;
 }
 

@@ -759,9 +759,13 @@ struct K2Args {
     SolverParams sp;
     int groups, nblk;
     size_t HW;
-    // Row slab: w+ of the first and last kHalo rows is also written to halo_send
-    // ([2][kHalo][W], the rows the ring neighbours need); nullptr = no slab.
-    double* halo_send;
+    // Row slab: w+ of the first kHalo rows is also stored at halo_up (the slab above's bottom
+    // ghost rows), of the last kHalo rows at halo_dn (the slab below's top ghost rows) -- a
+    // neighbour's buffer written directly (same GPU, or a peer GPU over NVLink through a CUDA IPC
+    // mapping), or this slab's send buffer for NCCL; nullptr = no slab.
+    double* halo_up;
+    double* halo_dn;
+    int halo_sys_fence;    // peer-GPU destination: make the stores visible system-wide
     size_t halo_px;        // kHalo * W
     int idiv;              // model (6) in u: closed-form prox of (lam/2)(u^2 - 2 f^2 log u), lam = lam1
 };
@@ -802,9 +806,9 @@ k_inertial_prox(const K2Args a) {  // (3 CTAs/SM: <= 80 registers)
             it = prox_newton(what, f, alpha, l1, l2, a.sp.newton_tol, a.sp.newton_cap, z, em, ep);
         }
         wn[p] = z;
-        if (a.halo_send != nullptr) {
-            if (p < a.halo_px) a.halo_send[p] = z;
-            else if (p >= a.HW - a.halo_px) a.halo_send[p - (a.HW - 2 * a.halo_px)] = z;
+        if (a.halo_up != nullptr) {
+            if (p < a.halo_px) a.halo_up[p] = z;
+            else if (p >= a.HW - a.halo_px) a.halo_dn[p - (a.HW - a.halo_px)] = z;
         }
         const double d = z - wv;
         gd += gv * d;
@@ -821,6 +825,7 @@ k_inertial_prox(const K2Args a) {  // (3 CTAs/SM: <= 80 registers)
         if (it < 0) fail += 1.0; else nit = fmax(nit, (double)it);
         if (!(z == z)) wmax = INFINITY;
     }
+    if (a.halo_sys_fence) __threadfence_system();
     // one fixed-order block reduction of the 7 partials (sums, except slots 4/5 = max)
     double v[7] = {gd, dd, Gp, ww, wmax, nit, fail};
 #pragma unroll
@@ -922,7 +927,7 @@ __global__ void __launch_bounds__(kThreads) k_decide(const K3Args a) {
 // partials of G(w^0) (slot 2 of ppart).
 __global__ void __launch_bounds__(kThreads)
 k_init(const float* f, float* ft, double* w, size_t w_slot_stride, double* ppart, int nblk,
-       const ImgCtl* ctl, size_t HW, int pxt, double* halo_send, size_t halo_px, int idiv) {
+       const ImgCtl* ctl, size_t HW, int pxt, double* halo_up, double* halo_dn, size_t halo_px, int idiv) {
     __shared__ double red[32];
     const int b = blockIdx.y;
     const double l1 = ctl[b].lam1, l2 = ctl[b].lam2;
@@ -938,14 +943,15 @@ k_init(const float* f, float* ft, double* w, size_t w_slot_stride, double* ppart
         const double z = idiv ? fd : log(fd);          // u^0 = f~ (model (6)) or w^0 = log f~
         w[gi] = z;
         w[w_slot_stride + gi] = z;
-        if (halo_send != nullptr) {   // row slab (B = 1): rows the ring neighbours need
-            if (p < halo_px) halo_send[p] = z;
-            else if (p >= HW - halo_px) halo_send[p - (HW - 2 * halo_px)] = z;
+        if (halo_up != nullptr) {   // row slab (B = 1): rows the ring neighbours need (as K2)
+            if (p < halo_px) halo_up[p] = z;
+            else if (p >= HW - halo_px) halo_dn[p - (HW - halo_px)] = z;
         }
         const double f2 = fd * fd;
         G += idiv ? 0.5 * l1 * (z * z - 2.0 * f2 * log(z))
                   : 0.5 * l1 * (2.0 * z + f2 * exp(-2.0 * z)) + 0.5 * l2 * (exp(2.0 * z) - 2.0 * f2 * z);
     }
+    if (halo_up != nullptr) __threadfence_system();
     const double s = block_sum_d(G, red);
     if (threadIdx.x == 0) {
         double* out = ppart + ((size_t)b * nblk + blockIdx.x) * kNumPart;

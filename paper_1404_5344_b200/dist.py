@@ -99,3 +99,13 @@ def share_bytes(payload, src: int = 0) -> bytes:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         dist.broadcast_object_list(obj, src=src)
     return obj[0]
+
+
+def all_true(flag: bool) -> bool:
+    """True on every rank iff the flag is true on every rank (collective decisions)."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return bool(flag)
+    vals = [None] * dist.get_world_size()
+    dist.all_gather_object(vals, bool(flag))
+    return all(vals)

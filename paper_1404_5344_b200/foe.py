@@ -32,6 +32,7 @@ EXPORTED = (
     "ipiano_state_destroy", "ipiano_state_stencil", "ipiano_run",
     "foe_model_set_stencil", "foe_comm_unique_id", "foe_comm_create", "foe_comm_destroy", "ipiano_slabs_create", "ipiano_slabs_reset",
     "ipiano_slabs_solve", "ipiano_slabs_get_iterate", "ipiano_slabs_member", "ipiano_slabs_destroy",
+    "ipiano_slabs_halo_handle", "ipiano_slabs_connect_peers", "ipiano_slabs_disconnect_peers",
 )
 
 
@@ -107,6 +108,9 @@ def lib():
     L.ipiano_slabs_solve.argtypes = [_vp, _vp]
     L.ipiano_slabs_get_iterate.argtypes = [_vp, _vp, _vp, _vp]
     L.ipiano_slabs_member.argtypes = [_vp, C.c_int, C.POINTER(_vp)]
+    L.ipiano_slabs_halo_handle.argtypes = [_vp, _vp]
+    L.ipiano_slabs_connect_peers.argtypes = [_vp, _vp, _vp]
+    L.ipiano_slabs_disconnect_peers.argtypes = [_vp]
     L.ipiano_slabs_destroy.argtypes = [_vp]
     L.ipiano_slabs_destroy.restype = None
     _configured = L
@@ -567,3 +571,22 @@ def ipiano_slabs_member(slabs: Slabs, j: int = 0) -> State:
 
 def ipiano_slabs_destroy(slabs: Slabs):
     slabs.destroy()
+
+
+def ipiano_slabs_halo_handle(slabs: Slabs) -> bytes:
+    """This rank's ghost-row buffer as a CUDA IPC handle (64 bytes) for its ring neighbours."""
+    buf = C.create_string_buffer(64)
+    _check(lib().ipiano_slabs_halo_handle(slabs.handle, C.cast(buf, _vp)))
+    return buf.raw
+
+
+def ipiano_slabs_connect_peers(slabs: Slabs, up_handle: bytes, down_handle: bytes):
+    """Switch the ghost-row exchange to direct NVLink stores from K2 (see include/foe.h)."""
+    ub = C.create_string_buffer(bytes(up_handle), 64)
+    db = C.create_string_buffer(bytes(down_handle), 64)
+    _check(lib().ipiano_slabs_connect_peers(slabs.handle, C.cast(ub, _vp), C.cast(db, _vp)))
+
+
+def ipiano_slabs_disconnect_peers(slabs: Slabs):
+    """Back to the ncclSend/Recv exchange (all ranks must take the same path)."""
+    _check(lib().ipiano_slabs_disconnect_peers(slabs.handle))

@@ -65,6 +65,7 @@ def _worker(rank, ws, port, q):
         out["max"] = D.max_over_ranks(float(rank + 1))
         out["sum"] = D.sum_over_ranks(float(rank + 1))
         out["id"] = D.share_bytes(bytes(range(128)) if rank == 0 else None)
+        out["all_true"] = (D.all_true(True), D.all_true(rank == 0))
         # slab ring on a 256 x 40 scene
         H, W = 256, 40
         scene = np.arange(H * W, dtype=np.float64).reshape(H, W)
@@ -121,6 +122,7 @@ def test_reductions_and_id_broadcast(two_ranks):
         assert two_ranks[rank]["max"] == 2.0
         assert two_ranks[rank]["sum"] == 3.0
         assert two_ranks[rank]["id"] == bytes(range(128))
+        assert two_ranks[rank]["all_true"] == (True, False)
 
 
 def test_slab_ring_ghost_rows_two_ranks(two_ranks):

@@ -141,13 +141,18 @@ def test_single_step_parity_P1():
     assert rel_l2(g1.cpu().numpy()[0], go1) <= 1e-5
 
 
-def test_teacher_forced_trajectory_P2():
+@pytest.mark.parametrize("policy", ["recommended", "spec"])
+@pytest.mark.parametrize("stencil", [P.FOE_STENCIL_FFMA, P.FOE_STENCIL_TENSOR])
+def test_teacher_forced_trajectory_P2(policy, stencil):
     # P2: every GPU step is re-done by the oracle from the GPU's own state (w, w_prev, L):
-    # per-step update parity <= 1e-5 and identical decisions unless |margin| is a near-tie
+    # per-step update parity <= 1e-5 and identical decisions unless |margin| is a near-tie.
+    # Under the SPEC policy (beta = 0.8, L halves after each accept; SURVEY
+    # 8(f) f3) this is the certificate: the long run is chaotic under rounding (R-9).
     cfg, d, L0 = _setup("c2", H=128, W=96, iters=12)
     md = _model(d["filters"], d["theta"], lam=tuple(d["lambdas"][0]))
+    pol = dict(beta=0.8, shrink=0.5) if policy == "spec" else {}
     st = P.ipiano_state_create(md, _cuda(d["f"], torch.float32), d["lambdas"], L0,
-                               P.ipiano_config_default(max_iters=12))
+                               P.ipiano_config_default(max_iters=12, stencil=stencil, **pol))
     f = d["f"][0]
     l1, l2 = d["lambdas"][0]
     w_prev = np.log(oracle.ftilde(f))
@@ -164,7 +169,7 @@ def test_teacher_forced_trajectory_P2():
         while True:
             trials += 1
             r = oracle.ipiano_trial(w_cur, w_prev, g, F, L, f, d["filters"], d["theta"], l1, l2,
-                                    oracle.make_cfg(L, 1))
+                                    oracle.make_cfg(L, 1, **pol))
             if r["accepted"]:
                 break
             L *= 2

@@ -88,6 +88,34 @@ def test_slab_nccl_self_ring_matches_in_process(small_case):
     np.testing.assert_array_equal(tr_n, tr_l)
 
 
+def test_slab_nccl_fused_p2p_self_ring(small_case):
+    """The fused exchange (K2 stores its boundary rows straight into the ring neighbours' ghost
+    buffers; here the 1-rank ring's neighbour is the slab itself) gives the same bits as the
+    ncclSend/ncclRecv path and the in-process path."""
+    c = small_case
+    comm = P.foe_comm_create(P.foe_comm_unique_id(), 1, 0, 0)
+    try:
+        ft = torch.as_tensor(c["f"], device="cuda")
+        sl = P.ipiano_slabs_create(c["md"], ft, c["H"], lam=(160.0, 0.004), lipschitz_init=c["L0"],
+                                   cfg=P.ipiano_config_default(max_iters=12), comm=comm)
+        h = P.ipiano_slabs_halo_handle(sl)
+        assert len(h) == 64
+        P.ipiano_slabs_connect_peers(sl, h, h)
+        with pytest.raises(P.FoeError):
+            P.ipiano_slabs_connect_peers(sl, h, h)           # only once
+        P.ipiano_slabs_reset(sl, ft, c["L0"])                # re-init on the fused path
+        P.ipiano_slabs_solve(sl)
+        w_p, _ = P.ipiano_slabs_get_iterate(sl, want_u=False)
+        tr_p = P.ipiano_get_trace(P.ipiano_slabs_member(sl, 0))[0]
+        w_p = w_p.cpu().numpy()
+        sl.destroy()
+    finally:
+        comm.destroy()
+    w_l, _, tr_l, _ = _run_slabs(c["md"], c["f"], 1, c["L0"], 12)
+    np.testing.assert_array_equal(w_p, w_l)
+    np.testing.assert_array_equal(tr_p, tr_l)
+
+
 def test_slab_parity_vs_oracle(small_case):
     """P3 on the slab path (2 slabs): free-running final image against the whole-scene oracle."""
     c = small_case
