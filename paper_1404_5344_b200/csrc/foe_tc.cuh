@@ -100,11 +100,15 @@ __device__ __forceinline__ void tc_im2col(const float* up, float vc, uint32_t t_
     for (int c8 = C0; c8 < C1; ++c8) {
         float h[8], lo[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const int tap = c8 * 8 + e;
-            const float v = tap < M * M ? up[(tap / M) * UP + (tap % M)] - vc : 0.f;
-            h[e] = tc::tf32_hi(v);
-            lo[e] = tc::tf32_hi(v - h[e]);
+        for (int e = 0; e < 8; e += 2) {
+            const int t0 = c8 * 8 + e, t1 = t0 + 1;
+            const float2 u2 = make_float2(t0 < M * M ? up[(t0 / M) * UP + (t0 % M)] : vc,
+                                          t1 < M * M ? up[(t1 / M) * UP + (t1 % M)] : vc);
+            const float2 v = __fadd2_rn(u2, make_float2(-vc, -vc));     // taps past m*m -> 0
+            float2 hi2, lo2;
+            tc::tf32_split2(v, hi2, lo2);
+            h[e] = hi2.x; h[e + 1] = hi2.y;
+            lo[e] = lo2.x; lo[e + 1] = lo2.y;
         }
         tc::tmem_st8(t_hi + c8 * 8, h);
         tc::tmem_st8(t_lo + c8 * 8, lo);
@@ -115,7 +119,6 @@ __device__ __forceinline__ void tc_im2col(const float* up, float vc, uint32_t t_
 template <int F0, int F1>
 __device__ __forceinline__ float tc_epilogue(uint32_t t_d, uint32_t t_phi, uint32_t t_plo, float uq,
                                              const float* css, const float* ths, const float* kbl, float& zlast) {
-    float el = 0.f, zl = 0.f;
     float r[(F1 - F0) * 8];
 #pragma unroll
     for (int f8 = F0; f8 < F1; ++f8) {
@@ -123,25 +126,31 @@ __device__ __forceinline__ float tc_epilogue(uint32_t t_d, uint32_t t_phi, uint3
         tc::tmem_ld8(t_d + f8 * 8, *reinterpret_cast<float(*)[8]>(rr));
     }
     tc::wait_ld();
+    // filters in pairs on the FP32x2 pipes (FFMA2 / FMUL2 / FADD2); MUFU stays scalar
+    const float2 uq2 = make_float2(uq, uq), one2 = make_float2(1.f, 1.f);
+    float2 el2 = make_float2(0.f, 0.f), zl2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int f8 = F0; f8 < F1; ++f8) {
         float ph[8], pl[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
+        for (int e = 0; e < 8; e += 2) {
             const int i = f8 * 8 + e;
-            const float rv = fmaf(uq, css[i], r[(f8 - F0) * 8 + e]);
-            const float d = fmaf(rv, rv, 1.f);
-            el = fmaf(ths[i], lg2_approx(d), el);
-            const float pv = rv * rcp_approx(d);
-            zl = fmaf(pv, kbl[i], zl);
-            ph[e] = tc::tf32_hi(pv);
-            pl[e] = tc::tf32_hi(pv - ph[e]);
+            const float2 r2 = make_float2(r[(f8 - F0) * 8 + e], r[(f8 - F0) * 8 + e + 1]);
+            const float2 rv = __ffma2_rn(uq2, make_float2(css[i], css[i + 1]), r2);
+            const float2 d = __ffma2_rn(rv, rv, one2);
+            el2 = __ffma2_rn(make_float2(ths[i], ths[i + 1]), make_float2(lg2_approx(d.x), lg2_approx(d.y)), el2);
+            const float2 pv = __fmul2_rn(rv, make_float2(rcp_approx(d.x), rcp_approx(d.y)));
+            zl2 = __ffma2_rn(pv, make_float2(kbl[i], kbl[i + 1]), zl2);
+            float2 hi2, lo2;
+            tc::tf32_split2(pv, hi2, lo2);
+            ph[e] = hi2.x; ph[e + 1] = hi2.y;
+            pl[e] = lo2.x; pl[e + 1] = lo2.y;
         }
         tc::tmem_st8(t_phi + f8 * 8, ph);
         tc::tmem_st8(t_plo + f8 * 8, pl);
     }
-    zlast = zl;
-    return el;
+    zlast = zl2.x + zl2.y;
+    return el2.x + el2.y;
 }
 // Z chunks [C0, C1) of 8 taps -> zs[tap][lane]
 template <int L, int C0, int C1>

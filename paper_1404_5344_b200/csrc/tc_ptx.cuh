@@ -176,6 +176,27 @@ __device__ __forceinline__ float tf32_hi(float x) {
     return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
+// Paired 3xTF32 split of two values (Veltkamp-Dekker with s = 2^13 + 1 on FP32x2 pipes, no
+// contraction): hi = x rounded to 11 significant bits (tf32), lo = x - hi rounded likewise.
+// 7 paired ops per 2 values instead of 5 integer/fp ops per value.
+// the rounded paired product x*s as an FFMA2 with a zero addend: ptxas fuses a separate
+// multiply into the following subtraction (FMUL2 + FADD2 -> FFMA2, even for the .rn forms),
+// which would break Veltkamp's split; an FMA result is not re-fused
+__device__ __forceinline__ float2 fmul2_nocontract(float2 a, float2 b) {
+    return __ffma2_rn(a, b, make_float2(0.0f, 0.0f));
+}
+
+__device__ __forceinline__ void tf32_split2(float2 x, float2& hi, float2& lo) {
+    const float2 s = make_float2(8193.0f, 8193.0f);
+    const float2 c = fmul2_nocontract(x, s);
+    const float2 t = __fadd2_rn(c, make_float2(-x.x, -x.y));
+    hi = __fadd2_rn(c, make_float2(-t.x, -t.y));
+    const float2 r = __fadd2_rn(x, make_float2(-hi.x, -hi.y));        // exact
+    const float2 c2 = fmul2_nocontract(r, s);
+    const float2 t2 = __fadd2_rn(c2, make_float2(-r.x, -r.y));
+    lo = __fadd2_rn(c2, make_float2(-t2.x, -t2.y));
+}
+
 // fp32 -> tf32 (round to nearest, ties away), kept in a 32-bit container
 __device__ __forceinline__ float to_tf32(float x) {
     uint32_t r;
