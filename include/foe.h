@@ -313,6 +313,25 @@ foe_status ipiano_slabs_disconnect_peers(ipiano_slabs* slabs);
 foe_status ipiano_slabs_member(const ipiano_slabs* slabs, int j, ipiano_state** out);
 void ipiano_slabs_destroy(ipiano_slabs* slabs);
 
+/* ------------------------------------------------- evaluation and synthesis */
+
+/* Pointers are device fp32 [B][H][W] arrays on the CURRENT CUDA device; results are host [B].
+ * All three synchronise `stream`.
+ *   foe_psnr: 10 log10(peak^2 / MSE) per image, +inf when x == ref.
+ *   foe_ssim: mean local SSIM over the valid region with an 11x11 Gaussian window (sigma 1.5),
+ *             K1 = 0.01, K2 = 0.03, C = (K peak)^2 (Wang et al., cited by the
+ *             paper's Sec. III); H, W >= 11.
+ *   foe_add_speckle: f = u sqrt(s), s ~ Gamma(looks[b], scale 1/looks[b]) (the amplitude model,
+ *             DESIGN.md R-14), looks[b] >= 1; Marsaglia-Tsang driven by Philox4x32-10 with
+ *             counter (p lo, p hi, attempt, 0) for the global pixel index p = b H W + y W + x
+ *             and key (seed lo, seed hi): the result depends only on (u, looks, seed). */
+foe_status foe_psnr(const float* x, const float* ref, int B, int H, int W, double peak, double* psnr_out,
+                    void* stream);
+foe_status foe_ssim(const float* x, const float* ref, int B, int H, int W, double peak, double* ssim_out,
+                    void* stream);
+foe_status foe_add_speckle(const float* u, int B, int H, int W, const double* looks, unsigned long long seed,
+                           float* f_out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -18,6 +18,7 @@
 #include "foe.h"
 #include "foe_kernels.cuh"
 #include "foe_tc.cuh"
+#include "foe_eval.cuh"
 
 using foe::ImgCtl;
 using foe::K1Args;
@@ -1884,6 +1885,126 @@ foe_status ipiano_slabs_member(const ipiano_slabs* g, int j, ipiano_state** out)
     if (j < 0 || j >= (int)g->members.size())
         return fail(FOE_ERR_INVALID_ARGUMENT, "member %d outside [0,%d)", j, (int)g->members.size());
     *out = g->members[j];
+    return FOE_OK;
+}
+
+}  // extern "C"
+
+// ========================================================= evaluation / synthesis
+
+namespace {
+
+foe_status check_eval(const void* a, const void* b, int B, int H, int W) {
+    if (!a || !b) return fail(FOE_ERR_INVALID_ARGUMENT, "image pointers must be non-NULL");
+    if (B < 1 || H < 1 || W < 1) return fail(FOE_ERR_INVALID_ARGUMENT, "B=%d H=%d W=%d must be >= 1", B, H, W);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(FOE_ERR_CUDA, "libfoe is built for sm_100a (B200); the current device is sm_%d%d", prop.major, prop.minor);
+    return FOE_OK;
+}
+
+// per-image sums of per-block partials [B][nblk] -> host [B]
+foe_status sum_parts(const double* part, int B, int nblk, double* host, cudaStream_t s) {
+    double* dsum = nullptr;
+    CK(cudaMallocAsync((void**)&dsum, sizeof(double) * B, s));
+    foe::k_reduce_rows<<<B, kThreads, 0, s>>>(part, nblk, 1, 1, dsum);
+    count_launch(1);
+    CKL("k_reduce_rows");
+    CK(cudaMemcpyAsync(host, dsum, sizeof(double) * B, cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(dsum, s));
+    CK(cudaStreamSynchronize(s));
+    return FOE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+foe_status foe_psnr(const float* x, const float* ref, int B, int H, int W, double peak, double* psnr_out,
+                    void* stream) {
+    foe_status r = check_eval(x, ref, B, H, W);
+    if (r != FOE_OK) return r;
+    if (!psnr_out || !(peak > 0)) return fail(FOE_ERR_INVALID_ARGUMENT, "psnr_out must be non-NULL and peak > 0");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t HW = (size_t)H * W;
+    const int nblk = std::max(1, std::min(div_up((long long)HW, kThreads * 8), 256));
+    double* part = nullptr;
+    CK(cudaMallocAsync((void**)&part, sizeof(double) * B * nblk, s));
+    foe::k_sq_err_part<<<dim3(nblk, B), kThreads, 0, s>>>(x, ref, HW, nblk, part);
+    count_launch(1);
+    CKL("k_sq_err_part");
+    std::vector<double> sse(B);
+    r = sum_parts(part, B, nblk, sse.data(), s);
+    cudaFreeAsync(part, s);
+    if (r != FOE_OK) return r;
+    for (int b = 0; b < B; ++b) {
+        const double mse = sse[b] / (double)HW;   // 10 log10(peak^2 / MSE), +inf at MSE = 0
+        psnr_out[b] = mse == 0.0 ? INFINITY : 10.0 * std::log10(peak * peak / mse);
+    }
+    return FOE_OK;
+}
+
+foe_status foe_ssim(const float* x, const float* ref, int B, int H, int W, double peak, double* ssim_out,
+                    void* stream) {
+    foe_status r = check_eval(x, ref, B, H, W);
+    if (r != FOE_OK) return r;
+    if (!ssim_out || !(peak > 0)) return fail(FOE_ERR_INVALID_ARGUMENT, "ssim_out must be non-NULL and peak > 0");
+    if (H < 11 || W < 11) return fail(FOE_ERR_INVALID_ARGUMENT, "image %dx%d smaller than the 11x11 SSIM window", H, W);
+    cudaStream_t s = (cudaStream_t)stream;
+    foe::SsimParams sp;
+    double g[11], gs = 0.0;
+    for (int i = 0; i < 11; ++i) { const double r_ = i - 5.0; g[i] = std::exp(-r_ * r_ / (2.0 * 1.5 * 1.5)); gs += g[i]; }
+    for (int i = 0; i < 11; ++i) sp.w[i] = g[i] / gs;
+    sp.c1 = (0.01 * peak) * (0.01 * peak);
+    sp.c2 = (0.03 * peak) * (0.03 * peak);
+    const size_t on = (size_t)(H - 10) * (W - 10);
+    const int nblk = std::max(1, std::min(div_up((long long)on, kThreads), 512));
+    double* part = nullptr;
+    CK(cudaMallocAsync((void**)&part, sizeof(double) * B * nblk, s));
+    foe::k_ssim_part<<<dim3(nblk, B), kThreads, 0, s>>>(x, ref, H, W, nblk, sp, part);
+    count_launch(1);
+    CKL("k_ssim_part");
+    std::vector<double> sum(B);
+    r = sum_parts(part, B, nblk, sum.data(), s);
+    cudaFreeAsync(part, s);
+    if (r != FOE_OK) return r;
+    for (int b = 0; b < B; ++b) ssim_out[b] = sum[b] / (double)on;
+    return FOE_OK;
+}
+
+foe_status foe_add_speckle(const float* u, int B, int H, int W, const double* looks, unsigned long long seed,
+                           float* f_out, void* stream) {
+    foe_status r = check_eval(u, f_out, B, H, W);
+    if (r != FOE_OK) return r;
+    if (!looks) return fail(FOE_ERR_INVALID_ARGUMENT, "looks is NULL");
+    for (int b = 0; b < B; ++b)
+        if (!(looks[b] >= 1.0) || !std::isfinite(looks[b]))
+            return fail(FOE_ERR_INVALID_ARGUMENT, "looks[%d]=%g: this generator needs L >= 1", b, looks[b]);
+    cudaStream_t s = (cudaStream_t)stream;
+    double* dl = nullptr;
+    unsigned int* capped = nullptr;
+    CK(cudaMallocAsync((void**)&dl, sizeof(double) * B, s));
+    CK(cudaMallocAsync((void**)&capped, sizeof(unsigned int), s));
+    CK(cudaMemcpyAsync(dl, looks, sizeof(double) * B, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(capped, 0, sizeof(unsigned int), s));
+    const size_t n = (size_t)B * H * W;
+    int nsm = 148;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int grid = std::max(1, std::min(div_up((long long)n, 256), 8 * nsm));
+    foe::k_add_speckle<<<grid, 256, 0, s>>>(u, dl, B, (size_t)H * W, seed, f_out, capped);
+    count_launch(1);
+    CKL("k_add_speckle");
+    unsigned int hc = 0;
+    CK(cudaMemcpyAsync(&hc, capped, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    CK(cudaFreeAsync(dl, s));
+    CK(cudaFreeAsync(capped, s));
+    CK(cudaStreamSynchronize(s));
+    if (hc) return fail(FOE_ERR_NONFINITE, "%u pixels exceeded 64 Marsaglia-Tsang attempts", hc);
     return FOE_OK;
 }
 

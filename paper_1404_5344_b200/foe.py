@@ -33,6 +33,7 @@ EXPORTED = (
     "foe_model_set_stencil", "foe_comm_unique_id", "foe_comm_create", "foe_comm_destroy", "ipiano_slabs_create", "ipiano_slabs_reset",
     "ipiano_slabs_solve", "ipiano_slabs_get_iterate", "ipiano_slabs_member", "ipiano_slabs_destroy",
     "ipiano_slabs_halo_handle", "ipiano_slabs_connect_peers", "ipiano_slabs_disconnect_peers",
+    "foe_psnr", "foe_ssim", "foe_add_speckle",
 )
 
 
@@ -111,6 +112,9 @@ def lib():
     L.ipiano_slabs_halo_handle.argtypes = [_vp, _vp]
     L.ipiano_slabs_connect_peers.argtypes = [_vp, _vp, _vp]
     L.ipiano_slabs_disconnect_peers.argtypes = [_vp]
+    L.foe_psnr.argtypes = [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_double, _dp, _vp]
+    L.foe_ssim.argtypes = [_vp, _vp, C.c_int, C.c_int, C.c_int, C.c_double, _dp, _vp]
+    L.foe_add_speckle.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _dp, C.c_ulonglong, _vp, _vp]
     L.ipiano_slabs_destroy.argtypes = [_vp]
     L.ipiano_slabs_destroy.restype = None
     _configured = L
@@ -590,3 +594,36 @@ def ipiano_slabs_connect_peers(slabs: Slabs, up_handle: bytes, down_handle: byte
 def ipiano_slabs_disconnect_peers(slabs: Slabs):
     """Back to the ncclSend/Recv exchange (all ranks must take the same path)."""
     _check(lib().ipiano_slabs_disconnect_peers(slabs.handle))
+
+
+# ------------------------------------------------- evaluation and synthesis (SURVEY 8(f) f4)
+
+def foe_psnr(x, ref, peak: float = 255.0, stream=None) -> np.ndarray:
+    """PSNR per image of device fp32 [B][H][W] tensors (host fp64 [B])."""
+    torch = _torch()
+    B, H, W = _bhw(x)
+    out = np.zeros(B)
+    _check(lib().foe_psnr(_dev_ptr(x, torch.float32, "x"), _dev_ptr(ref, torch.float32, "ref", x.shape), B, H, W,
+                          float(peak), out.ctypes.data_as(_dp), _stream(stream)))
+    return out
+
+
+def foe_ssim(x, ref, peak: float = 255.0, stream=None) -> np.ndarray:
+    """Mean SSIM per image (11x11 Gaussian window, valid region)."""
+    torch = _torch()
+    B, H, W = _bhw(x)
+    out = np.zeros(B)
+    _check(lib().foe_ssim(_dev_ptr(x, torch.float32, "x"), _dev_ptr(ref, torch.float32, "ref", x.shape), B, H, W,
+                          float(peak), out.ctypes.data_as(_dp), _stream(stream)))
+    return out
+
+
+def foe_add_speckle(u, looks, seed: int, stream=None):
+    """f = u sqrt(s), s ~ Gamma(L, 1/L) per image, Philox4x32-10 counter-based (device fp32)."""
+    torch = _torch()
+    B, H, W = _bhw(u)
+    lk, lp = _host_d(np.broadcast_to(np.asarray(looks, np.float64), (B,)), B, "looks")
+    f = torch.empty_like(u)
+    _check(lib().foe_add_speckle(_dev_ptr(u, torch.float32, "u"), B, H, W, lp, C.c_ulonglong(int(seed)),
+                                 C.c_void_p(f.data_ptr()), _stream(stream)))
+    return f

@@ -345,3 +345,61 @@ def test_ipiano_run_workspace_reuse_is_exact():
         np.testing.assert_array_equal(tr_h, tr_f)
         outs.append(u_h)
     assert not np.array_equal(outs[0], outs[1])
+
+
+@pytest.fixture(scope="module")
+def c3_oracle_run():
+    """The fp64 oracle's full c3 trajectory (512^2, L=8, 48 x 7x7, 300 iterations; ~1 min on
+    16 host cores), shared by the P3 tests of both stencils."""
+    cfg, d, L0 = _setup("c3")
+    l1, l2 = d["lambdas"][0]
+    ref = oracle.ipiano_run(d["f"][0], d["filters"], d["theta"], l1, l2, oracle.make_cfg(L0[0], cfg.iters))
+    assert ref["status"] == 0
+    return cfg, d, L0, ref
+
+
+@pytest.mark.parametrize("stencil", [P.FOE_STENCIL_FFMA, P.FOE_STENCIL_TENSOR])
+def test_free_running_c3_P3(c3_oracle_run, stencil):
+    """P3 on the full BASELINE config 3 (512^2 x 300 iterations) on both prior stencils."""
+    cfg, d, L0, ref = c3_oracle_run
+    md = _model(d["filters"], d["theta"], lam=tuple(d["lambdas"][0]))
+    c = P.ipiano_config_default(max_iters=cfg.iters, stencil=stencil)
+    st = P.ipiano_state_create(md, _cuda(d["f"], torch.float32), d["lambdas"], L0, c)
+    P.ipiano_solve(st)
+    _, u = P.ipiano_get_iterate(st)
+    u = u.cpu().numpy()[0]
+    tr = P.ipiano_get_trace(st)[0]
+    assert rel_l2(u, ref["u"]) <= 1e-4
+    clean = d["clean"][0]
+    assert abs(oracle.psnr(u, clean) - oracle.psnr(ref["u"], clean)) <= 0.01
+    np.testing.assert_array_equal(tr[1:, 3], ref["trace"][1:, 3])
+    np.testing.assert_array_equal(tr[1:, 4], ref["trace"][1:, 4])
+    np.testing.assert_allclose(tr[:, 2], ref["trace"][:, 2], rtol=1e-6)
+
+
+def test_c4_bench_launch_config_full_trajectory_P3():
+    """c4 in the launch configuration bench.py times (64 x 512^2, AUTO stencil -> K8, 300
+    iterations, per-image L_init from the GPU estimate): images 5 and 42 free-running against
+    the oracle run on each alone (final image rel L2 <= 1e-4, |dPSNR| <= 0.01 dB, identical
+    decisions)."""
+    cfg = S.config("c4")
+    d = S.make_inputs(cfg)
+    v0 = S.lipschitz_start_vector(cfg.B, cfg.H, cfg.W)
+    md = _model(d["filters"], d["theta"], lam=tuple(d["lambdas"][0]))
+    _, L0 = P.foe_estimate_lipschitz(md, _cuda(d["f"], torch.float32), _cuda(v0, torch.float64), 25)
+    c = P.ipiano_config_default(max_iters=cfg.iters)
+    st = P.ipiano_state_create(md, _cuda(d["f"], torch.float32), d["lambdas"], L0, c)
+    assert P.ipiano_state_stencil(st) == P.FOE_STENCIL_TENSOR
+    P.ipiano_solve(st)
+    _, u = P.ipiano_get_iterate(st)
+    u = u.cpu().numpy()
+    tr = P.ipiano_get_trace(st)
+    for b in (5, 42):
+        l1, l2 = d["lambdas"][b]
+        ref = oracle.ipiano_run(d["f"][b], d["filters"], d["theta"], l1, l2, oracle.make_cfg(L0[b], cfg.iters))
+        assert ref["status"] == 0
+        assert rel_l2(u[b], ref["u"]) <= 1e-4, b
+        clean = d["clean"][b]
+        assert abs(oracle.psnr(u[b], clean) - oracle.psnr(ref["u"], clean)) <= 0.01
+        np.testing.assert_array_equal(tr[b, 1:, 3], ref["trace"][1:, 3])
+        np.testing.assert_array_equal(tr[b, 1:, 4], ref["trace"][1:, 4])
