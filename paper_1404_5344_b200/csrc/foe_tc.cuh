@@ -192,7 +192,9 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
     const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
     const int y0 = ty * R, x0 = tx * G::OW;
     const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
-    const int t = threadIdx.x, warp = t >> 5;
+    // warp index broadcast from lane 0: provably warp-uniform, so TMEM addresses and the warp
+    // group branch stay in uniform registers (no per-op R2UR / collective fix-up code)
+    const int t = threadIdx.x, warp = __shfl_sync(0xffffffffu, t >> 5, 0);
     const int wg = warp >> 2;                                   // warp group (0, 1)
     const int l = (warp & 3) * 32 + (t & 31);                   // TMEM lane = response pixel
 
@@ -491,7 +493,7 @@ __global__ void __launch_bounds__(21 * 32, 1) k_prior_grad_tc4(const TcArgs ta, 
     const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
     const int y0 = ty * R, x0 = tx * G::OW;
     const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
-    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int t = threadIdx.x, warp = __shfl_sync(0xffffffffu, t >> 5, 0), lane = t & 31;   // warp-uniform
     const int l = (warp & 3) * 32 + lane;                       // TMEM lane = response pixel
     const bool udom = args.udom != 0;
 
