@@ -127,13 +127,13 @@ cudaError_t tc_set_attr() {
     return cudaFuncSetAttribute(foe::k_prior_grad_tc4<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 tc4_smem<M, NP>());
 }
-// K8 variant: 3 = two lock-step CTAs per SM (default; 1.90 ms vs 1.96 ms per c4 launch under
-// ncu), 4 = warp-specialised single-CTA pipeline (FOE_K8_VARIANT=4, experimental)
+// K8 variant: 4 = warp-specialised single-CTA pipeline (default; 1.54 ms per c4 launch under
+// ncu), 3 = two lock-step CTAs per SM (1.58 ms; FOE_K8_VARIANT=3)
 int tc_variant() {
     const char* e = std::getenv("FOE_K8_VARIANT");   // read per launch (A/B in one process)
-    if (e && e[0] == '4') return 4;
+    if (e && e[0] == '3') return 3;
     if (e && e[0] == 'k' && e[1] >= '1' && e[1] <= '4') return 40 + (e[1] - '0');   // profiling knockouts
-    return 3;
+    return 4;
 }
 // the banks K8 has an instantiation for: (m, padded N_f)
 int tc_np(int m, int nf) {

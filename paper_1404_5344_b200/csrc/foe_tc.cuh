@@ -92,6 +92,34 @@ struct TcArgs {
     int tiles_x;              // column tiles of OW
 };
 
+// u tile staging (a2): UY rows x UX columns of u - c from the fp64 iterate, one warp per row at a
+// time with all of a lane's loads of the row in flight; columns wrap periodically (their indices
+// are the same for every row), rows wrap or come from the slab's ghost rows
+template <int UY, int UX, int UP, int NWARPS>
+__device__ __forceinline__ void tc_stage_u(float* us, const double* w, const double* halo, int H, int W, int y0,
+                                           int x0, int c2, bool udom, float cst, double wc, int warp, int lane) {
+    constexpr int NX = (UX + 31) / 32;
+    int gx[NX];
+#pragma unroll
+    for (int k = 0; k < NX; ++k) gx[k] = wrap_idx(x0 - c2 + lane + 32 * k, W);
+    for (int uy = warp; uy < UY; uy += NWARPS) {
+        const int y = y0 - c2 + uy;
+        const double* src;
+        if (halo == nullptr) src = w + (size_t)wrap_idx(y, H) * W;
+        else if (y < 0) src = halo + (size_t)(kHalo + y) * W;
+        else if (y >= H) src = halo + (size_t)(kHalo + y - H) * W;
+        else src = w + (size_t)y * W;
+        double v[NX];
+#pragma unroll
+        for (int k = 0; k < NX; ++k) v[k] = (lane + 32 * k < UX) ? src[gx[k]] : wc;
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            const int ux = lane + 32 * k;
+            if (ux < UX) us[uy * UP + ux] = udom ? (float)(v[k] - (double)cst) : cst * expm1f((float)(v[k] - wc));
+        }
+    }
+}
+
 // ---- per-row thread work of K8, on compile-time chunk ranges (one call per warp group) ------
 // im2col chunks [C0, C1) of 8 taps: U = u(window) - u_q split into tf32 hi / lo, to TMEM
 template <int M, int UP, int C0, int C1>
@@ -208,6 +236,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
     {
         const float4* src = reinterpret_cast<const float4*>(ta.bimg);
         float4* dst = reinterpret_cast<float4*>(bsm);
+#pragma unroll 4
         for (int i = t; i < G::B_FLOATS / 4; i += 256) dst[i] = __ldg(src + i);
     }
     const int yc = min(y0 + R / 2, H - 1), xc = min(x0 + G::OW / 2, W - 1);
@@ -222,16 +251,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
         ths[t] = __ldg(ta.theta_ln2 + t);
     }
     const double* halo = args.halo;
-    for (int idx = t; idx < G::UY * G::UX; idx += 256) {
-        const int uy = idx / G::UX, ux = idx - uy * G::UX;
-        const int y = y0 - 2 * C + uy, gx = wrap_idx(x0 - 2 * C + ux, W);
-        const double* src;
-        if (halo == nullptr) src = w + (size_t)wrap_idx(y, H) * W;
-        else if (y < 0) src = halo + (size_t)(kHalo + y) * W;
-        else if (y >= H) src = halo + (size_t)(kHalo + y - H) * W;
-        else src = w + (size_t)y * W;
-        us[uy * G::UP + ux] = udom ? (float)(src[gx] - (double)cst) : cst * expm1f((float)(src[gx] - wc));
-    }
+    tc_stage_u<G::UY, G::UX, G::UP, 8>(us, w, halo, H, W, y0, x0, 2 * C, udom, cst, wc, warp, t & 31);
     tc::fence_proxy_async_smem();
     tc::fence_before_sync();
     __syncthreads();
@@ -526,16 +546,7 @@ __global__ void __launch_bounds__(21 * 32, 1) k_prior_grad_tc4(const TcArgs ta, 
         ths[t] = __ldg(ta.theta_ln2 + t);
     }
     const double* halo = args.halo;
-    for (int idx = t; idx < G::UY * G::UX; idx += G4::THREADS) {
-        const int uy = idx / G::UX, ux = idx - uy * G::UX;
-        const int y = y0 - 2 * C + uy, gx = wrap_idx(x0 - 2 * C + ux, W);
-        const double* src;
-        if (halo == nullptr) src = w + (size_t)wrap_idx(y, H) * W;
-        else if (y < 0) src = halo + (size_t)(kHalo + y) * W;
-        else if (y >= H) src = halo + (size_t)(kHalo + y - H) * W;
-        else src = w + (size_t)y * W;
-        us[uy * G::UP + ux] = udom ? (float)(src[gx] - (double)cst) : cst * expm1f((float)(src[gx] - wc));
-    }
+    tc_stage_u<G::UY, G::UX, G::UP, G4::THREADS / 32>(us, w, halo, H, W, y0, x0, 2 * C, udom, cst, wc, warp, lane);
     tc::fence_proxy_async_smem();
     tc::fence_before_sync();
     __syncthreads();
