@@ -124,14 +124,18 @@ cudaError_t tc_set_attr() {
     cudaError_t e = cudaFuncSetAttribute(foe::k_prior_grad_tc<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          tc_smem<M, NP>());
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(foe::k_prior_grad_tc4<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                tc4_smem<M, NP>());
+    e = cudaFuncSetAttribute(foe::k_prior_grad_tc4<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tc4_smem<M, NP>());
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(foe::k_prior_grad_tc5<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                foe::Tc5Geom<M, NP, kTcR>::SMEM_BYTES);
 }
 // K8 variant: 4 = warp-specialised single-CTA pipeline (default; 1.54 ms per c4 launch under
 // ncu), 3 = two lock-step CTAs per SM (1.58 ms; FOE_K8_VARIANT=3)
 int tc_variant() {
     const char* e = std::getenv("FOE_K8_VARIANT");   // read per launch (A/B in one process)
     if (e && e[0] == '3') return 3;
+    if (e && e[0] == '5') return 5;
     if (e && e[0] == 'k' && e[1] >= '1' && e[1] <= '4') return 40 + (e[1] - '0');   // profiling knockouts
     return 4;
 }
@@ -492,6 +496,15 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
         if (var == 42) foe::k_prior_grad_tc4<7, 48, kTcR, 2><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
         if (var == 43) foe::k_prior_grad_tc4<7, 48, kTcR, 3><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
         if (var == 44) foe::k_prior_grad_tc4<7, 48, kTcR, 4><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
+    } else if (var == 5) {
+        ta.nimg = B;
+        const int items = a.ntiles * B;
+        const int grid = std::max(1, std::min(items, md->nsm));
+        constexpr int T5 = foe::Tc5Geom<7, 48, kTcR>::THREADS;
+        if (md->tc_np == 48)
+            foe::k_prior_grad_tc5<7, 48, kTcR><<<dim3(grid, 1), T5, foe::Tc5Geom<7, 48, kTcR>::SMEM_BYTES, s>>>(ta, *md->tc_const);
+        else
+            foe::k_prior_grad_tc5<5, 32, kTcR><<<dim3(grid, 1), T5, foe::Tc5Geom<5, 32, kTcR>::SMEM_BYTES, s>>>(ta, *md->tc_const);
     } else if (var >= 4) {
         if (md->tc_np == 48)
             foe::k_prior_grad_tc4<7, 48, kTcR><<<dim3(a.ntiles, B), T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);

@@ -90,6 +90,7 @@ struct TcArgs {
     const float* sumk;        // [NP] sum_t k_i (fp64-summed, fp32) for the DC restore (0 past N_f)
     const float* theta_ln2;   // [NP] theta_i ln 2 (0 past N_f)
     int tiles_x;              // column tiles of OW
+    int nimg;                 // images in the batch (persistent variant: grid = min(items, SMs))
 };
 
 // u tile staging (a2): UY rows x UX columns of u - c from the fp64 iterate, one warp per row at a
@@ -720,6 +721,335 @@ __global__ void __launch_bounds__(21 * 32, 1) k_prior_grad_tc4(const TcArgs ta, 
     __syncwarp();
     const double e = block_sum_d(e_acc, red);
     if (t == 0) args.epart[(size_t)b * args.ntiles * args.groups + blockIdx.x] = e;
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tb);
+}
+
+}  // namespace foe
+
+namespace foe {
+
+// =============================================================================================
+// K8 v5: the v4 pipeline made persistent -- one CTA per SM loops over (tile, image) work items
+// (static stride), so the B images are loaded once per CTA, the pipeline runs on across item
+// boundaries (no fill/drain per tile), and a loader warp group stages the next item's u tile
+// into a second buffer while the current one is processed:
+//
+//   IM  warps 0-7, EP 8-15, ZC 16-19, MMA 20 (as v4); LD warps 21-24: u tile of item k into
+//   U[k%2] (waits U_empty[k%2]: ZC finished item k-2), arrives U_full[k%2].
+//
+// Rows are counted globally over the CTA's items (r), so every ring barrier keeps its parity
+// arithmetic; per-item energies are reduced over the 8 EP warps (named barrier 2).
+// =============================================================================================
+template <int M, int NP, int R>
+struct Tc5Geom {
+    using B = TcGeom<M, NP, R>;
+    using G4 = Tc4Geom<M, NP, R>;
+    static constexpr int UBUF = B::UY * B::UP;                // floats per u buffer
+    static constexpr int SM_B = 0;
+    static constexpr int SM_U = B::B_FLOATS;                  // [2][UBUF]
+    static constexpr int SM_Z = SM_U + 2 * UBUF;
+    static constexpr int SM_FLOATS = SM_Z + 2 * B::TAPS * B::LANES;
+    static constexpr int SMEM_BYTES = SM_FLOATS * 4 + 64;
+    static constexpr int THREADS = 25 * 32;                   // + 4 loader warps
+};
+
+template <int M, int NP, int R>
+__global__ void __launch_bounds__(25 * 32, 1) k_prior_grad_tc5(const TcArgs ta, const __grid_constant__ TcConst cc) {
+    using G = TcGeom<M, NP, R>;
+    using G4 = Tc4Geom<M, NP, R>;
+    using G5 = Tc5Geom<M, NP, R>;
+    constexpr int C = G::C, KT = G::KT, TAPS = G::TAPS, L = G::LANES, NB = G::NB, ND = G4::ND, RR = G::RR;
+    extern __shared__ __align__(128) float sm[];
+    float* bsm = sm + G5::SM_B;
+    float* ubuf = sm + G5::SM_U;
+    float* zs = sm + G5::SM_Z;
+    __shared__ uint32_t tbase_s;
+    __shared__ __align__(8) uint64_t bar_afull[2], bar_aempty[2], bar_dfull[ND], bar_dempty[ND], bar_zfull[ND];
+    __shared__ __align__(8) uint64_t bar_pfull, bar_pempty, bar_ufull[2], bar_uempty[2];
+    __shared__ float cst_s[2];
+    __shared__ double wc_s[2];
+    __shared__ double ep_red[2][8];
+
+    const K1Args& args = ta.k;
+    const int H = args.H, W = args.W;
+    const size_t HW = (size_t)H * W;
+    const int ntiles = args.ntiles, B = ta.nimg;
+    const int nitems = ntiles * B;
+    const int t = threadIdx.x, warp = __shfl_sync(0xffffffffu, t >> 5, 0), lane = t & 31;
+    const int l = (warp & 3) * 32 + lane;
+    const bool udom = args.udom != 0;
+
+    if (warp == 0) tc::tmem_alloc<512>(&tbase_s);
+    if (t == 0) {
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&bar_afull[s], 8);
+            tc::mbar_init(&bar_aempty[s], 1);
+            tc::mbar_init(&bar_ufull[s], 4);
+            tc::mbar_init(&bar_uempty[s], 4);
+        }
+        for (int s = 0; s < ND; ++s) {
+            tc::mbar_init(&bar_dfull[s], 1);
+            tc::mbar_init(&bar_dempty[s], 4);
+            tc::mbar_init(&bar_zfull[s], 1);
+        }
+        tc::mbar_init(&bar_pfull, 8);
+        tc::mbar_init(&bar_pempty, 1);
+        tc::mbar_fence_init();
+    }
+    {
+        const float4* src = reinterpret_cast<const float4*>(ta.bimg);
+        float4* dst = reinterpret_cast<float4*>(bsm);
+#pragma unroll 4
+        for (int i = t; i < G::B_FLOATS / 4; i += G5::THREADS) dst[i] = __ldg(src + i);
+    }
+    tc::fence_proxy_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tb = tbase_s;
+    const uint32_t tl = tb + ((uint32_t)((warp & 3) * 32) << 16);
+
+    // the CTA's items: it = blockIdx.x + k * gridDim.x (blockIdx.y == 0 launches only); an item of
+    // an inactive image is skipped identically by every role
+    auto item_ok = [&](int it, int& b, int& tile) -> bool {
+        b = it / ntiles;
+        tile = it - b * ntiles;
+        return args.ctl == nullptr || args.ctl[b].active;
+    };
+
+    if (warp < 8) {
+        // ================================ IM ================================
+        constexpr int H8 = (KT / 8 + 1) / 2;
+        const int ig = warp >> 2;
+        int k = 0, r = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            int b, tile;
+            if (!item_ok(it, b, tile)) continue;
+            const int ubi = k & 1;
+            tc::mbar_wait(&bar_ufull[ubi], (uint32_t)((k >> 1) & 1));
+            const float* us = ubuf + ubi * G5::UBUF;
+#pragma unroll 1
+            for (int j = 0; j < RR; ++j, ++r) {
+                const int s = r & 1;
+                if (r >= 2) {
+                    tc::mbar_wait(&bar_aempty[s], (uint32_t)(((r >> 1) - 1) & 1));
+                    tc::fence_after_sync();
+                }
+                const float* up = us + j * G::UP + l;
+                const float vc = up[C * G::UP + C];
+                const uint32_t a_hi = tl + G4::COL_A0 + s * 2 * KT, a_lo = a_hi + KT;
+                if (ig == 0) tc_im2col<M, G::UP, 0, H8>(up, vc, a_hi, a_lo);
+                else tc_im2col<M, G::UP, H8, KT / 8>(up, vc, a_hi, a_lo);
+                tc::wait_st();
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&bar_afull[s]);
+            }
+            ++k;
+        }
+    } else if (warp < 16) {
+        // ================================ EP ================================
+        const int half = (warp - 8) >> 2, ew = warp - 8;
+        int k = 0, r = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            int b, tile;
+            if (!item_ok(it, b, tile)) continue;
+            const int ubi = k & 1;
+            tc::mbar_wait(&bar_ufull[ubi], (uint32_t)((k >> 1) & 1));
+            const float* us = ubuf + ubi * G5::UBUF;
+            const float cst = cst_s[ubi];
+            const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
+            const int y0 = ty * R, x0 = tx * G::OW;
+            const int lx = x0 - C + l;
+            const bool col_own = (l >= C) && (l < C + G::OW) && (lx < W);
+            double e_acc = 0.0;
+#pragma unroll 1
+            for (int j = 0; j < RR; ++j, ++r) {
+                const int s = r % ND;
+                tc::mbar_wait(&bar_dfull[s], (uint32_t)((r / ND) & 1));
+                tc::fence_after_sync();
+                const float uq = us[(j + C) * G::UP + l + C] + cst;
+                constexpr int HF = NP / 2;
+                float el, zl, ph[HF], pl[HF];
+                if (half == 0) tc4_ep_half<NP, 0>(tl + G4::COL_D0 + s * NP, uq, cc, el, zl, ph, pl, false);
+                else tc4_ep_half<NP, 1>(tl + G4::COL_D0 + s * NP, uq, cc, el, zl, ph, pl, false);
+                const bool own = col_own && (j >= C) && (j < C + R) && (y0 - C + j < H);
+                if (own) e_acc += (double)el;
+                if (r >= 1) {
+                    tc::mbar_wait(&bar_pempty, (uint32_t)((r - 1) & 1));
+                    tc::fence_after_sync();
+                }
+#pragma unroll
+                for (int c8 = 0; c8 < HF / 8; ++c8) {
+                    tc::tmem_st8(tl + G4::COL_P + half * HF + c8 * 8, *reinterpret_cast<float(*)[8]>(ph + c8 * 8));
+                    tc::tmem_st8(tl + G4::COL_P + NP + half * HF + c8 * 8, *reinterpret_cast<float(*)[8]>(pl + c8 * 8));
+                }
+                tc::tmem_st1(tl + G4::COL_ZL + s * 2 + half, zl);
+                tc::wait_st();
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&bar_pfull);
+            }
+            // (a7) the item's energy: fixed-order sum over the 8 EP warps
+            const double ew_sum = warp_sum_d(e_acc);
+            if (lane == 0) ep_red[k & 1][ew] = ew_sum;
+            tc::named_sync(2, 256);
+            if (ew == 0 && lane == 0) {
+                double e = 0.0;
+                for (int i = 0; i < 8; ++i) e += ep_red[k & 1][i];
+                args.epart[(size_t)b * ntiles + tile] = e;
+            }
+            ++k;
+        }
+    } else if (warp < 20) {
+        // ================================ ZC ================================
+        int k = 0, r = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            int b, tile;
+            if (!item_ok(it, b, tile)) continue;
+            const int ubi = k & 1;
+            tc::mbar_wait(&bar_ufull[ubi], (uint32_t)((k >> 1) & 1));
+            const float* us = ubuf + ubi * G5::UBUF;
+            const float cst = cst_s[ubi];
+            const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
+            const int y0 = ty * R, x0 = tx * G::OW;
+            int gslot = 0;
+            if (args.ctl != nullptr) gslot = args.which_cur ? args.ctl[b].gcur : args.ctl[b].gcand;
+            float* gout = args.g + (size_t)gslot * args.g_slot_stride + (size_t)b * HW;
+            const bool out_col = (l < G::OW) && (x0 + l < W);
+            float acc[M];
+#pragma unroll
+            for (int q = 0; q < M; ++q) acc[q] = 0.f;
+#pragma unroll 1
+            for (int j = 0; j < RR; ++j, ++r) {
+                const int s = r % ND, zb = r & 1;
+                tc::mbar_wait(&bar_zfull[s], (uint32_t)((r / ND) & 1));
+                tc::fence_after_sync();
+                float z[NB < 32 ? 32 : NB];
+                if constexpr (NB == 48) {
+                    tc::tmem_ld32(tl + G4::COL_D0 + s * NP, z);
+                    tc::tmem_ld16(tl + G4::COL_D0 + s * NP + 32, *reinterpret_cast<float(*)[16]>(z + 32));
+                } else if constexpr (NB == 24) {
+                    tc::tmem_ld16(tl + G4::COL_D0 + s * NP, *reinterpret_cast<float(*)[16]>(z));
+                    tc::tmem_ld8(tl + G4::COL_D0 + s * NP + 16, *reinterpret_cast<float(*)[8]>(z + 16));
+                } else {
+                    tc::tmem_ld8(tl + G4::COL_D0 + s * NP, *reinterpret_cast<float(*)[8]>(z));
+                }
+                float zl0, zl1;
+                tc::tmem_ld2(tl + G4::COL_ZL + s * 2, zl0, zl1);
+                tc::wait_ld();
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&bar_dempty[s]);
+                float* zr = zs + zb * TAPS * L;
+#pragma unroll
+                for (int q = 0; q < NB; ++q) zr[q * L + l] = z[q];
+                zr[NB * L + l] = zl0 + zl1;
+                tc::named_sync(1, 128);
+#pragma unroll
+                for (int a = 0; a < M; ++a) {
+                    float sa = 0.f;
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) sa += zr[(a * M + bb) * L + l + bb];
+                    acc[a] += sa;
+                }
+                const int o = j - 2 * C;
+                if (o >= 0 && o < R && out_col && y0 + o < H) {
+                    const float u = udom ? 1.0f : us[(o + 2 * C) * G::UP + l + 2 * C] + cst;
+                    gout[(size_t)(y0 + o) * W + x0 + l] = u * acc[M - 1];
+                }
+#pragma unroll
+                for (int q = M - 1; q > 0; --q) acc[q] = acc[q - 1];
+                acc[0] = 0.f;
+            }
+            // every role is done with U[ubi] once the last Z row of the item is consumed
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&bar_uempty[ubi]);
+            ++k;
+        }
+    } else if (warp == 20) {
+        // ================================ MMA ================================
+        const uint32_t idf = tc::idesc_tf32(128, NP), idb = tc::idesc_tf32(128, NB);
+        const uint32_t b_base = tc::smem_u32(bsm);
+        int r = 0;
+        auto issue_b = [&](int rb) {
+            const int s = rb % ND;
+            tc::mbar_wait(&bar_pfull, (uint32_t)(rb & 1));
+            tc::fence_after_sync();
+            const uint32_t z = tb + G4::COL_D0 + s * NP, p_hi = tb + G4::COL_P, p_lo = p_hi + NP;
+#pragma unroll
+            for (int q = 0; q < NP / 8; ++q) {
+                const uint32_t off = (uint32_t)(q * 2 * NB * 16);
+                const uint64_t bh = tc::sdesc_kmajor(b_base + 2 * G::BF_FLOATS * 4 + off, NB * 16, 128);
+                const uint64_t bl = tc::sdesc_kmajor(b_base + (2 * G::BF_FLOATS + G::BB_FLOATS) * 4 + off, NB * 16, 128);
+                tc::mma_tf32_ts_warp(z, p_hi + q * 8, bl, idb, q > 0);
+                tc::mma_tf32_ts_warp(z, p_lo + q * 8, bh, idb, 1);
+            }
+#pragma unroll
+            for (int q = 0; q < NP / 8; ++q) {
+                const uint64_t bh = tc::sdesc_kmajor(b_base + 2 * G::BF_FLOATS * 4 + (uint32_t)(q * 2 * NB * 16), NB * 16, 128);
+                tc::mma_tf32_ts_warp(z, p_hi + q * 8, bh, idb, 1);
+            }
+            tc::mma_commit_warp(&bar_pempty);
+            tc::mma_commit_warp(&bar_zfull[s]);
+        };
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            int b, tile;
+            if (!item_ok(it, b, tile)) continue;
+#pragma unroll 1
+            for (int j = 0; j < RR; ++j, ++r) {
+                const int s = r & 1, sd = r % ND;
+                tc::mbar_wait(&bar_afull[s], (uint32_t)((r >> 1) & 1));
+                if (r >= ND) tc::mbar_wait(&bar_dempty[sd], (uint32_t)(((r / ND) - 1) & 1));
+                tc::fence_after_sync();
+                const uint32_t a_hi = tb + G4::COL_A0 + s * 2 * KT, a_lo = a_hi + KT, d = tb + G4::COL_D0 + sd * NP;
+#pragma unroll
+                for (int q = 0; q < KT / 8; ++q) {
+                    const uint32_t off = (uint32_t)(q * 2 * NP * 16);
+                    const uint64_t bh = tc::sdesc_kmajor(b_base + off, NP * 16, 128);
+                    const uint64_t bl = tc::sdesc_kmajor(b_base + G::BF_FLOATS * 4 + off, NP * 16, 128);
+                    tc::mma_tf32_ts_warp(d, a_hi + q * 8, bl, idf, q > 0);
+                    tc::mma_tf32_ts_warp(d, a_lo + q * 8, bh, idf, 1);
+                }
+#pragma unroll
+                for (int q = 0; q < KT / 8; ++q) {
+                    const uint64_t bh = tc::sdesc_kmajor(b_base + (uint32_t)(q * 2 * NP * 16), NP * 16, 128);
+                    tc::mma_tf32_ts_warp(d, a_hi + q * 8, bh, idf, 1);
+                }
+                tc::mma_commit_warp(&bar_aempty[s]);
+                tc::mma_commit_warp(&bar_dfull[sd]);
+                if (r >= 1) issue_b(r - 1);
+            }
+        }
+        if (r >= 1) issue_b(r - 1);
+    } else {
+        // ================================ LD: u tiles ================================
+        const int lw = warp - 21;
+        int k = 0;
+        for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+            int b, tile;
+            if (!item_ok(it, b, tile)) continue;
+            const int ubi = k & 1;
+            if (k >= 2) tc::mbar_wait(&bar_uempty[ubi], (uint32_t)(((k >> 1) - 1) & 1));
+            int wslot = 0;
+            if (args.ctl != nullptr) wslot = args.which_cur ? args.ctl[b].cur : args.ctl[b].cand;
+            const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
+            const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
+            const int y0 = ty * R, x0 = tx * G::OW;
+            const int yc = min(y0 + R / 2, H - 1), xc = min(x0 + G::OW / 2, W - 1);
+            const double wc = w[(size_t)yc * W + xc];
+            const float cst = (float)(udom ? wc : exp(wc));
+            tc_stage_u<G::UY, G::UX, G::UP, 4>(ubuf + ubi * G5::UBUF, w, args.halo, H, W, y0, x0, 2 * C, udom, cst,
+                                               wc, lw, lane);
+            if (lw == 0 && lane == 0) { cst_s[ubi] = cst; wc_s[ubi] = wc; }
+            __threadfence_block();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&bar_ufull[ubi]);
+            ++k;
+        }
+    }
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc<512>(tb);
