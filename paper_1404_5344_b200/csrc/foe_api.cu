@@ -130,14 +130,15 @@ cudaError_t tc_set_attr() {
     return cudaFuncSetAttribute(foe::k_prior_grad_tc5<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 foe::Tc5Geom<M, NP, kTcR>::SMEM_BYTES);
 }
-// K8 variant: 4 = warp-specialised single-CTA pipeline (default; 1.54 ms per c4 launch under
-// ncu), 3 = two lock-step CTAs per SM (1.58 ms; FOE_K8_VARIANT=3)
+// K8 variant (ncu, one c4 launch): 3 = two lock-step CTAs per SM (default, 1.43 ms), 4 = warp-
+// specialised single-CTA pipeline (1.49 ms; FOE_K8_VARIANT=4), 5 = the pipeline persistent over
+// tiles (no gain over 4; FOE_K8_VARIANT=5)
 int tc_variant() {
     const char* e = std::getenv("FOE_K8_VARIANT");   // read per launch (A/B in one process)
-    if (e && e[0] == '3') return 3;
+    if (e && e[0] == '4') return 4;
     if (e && e[0] == '5') return 5;
     if (e && e[0] == 'k' && e[1] >= '1' && e[1] <= '4') return 40 + (e[1] - '0');   // profiling knockouts
-    return 4;
+    return 3;
 }
 // the banks K8 has an instantiation for: (m, padded N_f)
 int tc_np(int m, int nf) {

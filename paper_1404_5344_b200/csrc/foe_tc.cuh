@@ -13,7 +13,8 @@
 // A operands (U, P) live in TMEM, written by the epilogue threads (one pixel = one TMEM lane);
 // B operands (Kf, Kb; hi and lo tf32 halves) are staged once per CTA in shared memory in the
 // K-major no-swizzle canonical layout; accumulators R and Z are in TMEM.  Each product x.y is
-// evaluated as x_hi y_hi + x_hi y_lo + x_lo y_hi with x_hi = tf32(x), x_lo = tf32(x - x_hi):
+// evaluated as x_hi y_hi + x_hi y_lo + x_lo y_hi with x_hi = tf32(x), x_lo = x - x_hi (its top
+// 11 bits are what the tensor core reads):
 // error ~2^-21 relative, i.e. fp32-level (the path's tolerance is 1e-5 relative L2,
 // BASELINE.json north_star).  The im2col subtracts each response pixel's own window centre
 // u_q (a per-pixel DC shift, restored as u_q sum_t k in the epilogue), so the tensor-core

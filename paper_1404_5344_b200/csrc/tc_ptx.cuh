@@ -13,6 +13,12 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+// 1: round the low part of each 3xTF32 split to tf32 (unbiased); 0: let the tensor core drop its
+// low bits (3 fewer FP32x2 operations per value pair)
+#ifndef FOE_TF32_LO_ROUND
+#define FOE_TF32_LO_ROUND 0
+#endif
 #include <stdint.h>
 
 namespace foe {
@@ -192,9 +198,13 @@ __device__ __forceinline__ void tf32_split2(float2 x, float2& hi, float2& lo) {
     const float2 t = __fadd2_rn(c, make_float2(-x.x, -x.y));
     hi = __fadd2_rn(c, make_float2(-t.x, -t.y));
     const float2 r = __fadd2_rn(x, make_float2(-hi.x, -hi.y));        // exact
+#if FOE_TF32_LO_ROUND
     const float2 c2 = fmul2_nocontract(r, s);
     const float2 t2 = __fadd2_rn(c2, make_float2(-r.x, -r.y));
     lo = __fadd2_rn(c2, make_float2(-t2.x, -t2.y));
+#else
+    lo = r;   // the tensor core keeps lo's top 11 bits: error <= 2^-11 |lo| <= 2^-22 |x|
+#endif
 }
 
 // fp32 -> tf32 (round to nearest, ties away), kept in a 32-bit container

@@ -1,5 +1,5 @@
 #!/bin/bash
-OUT=gpurun_out/r01w
+OUT=gpurun_out/r01y
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/rc.txt
 timeout 1500 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/rc.txt
@@ -7,3 +7,4 @@ timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=
 timeout 900 python bench.py --config c5 --steps 2 --warmup 3 > $OUT/bench_c5.json 2> $OUT/bench_c5.err; echo "bench c5 rc=$?" >> $OUT/rc.txt
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "bench ref rc=$?" >> $OUT/rc.txt
 cat $OUT/rc.txt
+timeout 300 python tools/prof_stencil.py > $OUT/prof.log 2>&1
