@@ -627,21 +627,25 @@ __device__ __forceinline__ double exp_small(double x) {
 }
 __device__ __forceinline__ double exp_near0(double x) { return fabs(x) <= 0.0625 ? exp_small(x) : exp(x); }
 
+// Taylor coefficients 1/k! of the cosh / sinh parts, in the constant bank (fp64 FMAs take them
+// as c[] operands; as immediates every use cost two uniform moves)
+__constant__ double kCoshC[9] = {4.7794773323873853e-14, 1.1470745597729725e-11, 2.0876756987868100e-09,
+                                 2.7557319223985891e-07, 2.4801587301587302e-05, 1.3888888888888889e-03,
+                                 4.1666666666666664e-02, 0.5, 1.0};   // 1/16!, 1/14!, ..., 1/2!, 1
+__constant__ double kSinhC[8] = {7.6471637318198164e-13, 1.6059043836821613e-10, 2.5052108385441720e-08,
+                                 2.7557319223985893e-06, 1.9841269841269841e-04, 8.3333333333333332e-03,
+                                 1.6666666666666666e-01, 1.0};        // 1/15!, 1/13!, ..., 1/3!, 1
+
 // e^{x} and e^{-x} together for |x| <= 1/16: even and odd Taylor parts C = cosh x, S = sinh x
 // (terms to x^10, remainder < 1e-20 relative), e^{+-x} = C +- S -- half the work of two exp_small
 __device__ __forceinline__ void exp_pm_small(double x, double& ep, double& em) {
     const double x2 = x * x;
-    double c = 2.7557319223985891e-07;             // 1/10!
-    c = fma(c, x2, 2.4801587301587302e-05);        // 1/8!
-    c = fma(c, x2, 1.3888888888888889e-03);        // 1/6!
-    c = fma(c, x2, 4.1666666666666664e-02);        // 1/4!
-    c = fma(c, x2, 0.5);
-    c = fma(c, x2, 1.0);
-    double sh = 2.7557319223985893e-06;            // 1/9!
-    sh = fma(sh, x2, 1.9841269841269841e-04);      // 1/7!
-    sh = fma(sh, x2, 8.3333333333333332e-03);      // 1/5!
-    sh = fma(sh, x2, 1.6666666666666666e-01);      // 1/3!
-    sh = fma(sh, x2, 1.0);
+    double c = kCoshC[3];                          // 1/10!
+#pragma unroll
+    for (int i = 4; i < 9; ++i) c = fma(c, x2, kCoshC[i]);
+    double sh = kSinhC[3];                         // 1/9!
+#pragma unroll
+    for (int i = 4; i < 8; ++i) sh = fma(sh, x2, kSinhC[i]);
     sh *= x;
     ep = c + sh;
     em = c - sh;
@@ -654,23 +658,12 @@ __device__ __forceinline__ void exp2a_pm(double a, double& ep, double& em) {
     const double n = rint(x * 1.4426950408889634);                   // x / ln 2
     const double r = fma(-n, 2.3190468138462996e-17, fma(-n, 6.9314718055994529e-01, x));   // x - n ln2
     const double r2 = r * r;
-    double c = 4.7794773323873853e-14;             // 1/16!
-    c = fma(c, r2, 1.1470745597729725e-11);        // 1/14!
-    c = fma(c, r2, 2.0876756987868100e-09);        // 1/12!
-    c = fma(c, r2, 2.7557319223985891e-07);        // 1/10!
-    c = fma(c, r2, 2.4801587301587302e-05);        // 1/8!
-    c = fma(c, r2, 1.3888888888888889e-03);        // 1/6!
-    c = fma(c, r2, 4.1666666666666664e-02);        // 1/4!
-    c = fma(c, r2, 0.5);
-    c = fma(c, r2, 1.0);
-    double sh = 7.6471637318198164e-13;            // 1/15!
-    sh = fma(sh, r2, 1.6059043836821613e-10);      // 1/13!
-    sh = fma(sh, r2, 2.5052108385441720e-08);      // 1/11!
-    sh = fma(sh, r2, 2.7557319223985893e-06);      // 1/9!
-    sh = fma(sh, r2, 1.9841269841269841e-04);      // 1/7!
-    sh = fma(sh, r2, 8.3333333333333332e-03);      // 1/5!
-    sh = fma(sh, r2, 1.6666666666666666e-01);      // 1/3!
-    sh = fma(sh, r2, 1.0);
+    double c = kCoshC[0];                          // 1/16!
+#pragma unroll
+    for (int i = 1; i < 9; ++i) c = fma(c, r2, kCoshC[i]);
+    double sh = kSinhC[0];                         // 1/15!
+#pragma unroll
+    for (int i = 1; i < 8; ++i) sh = fma(sh, r2, kSinhC[i]);
     sh *= r;
     const int ni = (int)n;
     ep = (c + sh) * __hiloint2double((ni + 1023) << 20, 0);
