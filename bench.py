@@ -198,6 +198,12 @@ def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cf
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     fp32_peak = nsm * 128 * 2 * sm_max * 1e6 / 1e12
+    micro = {}
+    try:   # our own microbenchmarks (tools/probes/peaks.cu): FFMA2 chains, back-to-back tcgen05 TF32
+        with open(os.path.join(ROOT, "profiles", "r01_peaks_microbench.json")) as fh:
+            micro = json.load(fh)
+    except Exception:
+        pass
     common = {"achieved": alg_tflops, "unit": "TFLOP/s", "traffic": args.traffic_bytes,
               "fp32_peak": fp32_peak, "fp32_frac": (alg_tflops / fp32_peak) if alg_tflops else None,
               "k_ms_per_launch": k_ms / max(k_launches, 1), "k_launches": k_launches,
@@ -214,6 +220,11 @@ def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cf
         exec_px = 3 * 2 * 2 * kt * np_ * (64 + 2 * c) * 128 / (64 * ow)
         alg_px = 4.0 * nf * m * m
         ex = alg_tflops * exec_px / alg_px if alg_tflops else None
+        if micro.get("tf32_tflops", -1) > 0:
+            common["tf32_peak_microbench"] = micro["tf32_tflops"]
+            common["tensor_executed_frac_of_microbench"] = (ex / micro["tf32_tflops"]) if ex else None
+        if micro.get("fp32_tflops", -1) > 0:
+            common["fp32_peak_microbench"] = micro["fp32_tflops"]
         return dict(common, bound="tensor", peak=tf32_peak, frac=(alg_tflops / tf32_peak) if alg_tflops else None,
                     kernel="k_prior_grad_tc (K8: tcgen05 TF32 x3, TMEM accumulators)",
                     peak_source=f"derived: measured sustained bf16 {bf16:.1f} TFLOP/s x 1.1/2.25 (nominal TF32/BF16), "
