@@ -527,6 +527,7 @@ foe_status check_dims(const foe_model* md, int B, int H, int W) {
         return fail(FOE_ERR_INVALID_ARGUMENT, "image %dx%d smaller than the %dx%d filters (SPEC.md:92)", H, W,
                     md->m, md->m);
     if ((long long)B * H * W > (1LL << 40)) return fail(FOE_ERR_INVALID_ARGUMENT, "B*H*W too large");
+    if (B > 65535) return fail(FOE_ERR_INVALID_ARGUMENT, "B=%d exceeds 65535 images per call (one grid row per image)", B);
     return FOE_OK;
 }
 
