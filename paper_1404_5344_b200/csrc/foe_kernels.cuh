@@ -764,8 +764,8 @@ struct K2Args {
 };
 
 template <int PXT>
-__global__ void __launch_bounds__(kThreads, 3)
-k_inertial_prox(const K2Args a) {  // (3 CTAs/SM: <= 80 registers)
+__global__ void __launch_bounds__(kThreads, 4)
+k_inertial_prox(const K2Args a) {  // (4 CTAs/SM: <= 64 registers; 3 -> 4 gave 253 -> 222 us, 5 spills)
     const int b = blockIdx.y;
     const ImgCtl& c = a.ctl[b];
     if (!c.active) return;
