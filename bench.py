@@ -52,6 +52,8 @@ def parse_args():
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--images", type=int, default=0, help="images per GPU (default: the config's batch)")
     ap.add_argument("--iters", type=int, default=0, help="override iteration count (quick runs only)")
+    ap.add_argument("--solver", choices=["auto", "graph", "persistent"], default="auto",
+                    help="trial-loop driver (auto: persistent for single small images, SURVEY 8(f) f4)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-p2p", action="store_true", help="c5: ghost rows over ncclSend/Recv instead of K2 peer stores")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -184,7 +186,7 @@ def run_reference(args, cfg):
     return 0
 
 
-def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cfg):
+def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cfg, persistent=False):
     """Roofline of the dominant kernel (the prior stencil, ~90% of the step).
 
     achieved = ALGORITHMIC flops (4 N_f m^2 per pixel per evaluation) / the
@@ -230,8 +232,11 @@ def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cf
                     peak_source=f"derived: measured sustained bf16 {bf16:.1f} TFLOP/s x 1.1/2.25 (nominal TF32/BF16), "
                                 f"{peak_src} MEASURED_PEAKS.json",
                     tensor_executed_tflops=ex, tensor_executed_frac=(ex / tf32_peak) if ex else None)
+    kname = ("k_ipiano_persistent (all trial rounds of a solve in one cooperative launch: K2 + K1 FFMA2 "
+             "stencil + K3 per round; timed around ipiano_solve, so achieved covers the whole round)"
+             if persistent else "k_prior_grad2 (K1: FFMA2 fused FoE energy+gradient stencil)")
     return dict(common, bound="alu", peak=fp32_peak, frac=(alg_tflops / fp32_peak) if alg_tflops else None,
-                kernel="k_prior_grad2 (K1: FFMA2 fused FoE energy+gradient stencil)",
+                kernel=kname,
                 peak_source=f"derived: {nsm} SMs x 128 FP32 lanes x 2 flop x {sm_max:.0f} MHz "
                             f"(sm_max_mhz, {peak_src} MEASURED_PEAKS.json) -- DESIGN.md")
 
@@ -310,14 +315,28 @@ def main():
     d["L0"] = L0
     del v0
 
-    cfgc = P.ipiano_config_default(max_iters=cfg.iters, record_trace=0)
+    solver = {"auto": P.FOE_SOLVER_AUTO, "graph": P.FOE_SOLVER_GRAPH, "persistent": P.FOE_SOLVER_PERSISTENT}[args.solver]
+    cfgc = P.ipiano_config_default(max_iters=cfg.iters, record_trace=0, solver=solver)
     st = P.ipiano_state_create(md, f_dev, d["lambdas"], L0, cfgc)
     u_dev = torch.empty((B, H, W), dtype=torch.float32, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
-    def step():
+    # small single-image configs resolve to the persistent driver (one cooperative launch per
+    # solve); its dominant kernel is that launch, timed around ipiano_solve
+    persistent = P.ipiano_state_solver(st) == P.FOE_SOLVER_PERSISTENT
+    solve_ms = []
+
+    def step(timed=False):
         P.ipiano_state_reset(st, f_dev, L0)
-        P.ipiano_solve(st)
+        if timed and persistent:
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            P.ipiano_solve(st)
+            s1.record(stream)
+            solve_ms.append((s0, s1))
+        else:
+            P.ipiano_solve(st)
         P.ipiano_get_iterate(st, want_w=False, u_out=u_dev)
 
     for _ in range(args.warmup):
@@ -325,8 +344,9 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region (value): inputs resident in HBM
-    P.ipiano_profile(st, True)
-    P.ipiano_profile_read(st)  # reset counters
+    if not persistent:
+        P.ipiano_profile(st, True)
+        P.ipiano_profile_read(st)  # reset counters
     sampler = ClockSampler(smi_index(local)) if rank == 0 else None
     if sampler:
         sampler.start()
@@ -339,7 +359,7 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        step()
+        step(timed=True)
         e1.record(stream)
         e1.synchronize()
         step_ms.append(e0.elapsed_time(e1))
@@ -347,7 +367,10 @@ def main():
     launches = P.foe_kernel_launches() - launches0
     D.barrier()
     clocks = sampler.stop() if sampler else None
-    k1_ms, k1_launches, _ = P.ipiano_profile_read(st)
+    if persistent:
+        k1_ms, k1_launches = sum(a.elapsed_time(b) for a, b in solve_ms), len(solve_ms)
+    else:
+        k1_ms, k1_launches, _ = P.ipiano_profile_read(st)
     cnt = P.ipiano_get_counters(st)
     total_ms = D.max_over_ranks(sum(step_ms), dev)
     mp_it_rank = B * H * W * cfg.iters / 1e6
@@ -360,7 +383,8 @@ def main():
     flops_per_eval_px = 4.0 * cfg.n_filters * cfg.m * cfg.m
     k1_flops = flops_per_eval_px * H * W * trials_per_step * args.steps
     k1_tflops = k1_flops / (k1_ms / 1e3) / 1e12 if k1_ms > 0 else None
-    roofline = roofline_entry(P.ipiano_state_stencil(st), k1_tflops, k1_ms, k1_launches, step_ms, args, dev, cfg)
+    roofline = roofline_entry(P.ipiano_state_stencil(st), k1_tflops, k1_ms, k1_launches, step_ms, args, dev, cfg,
+                              persistent=persistent)
     fp32_peak = roofline["fp32_peak"]
 
     # ---- e2e: the public C-ABI call with host buffers (H2D of f and D2H of u inside)
@@ -409,6 +433,7 @@ def main():
             "run_fp32_frac": (flops_per_eval_px * H * W * trials_per_step * args.steps * ws / (total_ms / 1e3) / 1e12)
                              / fp32_peak / ws,
             "lipschitz_ms": lipschitz_ms, "status": [int(s) for s in set(cnt["status"].tolist())],
+            "solver": "persistent" if persistent else "graph",
         }
         emit(line)
     st.destroy()

@@ -162,7 +162,24 @@ typedef struct {
     int filter_groups;       /* 0 = automatic; else split the N_f filters over this many CTAs
                                 per tile (partial gradients summed in fixed order)                    */
     int stencil;             /* prior energy+gradient kernel: FOE_STENCIL_AUTO / _FFMA / _TENSOR     */
+    int solver;              /* trial-loop driver: FOE_SOLVER_AUTO / _GRAPH / _PERSISTENT (below)    */
 } ipiano_config;
+
+/* Trial-loop drivers.  Both run the same K2 -> K1 -> K3 round per trial
+ * (inertial point + prox, prior energy+gradient at the candidate, backtracking decision):
+ *   FOE_SOLVER_GRAPH       three dependent launches per round, captured as a CUDA graph of 10
+ *                          rounds; any size, either stencil.
+ *   FOE_SOLVER_PERSISTENT  ONE cooperative launch runs all rounds: a co-resident grid does K2
+ *                          and K1 as grid-strided phases separated by grid barriers, and every
+ *                          CTA takes the (identical, fixed-order) decision itself.  FFMA stencil
+ *                          only (FOE_ERR_UNSUPPORTED with FOE_STENCIL_TENSOR); for images that
+ *                          cannot fill the GPU, where launches and their gaps dominate a round.
+ *   FOE_SOLVER_AUTO        persistent when the state resolves to the FFMA stencil and
+ *                          B*H*W <= 2^18 (configs c1-c3), else the graph.
+ * ipiano_profile(st, 1) (per-launch K1 timing) always uses the graph driver. */
+#define FOE_SOLVER_AUTO 0
+#define FOE_SOLVER_GRAPH 1
+#define FOE_SOLVER_PERSISTENT 2
 
 /* Fills the defaults above (graded policy). */
 void ipiano_config_default(ipiano_config* cfg);
@@ -230,6 +247,9 @@ foe_status ipiano_profile_read(ipiano_state* st, double* k1_ms, long long* k1_la
 
 /* The stencil this state resolved to (FOE_STENCIL_FFMA or FOE_STENCIL_TENSOR). */
 int ipiano_state_stencil(const ipiano_state* st);
+
+/* The trial-loop driver this state resolved to (FOE_SOLVER_GRAPH or FOE_SOLVER_PERSISTENT). */
+int ipiano_state_solver(const ipiano_state* st);
 
 void ipiano_state_destroy(ipiano_state* st);
 

@@ -19,6 +19,7 @@
 #include "foe_kernels.cuh"
 #include "foe_tc.cuh"
 #include "foe_eval.cuh"
+#include "foe_persist.cuh"
 
 using foe::ImgCtl;
 using foe::K1Args;
@@ -185,14 +186,19 @@ struct ipiano_state {
     ipiano_config cfg_in{};   // the configuration as the caller passed it (ipiano_run's cache key)
     foe::SolverParams sp{};
     int tiles_x = 0, ntiles = 0, groups = 1, nchunks = 0, nblk2 = 0;
+    int pxt2 = 8;                 // pixels per thread of K2 (nblk2 = HW / (kThreads pxt2) blocks)
     int kind = FOE_STENCIL_FFMA;  // resolved stencil of this state (K1 or K8)
+    int solver = FOE_SOLVER_GRAPH;  // resolved trial-loop driver
+    int pgrid = 0;                // persistent driver: co-resident CTAs
+    unsigned int* bar = nullptr;  // persistent driver: grid barrier counter
+    unsigned long long* phase_ns = nullptr;  // FOE_PERSIST_PHASES=1: CTA 0's phase timestamps
     double* w = nullptr;      // [3][B][HW]
     float* g = nullptr;       // [2][groups][B][HW]
     float* ft = nullptr;      // [B][HW]
     double* epart = nullptr;  // [B][ntiles*groups]
-    double* ppart = nullptr;  // [B][nblk2][8]
+    double* ppart = nullptr;  // [2][B][nblk2][8] (buffer 1: the persistent driver's odd rounds)
     double* trace = nullptr;  // [B][max_iters+1][8]
-    ImgCtl* ctl = nullptr;
+    ImgCtl* ctl = nullptr;    // [B] ([pgrid][B] with the persistent driver: per-CTA copies)
     ImgCtl* hctl = nullptr;   // pinned mirror
     std::vector<double> lam;  // [B][2]
     cudaStream_t s = nullptr;
@@ -751,6 +757,7 @@ void ipiano_config_default(ipiano_config* c) {
     c->record_trace = 1;
     c->filter_groups = 0;
     c->stencil = FOE_STENCIL_AUTO;
+    c->solver = FOE_SOLVER_AUTO;
 }
 
 }  // extern "C"
@@ -802,8 +809,7 @@ cudaEvent_t pool_event(ipiano_state* st) {
     return e;
 }
 
-// One trial round for every active image: K2 -> K1 (candidate) -> K3.
-foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
+foe::K2Args state_k2_args(const ipiano_state* st) {
     foe::K2Args a2{};
     a2.w = st->w;
     a2.w_slot_stride = (size_t)st->B * st->HW;
@@ -818,7 +824,29 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
     a2.nblk = st->nblk2;
     a2.HW = st->HW;
     a2.idiv = st->model->term == FOE_DATA_IDIV;
-    foe::k_inertial_prox<kPxt2><<<dim3(st->nblk2, st->B), kThreads, 0, s>>>(a2);
+    return a2;
+}
+
+foe::K3Args state_k3_args(const ipiano_state* st) {
+    foe::K3Args a3{};
+    a3.ctl = st->ctl;
+    a3.epart = st->epart;
+    a3.ppart = st->ppart;
+    a3.trace = st->trace;
+    a3.ne = st->ntiles * st->groups;
+    a3.nblk = st->nblk2;
+    a3.estride = 1;
+    a3.sp = st->sp;
+    return a3;
+}
+
+// One trial round for every active image: K2 -> K1 (candidate) -> K3.
+foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
+    const foe::K2Args a2 = state_k2_args(st);
+    const dim3 g2(st->nblk2, st->B);
+    if (st->pxt2 == 1) foe::k_inertial_prox<1><<<g2, kThreads, 0, s>>>(a2);
+    else if (st->pxt2 == 4) foe::k_inertial_prox<4><<<g2, kThreads, 0, s>>>(a2);
+    else foe::k_inertial_prox<kPxt2><<<g2, kThreads, 0, s>>>(a2);
     count_launch(1);
     CKL("k_inertial_prox");
     const K1Args a1 = state_k1_args(st, 0);
@@ -835,19 +863,65 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
         st->ev_live.emplace_back(e0, e1);
         st->k1_launches += 1;
     }
-    foe::K3Args a3{};
-    a3.ctl = st->ctl;
-    a3.epart = st->epart;
-    a3.ppart = st->ppart;
-    a3.trace = st->trace;
-    a3.ne = st->ntiles * st->groups;
-    a3.nblk = st->nblk2;
-    a3.estride = 1;
-    a3.sp = st->sp;
+    const foe::K3Args a3 = state_k3_args(st);
     foe::k_decide<<<st->B, kThreads, 0, s>>>(a3);
     count_launch(1);
     CKL("k_decide");
     st->total_launches += 3;
+    return FOE_OK;
+}
+
+// ---- persistent driver (foe_persist.cuh) ----
+template <int M, int PXT>
+const void* persist_kernel() { return (const void*)foe::k_ipiano_persistent<M, kNCP, kSF2, PXT>; }
+const void* persist_kernel_for(int m, int pxt) {
+    if (m == 7) return pxt == 1 ? persist_kernel<7, 1>() : persist_kernel<7, 4>();
+    if (m == 5) return pxt == 1 ? persist_kernel<5, 1>() : persist_kernel<5, 4>();
+    return pxt == 1 ? persist_kernel<3, 1>() : persist_kernel<3, 4>();
+}
+int smem2_for(int m) { return m == 7 ? smem2_bytes<7>() : m == 5 ? smem2_bytes<5>() : smem2_bytes<3>(); }
+
+// co-resident CTAs of the persistent kernel on this device (0 if cooperative launch is unsupported)
+int persist_capacity(const foe_model* md, int pxt) {
+    int coop = 0;
+    if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, md->dev) != cudaSuccess || !coop) {
+        cudaGetLastError();
+        return 0;
+    }
+    const void* k = persist_kernel_for(md->m, pxt);
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2_for(md->m)) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem2_for(md->m)) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return per_sm * md->nsm;
+}
+
+// up to max_rounds trial rounds (fewer once no image is active) in one cooperative launch
+foe_status launch_persistent(ipiano_state* st, long long max_rounds) {
+    foe::PersistArgs pa{};
+    pa.a1 = state_k1_args(st, 0);
+    pa.a2 = state_k2_args(st);
+    pa.a3 = state_k3_args(st);
+    pa.ctl = st->ctl;
+    pa.bar = st->bar;
+    pa.ppart_stride = (size_t)st->B * st->nblk2 * foe::kNumPart;
+    pa.B = st->B;
+    pa.max_rounds = (int)std::min<long long>(max_rounds, 1LL << 30);
+    pa.k1_items = st->ntiles * st->groups;
+    pa.k2_items = st->nblk2;
+    pa.rounds_out = nullptr;
+    pa.phase_ns = st->phase_ns;
+    CK(cudaMemsetAsync(st->bar, 0, sizeof(unsigned int), st->s));
+    void* args[] = {(void*)&pa, (void*)st->model->tp2};
+    CK(cudaLaunchCooperativeKernel(persist_kernel_for(st->model->m, st->pxt2), dim3(st->pgrid), dim3(kThreads), args,
+                                   (size_t)smem2_for(st->model->m), st->s));
+    count_launch(1);
+    st->total_launches += 1;
     return FOE_OK;
 }
 
@@ -873,7 +947,8 @@ foe_status ensure_graph(ipiano_state* st) {
     return FOE_OK;
 }
 
-foe_status launch_rounds(ipiano_state* st, int rounds) {
+foe_status launch_rounds(ipiano_state* st, long long rounds) {
+    if (st->solver == FOE_SOLVER_PERSISTENT && !st->profile) return launch_persistent(st, rounds);
     if (st->profile) {
         for (int i = 0; i < rounds; ++i) {
             foe_status r = launch_round(st, st->s, true);
@@ -941,7 +1016,7 @@ foe_status state_init(ipiano_state* st, const float* f, const double* lipschitz_
     if (st->cfg.record_trace)
         CK(cudaMemsetAsync(st->trace, 0, sizeof(double) * B * (st->cfg.max_iters + 1) * 8, st->s));
     foe::k_init<<<dim3(st->nblk2, B), kThreads, 0, st->s>>>(f, st->ft, st->w, n, st->ppart, st->nblk2, st->ctl,
-                                                             st->HW, kPxt2, nullptr, nullptr, 0,
+                                                             st->HW, st->pxt2, nullptr, nullptr, 0,
                                                              st->model->term == FOE_DATA_IDIV);
     count_launch(1);
     CKL("k_init");
@@ -963,6 +1038,7 @@ foe_status state_init(ipiano_state* st, const float* f, const double* lipschitz_
 extern "C" {
 
 int ipiano_state_stencil(const ipiano_state* st) { return st ? st->kind : -1; }
+int ipiano_state_solver(const ipiano_state* st) { return st ? st->solver : -1; }
 
 void ipiano_state_destroy(ipiano_state* st) {
     if (!st) return;
@@ -970,7 +1046,19 @@ void ipiano_state_destroy(ipiano_state* st) {
     if (st->s) cudaStreamSynchronize(st->s);
     if (st->graph) cudaGraphExecDestroy(st->graph);
     cudaFree(st->w); cudaFree(st->g); cudaFree(st->ft); cudaFree(st->epart); cudaFree(st->ppart);
-    cudaFree(st->trace); cudaFree(st->ctl);
+    if (st->phase_ns) {   // FOE_PERSIST_PHASES diagnostics: mean phase durations of the last launch
+        std::vector<unsigned long long> h(4 * foe::kPhaseRounds, 0);
+        cudaMemcpy(h.data(), st->phase_ns, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
+        double t[3] = {0, 0, 0};
+        int n = 0;
+        for (int r = 1; r < foe::kPhaseRounds && h[4 * r + 3] > h[4 * r]; ++r, ++n)
+            for (int k = 0; k < 3; ++k) t[k] += (double)(h[4 * r + k + 1] - h[4 * r + k]);
+        if (n > 0)
+            std::fprintf(stderr, "[foe persistent] grid %d, %d rounds: K2+barrier %.2f us, K1+barrier %.2f us, K3 %.2f us\n",
+                         st->pgrid, n, 1e-3 * t[0] / n, 1e-3 * t[1] / n, 1e-3 * t[2] / n);
+        cudaFree(st->phase_ns);
+    }
+    cudaFree(st->trace); cudaFree(st->ctl); cudaFree(st->bar);
     if (st->hctl) cudaFreeHost(st->hctl);
     for (auto e : st->ev_pool) cudaEventDestroy(e);
     for (auto& pr : st->ev_live) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
@@ -1034,13 +1122,42 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
         delete st;
         return fail(FOE_ERR_UNSUPPORTED, "no tensor-core stencil for %d filters of %dx%d", md->nf, md->m, md->m);
     }
-    const Plan pl = plan_stencil(md, B, H, W, H, cfg.stencil, cfg.filter_groups);
+    if (cfg.solver < FOE_SOLVER_AUTO || cfg.solver > FOE_SOLVER_PERSISTENT) {
+        delete st;
+        return fail(FOE_ERR_INVALID_ARGUMENT, "unknown solver %d", cfg.solver);
+    }
+    if (cfg.solver == FOE_SOLVER_PERSISTENT && cfg.stencil == FOE_STENCIL_TENSOR) {
+        delete st;
+        return fail(FOE_ERR_UNSUPPORTED, "the persistent solver runs the FFMA stencil only");
+    }
+    // trial-loop driver (f4): persistent for problems that cannot fill the GPU
+    const long long npx = (long long)B * H * W;
+    const bool want_persist = cfg.solver == FOE_SOLVER_PERSISTENT ||
+                              (cfg.solver == FOE_SOLVER_AUTO && cfg.stencil != FOE_STENCIL_TENSOR && npx <= (1LL << 18));
+    const int pref = want_persist ? FOE_STENCIL_FFMA : cfg.stencil;
+    const Plan pl = plan_stencil(md, B, H, W, H, pref, cfg.filter_groups);
     st->kind = pl.kind;
     st->tiles_x = pl.tiles_x;
     st->ntiles = pl.ntiles;
     st->nchunks = div_up(md->nf, Tr<7>::NC);
     st->groups = pl.groups;
-    st->nblk2 = div_up((long long)st->HW, (long long)kThreads * kPxt2);
+    st->pxt2 = kPxt2;
+    if (want_persist && pl.kind == FOE_STENCIL_FFMA) {
+        // K2 items: one pixel per thread while the grid can hold them all, else four
+        const int pxt = npx <= 2LL * md->nsm * kThreads ? 1 : 4;
+        const int cap = persist_capacity(md, pxt);
+        if (cap > 0) {
+            const long long items = std::max((long long)pl.ntiles * pl.groups * B,
+                                             (long long)div_up((long long)st->HW, (long long)kThreads * pxt) * B);
+            st->solver = FOE_SOLVER_PERSISTENT;
+            st->pxt2 = pxt;
+            st->pgrid = (int)std::max(1LL, std::min<long long>(cap, items));
+        } else if (cfg.solver == FOE_SOLVER_PERSISTENT) {
+            delete st;
+            return fail(FOE_ERR_UNSUPPORTED, "cooperative launch of the persistent solver is not available");
+        }
+    }
+    st->nblk2 = div_up((long long)st->HW, (long long)kThreads * st->pxt2);
     auto cleanup = [&](foe_status s) { ipiano_state_destroy(st); return s; };
 #define CKS(call)                                                                    \
     do {                                                                             \
@@ -1054,10 +1171,18 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     CKS(cudaMalloc((void**)&st->g, sizeof(float) * 2 * st->groups * n));
     CKS(cudaMalloc((void**)&st->ft, sizeof(float) * n));
     CKS(cudaMalloc((void**)&st->epart, sizeof(double) * B * st->ntiles * st->groups));
-    CKS(cudaMalloc((void**)&st->ppart, sizeof(double) * B * st->nblk2 * foe::kNumPart));
+    CKS(cudaMalloc((void**)&st->ppart, sizeof(double) * 2 * B * st->nblk2 * foe::kNumPart));
     CKS(cudaMalloc((void**)&st->trace, sizeof(double) * B * (cfg.max_iters + 1) * 8));
     CKS(cudaMemset(st->trace, 0, sizeof(double) * B * (cfg.max_iters + 1) * 8));
-    CKS(cudaMalloc((void**)&st->ctl, sizeof(ImgCtl) * B));
+    CKS(cudaMalloc((void**)&st->ctl, sizeof(ImgCtl) * B * std::max(1, st->pgrid)));
+    if (st->solver == FOE_SOLVER_PERSISTENT) {
+        CKS(cudaMalloc((void**)&st->bar, sizeof(unsigned int)));
+        const char* ph = std::getenv("FOE_PERSIST_PHASES");
+        if (ph && ph[0] == '1') {
+            CKS(cudaMalloc((void**)&st->phase_ns, sizeof(unsigned long long) * 4 * foe::kPhaseRounds));
+            CKS(cudaMemset(st->phase_ns, 0, sizeof(unsigned long long) * 4 * foe::kPhaseRounds));
+        }
+    }
     CKS(cudaMallocHost((void**)&st->hctl, sizeof(ImgCtl) * B));
     st->lam.resize(2 * (size_t)B);
     for (int b = 0; b < B; ++b) {
@@ -1114,7 +1239,9 @@ foe_status ipiano_solve(ipiano_state* st, void* stream) {
         for (int b = 0; b < st->B; ++b)
             if (st->hctl[b].active) { any = true; min_n = std::min(min_n, st->hctl[b].n); }
         if (!any || done_rounds > max_rounds) break;
-        const int rounds = std::max(1, st->cfg.max_iters - min_n);
+        const long long rounds = st->solver == FOE_SOLVER_PERSISTENT && !st->profile
+                                     ? max_rounds - done_rounds + 1
+                                     : std::max(1, st->cfg.max_iters - min_n);
         r = launch_rounds(st, rounds);
         if (r != FOE_OK) return r;
         done_rounds += rounds;
@@ -1146,7 +1273,7 @@ foe_status ipiano_step(ipiano_state* st, void* stream, int* accepted_iters_out) 
         bool any = false;
         for (int b = 0; b < st->B; ++b) any |= st->hctl[b].active != 0;
         if (!any) break;
-        r = launch_rounds(st, 1);
+        r = launch_rounds(st, st->solver == FOE_SOLVER_PERSISTENT ? max_rounds - i : 1);
         if (r != FOE_OK) return r;
         r = sync_ctl(st);
         if (r != FOE_OK) return r;
@@ -1743,6 +1870,7 @@ foe_status ipiano_slabs_create(const foe_model* md, const float* f, int H_global
     if (cfg_in) cfg = *cfg_in; else ipiano_config_default(&cfg);
     cfg.filter_groups = groups;
     cfg.stencil = pl.kind;
+    cfg.solver = FOE_SOLVER_GRAPH;   // the slab rounds are driven by ipiano_slabs_* (kPxt2 K2 blocks)
     // members: per-slab iPiano states of one image (B = 1) sharing the group's stream.
     // ipiano_state_create evaluates w^0 with periodic wrap; slab_init below redoes it with halos.
     const size_t HWs = (size_t)g->Hs * W;

@@ -203,7 +203,7 @@ k_prior_grad(const K1Args args, const __grid_constant__ TapParams tp) {
     float* ps = us + (HVP ? 2 : 1) * G::UY * G::UP;         // [NC][RY][PP] rho' (or rho'' t)
     __shared__ double red[32];
 
-    const int b = blockIdx.y;
+    const int b = blockIdx.y, bx = blockIdx.x;
     int wslot = 0, gslot = 0;
     if (args.ctl != nullptr) {
         const ImgCtl& c = args.ctl[b];
@@ -213,7 +213,7 @@ k_prior_grad(const K1Args args, const __grid_constant__ TapParams tp) {
     }
     const int H = args.H, W = args.W;
     const size_t HW = (size_t)H * W;
-    const int tile = blockIdx.x / args.groups, grp = blockIdx.x - tile * args.groups;
+    const int tile = bx / args.groups, grp = bx - tile * args.groups;
     const int ty = tile / args.tiles_x, tx = tile - ty * args.tiles_x;
     const int y0 = ty * kTile, x0 = tx * kTile;
     const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
@@ -466,9 +466,10 @@ __device__ __forceinline__ void corr_bwd2(const float2* __restrict__ in, int pit
     }
 }
 
+// one (tile x filter group, image) work item: bx = tile * groups + group, b = image (the
+// persistent solver runs several per CTA; the caller syncs the CTA between items)
 template <int M, int NCP, int SF>
-__global__ void __launch_bounds__(kThreads, 2)
-k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
+__device__ __forceinline__ void prior_grad2_item(const K1Args& args, const TapParams2& tp, const int bx, const int b) {
     using G = G2<M, NCP, SF>;
     constexpr int C = G::C;
     extern __shared__ float4 smem4[];
@@ -476,7 +477,6 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
     float2* ps = reinterpret_cast<float2*>(us + G::UY * G::UP);          // [NCP][RY][PP] (rho'_A, rho'_B)/2
     __shared__ double red[32];
 
-    const int b = blockIdx.y;
     int wslot = 0, gslot = 0;
     if (args.ctl != nullptr) {
         const ImgCtl& c = args.ctl[b];
@@ -486,7 +486,7 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
     }
     const int H = args.H, W = args.W;
     const size_t HW = (size_t)H * W;
-    const int tile = blockIdx.x / args.groups, grp = blockIdx.x - tile * args.groups;
+    const int tile = bx / args.groups, grp = bx - tile * args.groups;
     const int ty = tile / args.tiles_x, tx = tile - ty * args.tiles_x;
     const int y0 = ty * kTile, x0 = tx * kTile;
     const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
@@ -501,15 +501,34 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
     const float cst = (float)(udom ? w[(size_t)yc * W + xc] : exp(w[(size_t)yc * W + xc]));
     const double cstd = (double)cst;
     const double* halo = args.halo;
-    for (int idx = threadIdx.x; idx < G::UY * G::UX; idx += kThreads) {
-        const int uy = idx / G::UX, ux = idx - uy * G::UX;
-        const int y = y0 - 2 * C + uy, gx = wrap_idx(x0 - 2 * C + ux, W);
-        const double* src;
-        if (halo == nullptr) src = w + (size_t)wrap_idx(y, H) * W;
-        else if (y < 0) src = halo + (size_t)(kHalo + y) * W;
-        else if (y >= H) src = halo + (size_t)(kHalo + y - H) * W;
-        else src = w + (size_t)y * W;
-        us[uy * G::UP + ux] = (float)((udom ? src[gx] : exp(src[gx])) - cstd);
+    // batches of SB independent loads per thread before their exponentials, so that a CTA
+    // alone on its SM (small images, the persistent driver) does not wait one memory latency
+    // per staged pixel
+    constexpr int NST = G::UY * G::UX, SBAT = 8;
+    for (int i0 = threadIdx.x; i0 < NST; i0 += SBAT * kThreads) {
+        double v[SBAT];
+#pragma unroll
+        for (int j = 0; j < SBAT; ++j) {
+            const int idx = i0 + j * kThreads;
+            if (idx < NST) {
+                const int uy = idx / G::UX, ux = idx - uy * G::UX;
+                const int y = y0 - 2 * C + uy, gx = wrap_idx(x0 - 2 * C + ux, W);
+                const double* src;
+                if (halo == nullptr) src = w + (size_t)wrap_idx(y, H) * W;
+                else if (y < 0) src = halo + (size_t)(kHalo + y) * W;
+                else if (y >= H) src = halo + (size_t)(kHalo + y - H) * W;
+                else src = w + (size_t)y * W;
+                v[j] = src[gx];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < SBAT; ++j) {
+            const int idx = i0 + j * kThreads;
+            if (idx < NST) {
+                const int uy = idx / G::UX, ux = idx - uy * G::UX;
+                us[uy * G::UP + ux] = (float)((udom ? v[j] : exp(v[j])) - cstd);
+            }
+        }
     }
     __syncthreads();
 
@@ -604,7 +623,13 @@ k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
         }
     }
     const double e = block_sum_d(e_acc, red);
-    if (threadIdx.x == 0) args.epart[(size_t)b * args.ntiles * args.groups + blockIdx.x] = e;
+    if (threadIdx.x == 0) args.epart[(size_t)b * args.ntiles * args.groups + bx] = e;
+}
+
+template <int M, int NCP, int SF>
+__global__ void __launch_bounds__(kThreads, 2)
+k_prior_grad2(const K1Args args, const __grid_constant__ TapParams2 tp) {
+    prior_grad2_item<M, NCP, SF>(args, tp, blockIdx.x, blockIdx.y);
 }
 
 // ---------------------------------------------------------------------------------
@@ -763,10 +788,9 @@ struct K2Args {
     int idiv;              // model (6) in u: closed-form prox of (lam/2)(u^2 - 2 f^2 log u), lam = lam1
 };
 
+// pixel block bx of image b (kThreads * PXT pixels); the caller syncs the CTA between blocks
 template <int PXT>
-__global__ void __launch_bounds__(kThreads, 4)
-k_inertial_prox(const K2Args a) {  // (4 CTAs/SM: <= 64 registers; 3 -> 4 gave 253 -> 222 us, 5 spills)
-    const int b = blockIdx.y;
+__device__ __forceinline__ void inertial_prox_blk(const K2Args& a, const int bx, const int b) {
     const ImgCtl& c = a.ctl[b];
     if (!c.active) return;
     const double alpha = a.sp.safety * 2.0 * (1.0 - a.sp.beta) / c.L;
@@ -777,7 +801,7 @@ k_inertial_prox(const K2Args a) {  // (4 CTAs/SM: <= 64 registers; 3 -> 4 gave 2
     const float* g = a.g + (size_t)c.gcur * a.g_slot_stride + (size_t)b * a.HW;
     const float* ft = a.ft + (size_t)b * a.HW;
     double gd = 0, dd = 0, Gp = 0, ww = 0, wmax = 0, nit = 0, fail = 0;
-    const size_t base = (size_t)blockIdx.x * (kThreads * PXT);
+    const size_t base = (size_t)bx * (kThreads * PXT);
 #pragma unroll 2
     for (int k = 0; k < PXT; ++k) {
         const size_t p = base + (size_t)k * kThreads + threadIdx.x;
@@ -837,10 +861,16 @@ k_inertial_prox(const K2Args a) {  // (4 CTAs/SM: <= 64 registers; 3 -> 4 gave 2
         const int k = threadIdx.x;
         double t = wred[0][k];
         for (int i = 1; i < kThreads / 32; ++i) t = (k == 4 || k == 5) ? fmax(t, wred[i][k]) : t + wred[i][k];
-        double* out = a.ppart + ((size_t)b * a.nblk + blockIdx.x) * kNumPart;
+        double* out = a.ppart + ((size_t)b * a.nblk + bx) * kNumPart;
         out[k] = t;
         if (k == 0) out[7] = 0.0;
     }
+}
+
+template <int PXT>
+__global__ void __launch_bounds__(kThreads, 4)
+k_inertial_prox(const K2Args a) {  // (4 CTAs/SM: <= 64 registers; 3 -> 4 gave 253 -> 222 us, 5 spills)
+    inertial_prox_blk<PXT>(a, blockIdx.x, blockIdx.y);
 }
 
 // ---------------------------------------------------------------------------------
@@ -857,9 +887,8 @@ struct K3Args {
 
 enum { ST_OK = 0, ST_NONFINITE = 4, ST_BACKTRACK = 5, ST_PROX = 6, ST_DOMAIN = 7 };
 
-__global__ void __launch_bounds__(kThreads) k_decide(const K3Args a) {
-    __shared__ double red[32];
-    const int b = blockIdx.x;
+// the decision of image b by one CTA (trace == nullptr: not recorded by this CTA)
+__device__ __forceinline__ void decide_img(const K3Args& a, const int b) {
     ImgCtl& c = a.ctl[b];
     if (!c.active) return;
     double e = 0.0;
@@ -870,15 +899,25 @@ __global__ void __launch_bounds__(kThreads) k_decide(const K3Args a) {
         s[0] += p[0]; s[1] += p[1]; s[2] += p[2]; s[3] += p[3];
         s[4] = fmax(s[4], p[4]); s[5] = fmax(s[5], p[5]); s[6] += p[6];
     }
-    const double Fp = block_sum_d(e, red);
-    const double gd = block_sum_d(s[0], red);
-    const double dd = block_sum_d(s[1], red);
-    const double Gp = block_sum_d(s[2], red);
-    const double ww = block_sum_d(s[3], red);
-    const double wmax = block_max_d(s[4], red);
-    const double nit = block_max_d(s[5], red);
-    const double fail = block_sum_d(s[6], red);
+    // the 8 reductions in one pass (per value the order of block_sum_d / block_max_d: xor
+    // butterfly in the warp, then the warps in index order), one CTA barrier
+    double v[8] = {e, s[0], s[1], s[2], s[3], s[4], s[5], s[6]};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = (k == 5 || k == 6) ? warp_max_d(v[k]) : warp_sum_d(v[k]);
+    __shared__ double wred8[kThreads / 32][8];
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) wred8[threadIdx.x >> 5][k] = v[k];
+    __syncthreads();
     if (threadIdx.x != 0) return;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        double t = (k == 5 || k == 6) ? wred8[0][k] : 0.0 + wred8[0][k];
+        for (int i = 1; i < kThreads / 32; ++i) t = (k == 5 || k == 6) ? fmax(t, wred8[i][k]) : t + wred8[i][k];
+        v[k] = t;
+    }
+    const double Fp = v[0], gd = v[1], dd = v[2], Gp = v[3], ww = v[4], wmax = v[5], nit = v[6], fail = v[7];
     c.trials += 1;
     c.total_trials += 1;
     if (fail > 0.0) {
@@ -897,7 +936,7 @@ __global__ void __launch_bounds__(kThreads) k_decide(const K3Args a) {
         c.F = Fp;
         c.n += 1;
         const double relchg = sqrt(dd) / fmax(sqrt(ww), 1.0);
-        if (a.sp.record_trace) {
+        if (a.sp.record_trace && a.trace != nullptr) {
             double* r = a.trace + ((size_t)b * (a.sp.max_iters + 1) + c.n) * 8;
             r[0] = Fp; r[1] = Gp; r[2] = Fp + Gp; r[3] = L; r[4] = (double)c.trials;
             r[5] = margin; r[6] = nit; r[7] = relchg;
@@ -911,6 +950,8 @@ __global__ void __launch_bounds__(kThreads) k_decide(const K3Args a) {
     }
     c.active = (c.status == ST_OK && !c.done && c.n < c.target) ? 1 : 0;
 }
+
+__global__ void __launch_bounds__(kThreads) k_decide(const K3Args a) { decide_img(a, blockIdx.x); }
 
 // ---------------------------------------------------------------------------------
 // Setup / helper kernels

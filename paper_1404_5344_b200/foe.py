@@ -22,6 +22,7 @@ STATUS_NAMES = {
 }
 FOE_DATA_COMBINED, FOE_DATA_NAKAGAMI, FOE_DATA_IDIV = 0, 1, 2
 FOE_STENCIL_AUTO, FOE_STENCIL_FFMA, FOE_STENCIL_TENSOR = 0, 1, 2
+FOE_SOLVER_AUTO, FOE_SOLVER_GRAPH, FOE_SOLVER_PERSISTENT = 0, 1, 2
 TRACE_FIELDS = ("F", "G", "H", "L", "trials", "margin", "newton", "relchg")
 
 EXPORTED = (
@@ -29,7 +30,7 @@ EXPORTED = (
     "foe_energy_grad", "foe_hvp", "foe_estimate_lipschitz", "ipiano_config_default",
     "ipiano_state_create", "ipiano_state_reset", "ipiano_step", "ipiano_solve", "ipiano_get_iterate",
     "ipiano_get_counters", "ipiano_get_trace", "ipiano_profile", "ipiano_profile_read",
-    "ipiano_state_destroy", "ipiano_state_stencil", "ipiano_run",
+    "ipiano_state_destroy", "ipiano_state_stencil", "ipiano_state_solver", "ipiano_run",
     "foe_model_set_stencil", "foe_comm_unique_id", "foe_comm_create", "foe_comm_destroy", "ipiano_slabs_create", "ipiano_slabs_reset",
     "ipiano_slabs_solve", "ipiano_slabs_get_iterate", "ipiano_slabs_member", "ipiano_slabs_destroy",
     "ipiano_slabs_halo_handle", "ipiano_slabs_connect_peers", "ipiano_slabs_disconnect_peers",
@@ -50,7 +51,7 @@ class IPianoConfig(C.Structure):
         ("shrink", C.c_double), ("max_iters", C.c_int), ("max_backtracks", C.c_int),
         ("newton_max_iters", C.c_int), ("newton_tol", C.c_double), ("rel_change_tol", C.c_double),
         ("w_guard", C.c_double), ("record_trace", C.c_int), ("filter_groups", C.c_int),
-        ("stencil", C.c_int),
+        ("stencil", C.c_int), ("solver", C.c_int),
     ]
 
 
@@ -94,6 +95,8 @@ def lib():
     L.ipiano_profile_read.argtypes = [_vp, _dp, _llp, _llp]
     L.ipiano_state_stencil.argtypes = [_vp]
     L.ipiano_state_stencil.restype = C.c_int
+    L.ipiano_state_solver.argtypes = [_vp]
+    L.ipiano_state_solver.restype = C.c_int
     L.ipiano_state_destroy.argtypes = [_vp]
     L.ipiano_state_destroy.restype = None
     L.ipiano_run.argtypes = [_vp, _vp, C.c_int, C.c_int, C.c_int, _dp, _dp, C.POINTER(IPianoConfig),
@@ -401,6 +404,11 @@ def ipiano_profile_read(state: State):
 def ipiano_state_stencil(state: State) -> int:
     """FOE_STENCIL_FFMA (K1) or FOE_STENCIL_TENSOR (K8): the prior kernel this state runs."""
     return int(lib().ipiano_state_stencil(state.handle))
+
+
+def ipiano_state_solver(state: State) -> int:
+    """FOE_SOLVER_GRAPH or FOE_SOLVER_PERSISTENT: the trial-loop driver this state runs."""
+    return int(lib().ipiano_state_solver(state.handle))
 
 
 def ipiano_state_destroy(state: State):
