@@ -52,6 +52,8 @@ def parse_args():
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--images", type=int, default=0, help="images per GPU (default: the config's batch)")
     ap.add_argument("--iters", type=int, default=0, help="override iteration count (quick runs only)")
+    ap.add_argument("--stencil", choices=["auto", "ffma", "tensor"], default="auto",
+                    help="prior kernel (auto: K8 tensor cores where it fills the GPU, else K1)")
     ap.add_argument("--solver", choices=["auto", "graph", "persistent"], default="auto",
                     help="trial-loop driver (auto: persistent for single small images, SURVEY 8(f) f4)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -316,7 +318,8 @@ def main():
     del v0
 
     solver = {"auto": P.FOE_SOLVER_AUTO, "graph": P.FOE_SOLVER_GRAPH, "persistent": P.FOE_SOLVER_PERSISTENT}[args.solver]
-    cfgc = P.ipiano_config_default(max_iters=cfg.iters, record_trace=0, solver=solver)
+    stencil = {"auto": P.FOE_STENCIL_AUTO, "ffma": P.FOE_STENCIL_FFMA, "tensor": P.FOE_STENCIL_TENSOR}[args.stencil]
+    cfgc = P.ipiano_config_default(max_iters=cfg.iters, record_trace=0, solver=solver, stencil=stencil)
     st = P.ipiano_state_create(md, f_dev, d["lambdas"], L0, cfgc)
     u_dev = torch.empty((B, H, W), dtype=torch.float32, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
@@ -471,7 +474,8 @@ def run_slabs(args, cfg):
     L0 = float(L0[0])
     comm = P.foe_comm_create(D.share_bytes(P.foe_comm_unique_id() if rank == 0 else None), ws, rank, local)
     f_dev = torch.as_tensor(np.ascontiguousarray(f_full[r0:r1]), device=dev)
-    cfgc = P.ipiano_config_default(max_iters=cfg.iters, record_trace=0)
+    stencil = {"auto": P.FOE_STENCIL_AUTO, "ffma": P.FOE_STENCIL_FFMA, "tensor": P.FOE_STENCIL_TENSOR}[args.stencil]
+    cfgc = P.ipiano_config_default(max_iters=cfg.iters, record_trace=0, stencil=stencil)
     sl = P.ipiano_slabs_create(md, f_dev, Hg, lam=lam, lipschitz_init=L0, cfg=cfgc, comm=comm)
     # fused ghost-row exchange: K2 stores straight into the ring neighbours' ghost rows (CUDA IPC
     # over NVLink); the NCCL send/recv path stays if a mapping cannot be opened

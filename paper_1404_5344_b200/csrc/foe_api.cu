@@ -128,6 +128,9 @@ cudaError_t tc_set_attr() {
     e = cudaFuncSetAttribute(foe::k_prior_grad_tc4<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              tc4_smem<M, NP>());
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(foe::k_prior_grad_tc6<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             foe::Tc3Geom<M, NP, kTcR>::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(foe::k_prior_grad_tc5<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 foe::Tc5Geom<M, NP, kTcR>::SMEM_BYTES);
 }
@@ -138,6 +141,7 @@ int tc_variant() {
     const char* e = std::getenv("FOE_K8_VARIANT");   // read per launch (A/B in one process)
     if (e && e[0] == '4') return 4;
     if (e && e[0] == '5') return 5;
+    if (e && e[0] == '6') return 6;
     if (e && e[0] == 'k' && e[1] >= '1' && e[1] <= '4') return 40 + (e[1] - '0');   // profiling knockouts
     return 3;
 }
@@ -503,6 +507,11 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
         if (var == 42) foe::k_prior_grad_tc4<7, 48, kTcR, 2><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
         if (var == 43) foe::k_prior_grad_tc4<7, 48, kTcR, 3><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
         if (var == 44) foe::k_prior_grad_tc4<7, 48, kTcR, 4><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
+    } else if (var == 6) {
+        if (md->tc_np == 48)
+            foe::k_prior_grad_tc6<7, 48, kTcR><<<dim3(a.ntiles, B), 384, foe::Tc3Geom<7, 48, kTcR>::SMEM_BYTES, s>>>(ta, *md->tc_const);
+        else
+            foe::k_prior_grad_tc6<5, 32, kTcR><<<dim3(a.ntiles, B), 384, foe::Tc3Geom<5, 32, kTcR>::SMEM_BYTES, s>>>(ta, *md->tc_const);
     } else if (var == 5) {
         ta.nimg = B;
         const int items = a.ntiles * B;

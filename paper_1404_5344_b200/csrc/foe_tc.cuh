@@ -32,6 +32,12 @@
 #include "foe_kernels.cuh"
 #include "tc_ptx.cuh"
 
+// 1: K8's epilogue takes one MUFU reciprocal per filter pair (the XU pipe is K8's busiest
+// thread-work pipe); 0: one per filter
+#ifndef FOE_K8_PAIR_RCP
+#define FOE_K8_PAIR_RCP 1
+#endif
+
 namespace foe {
 
 template <int M, int NP, int R>
@@ -169,7 +175,16 @@ __device__ __forceinline__ float tc_epilogue(uint32_t t_d, uint32_t t_phi, uint3
             const float2 rv = __ffma2_rn(uq2, make_float2(css[i], css[i + 1]), r2);
             const float2 d = __ffma2_rn(rv, rv, one2);
             el2 = __ffma2_rn(make_float2(ths[i], ths[i + 1]), make_float2(lg2_approx(d.x), lg2_approx(d.y)), el2);
+#if FOE_K8_PAIR_RCP
+            // one MUFU reciprocal per filter pair: 1/d_A = d_B / (d_A d_B), 1/d_B = d_A / (d_A d_B)
+            // (d >= 1; d_A d_B overflows only for |r| > ~4e9 -- u ~ 1e9 -- where rho'/2 ~ 1/r
+            // flushes to 0; an infinite d (u past the w guard) makes the energy infinite, so the
+            // trial is rejected either way)
+            const float q = rcp_approx(d.x * d.y);
+            const float2 pv = __fmul2_rn(rv, __fmul2_rn(make_float2(d.y, d.x), make_float2(q, q)));
+#else
             const float2 pv = __fmul2_rn(rv, make_float2(rcp_approx(d.x), rcp_approx(d.y)));
+#endif
             zl2 = __ffma2_rn(pv, make_float2(kbl[i], kbl[i + 1]), zl2);
             float2 hi2, lo2;
             tc::tf32_split2(pv, hi2, lo2);
@@ -1054,6 +1069,241 @@ __global__ void __launch_bounds__(25 * 32, 1) k_prior_grad_tc5(const TcArgs ta, 
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc<512>(tb);
+}
+
+// =============================================================================================
+// K8 v6: v3's lock-step row loop with THREE warp groups (384 threads, 2 CTAs per SM = 24 warps)
+// instead of two, so that more warps hide the latencies of the per-row thread work (ncu of v3:
+// issue active 52 %, stalls on fixed-latency dependencies, MIO throttle and the two CTA
+// barriers per row).  The row phases are split three ways by compile-time tables (Tc3Part):
+// im2col tap chunks, Z tap chunks and epilogue filter chunks over all three groups, the col2im
+// rows over groups 0 and 1 (as v3), so group 2 takes a larger share of the im2col and Z
+// copies.  Shared memory as v3 minus the unused 49th Z column and the u pitch padding (the
+// third group's last-tap partial needs the room; 2 CTAs per SM must still fit).
+// =============================================================================================
+template <int M>
+struct Tc3Part;
+template <>
+struct Tc3Part<7> {   // KT 56 -> 7 im2col chunks, NB 48 -> 6 Z chunks, NP 48 -> 6 filter chunks
+    static constexpr int IM[4] = {0, 1, 3, 7};
+    static constexpr int ZC[4] = {0, 1, 2, 6};
+    static constexpr int EP[4] = {0, 2, 4, 6};
+};
+template <>
+struct Tc3Part<5> {   // KT 32 -> 4, NB 24 -> 3, NP 32 -> 4
+    static constexpr int IM[4] = {0, 1, 2, 4};
+    static constexpr int ZC[4] = {0, 1, 2, 3};
+    static constexpr int EP[4] = {0, 1, 3, 4};
+};
+
+template <int M, int NP, int R>
+struct Tc3Geom {
+    using B = TcGeom<M, NP, R>;
+    static constexpr int C = B::C, TAPS = B::TAPS, KT = B::KT, LANES = B::LANES, OW = B::OW, RR = B::RR;
+    static constexpr int UY = B::UY, UX = B::UX, UP = B::UX, NB = B::NB;
+    static constexpr int SM_B = 0;
+    static constexpr int SM_U = SM_B + B::B_FLOATS;
+    static constexpr int SM_Z = SM_U + UY * UP;
+    static constexpr int SM_HAND = SM_Z + NB * LANES;
+    static constexpr int SM_ZL = SM_HAND + 8 * LANES;     // [2 rows][3 groups][LANES]
+    static constexpr int SM_FLOATS = SM_ZL + 6 * LANES;
+    static constexpr int SMEM_BYTES = SM_FLOATS * 4 + 64;
+    static_assert(2 * (SMEM_BYTES + 1024) <= 228 * 1024, "two CTAs per SM");
+};
+
+template <int M, int NP, int R>
+__global__ void __launch_bounds__(384, 2) k_prior_grad_tc6(const TcArgs ta, const __grid_constant__ TcConst cc) {
+    using G = Tc3Geom<M, NP, R>;
+    using GB = TcGeom<M, NP, R>;
+    using PT = Tc3Part<M>;
+    constexpr int C = G::C, L = G::LANES;
+    extern __shared__ __align__(128) float sm[];
+    float* bsm = sm + G::SM_B;
+    float* us = sm + G::SM_U;
+    float* zs = sm + G::SM_Z;
+    __shared__ uint32_t tbase_s;
+    __shared__ __align__(8) uint64_t mbar_f, mbar_b;
+    __shared__ double red[32];
+
+    const K1Args& args = ta.k;
+    const int b = blockIdx.y;
+    int wslot = 0, gslot = 0;
+    if (args.ctl != nullptr) {
+        const ImgCtl& c = args.ctl[b];
+        if (!c.active) return;
+        wslot = args.which_cur ? c.cur : c.cand;
+        gslot = args.which_cur ? c.gcur : c.gcand;
+    }
+    const int H = args.H, W = args.W;
+    const size_t HW = (size_t)H * W;
+    const int tile = blockIdx.x;
+    const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
+    const int y0 = ty * R, x0 = tx * G::OW;
+    const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
+    const int t = threadIdx.x, warp = __shfl_sync(0xffffffffu, t >> 5, 0);
+    const int wg = warp >> 2;                                   // warp group (0, 1, 2)
+    const int l = (warp & 3) * 32 + (t & 31);                   // TMEM lane = response pixel
+
+    if (warp == 0) tc::tmem_alloc<GB::TCOLS>(&tbase_s);
+    if (t == 0) {
+        tc::mbar_init(&mbar_f, 1);
+        tc::mbar_init(&mbar_b, 1);
+        tc::mbar_fence_init();
+    }
+    {
+        const float4* src = reinterpret_cast<const float4*>(ta.bimg);
+        float4* dst = reinterpret_cast<float4*>(bsm);
+#pragma unroll 4
+        for (int i = t; i < GB::B_FLOATS / 4; i += 384) dst[i] = __ldg(src + i);
+    }
+    const int yc = min(y0 + R / 2, H - 1), xc = min(x0 + G::OW / 2, W - 1);
+    const bool udom = args.udom != 0;
+    const double wc = w[(size_t)yc * W + xc];
+    const float cst = (float)(udom ? wc : exp(wc));
+    tc_stage_u<G::UY, G::UX, G::UP, 12>(us, w, args.halo, H, W, y0, x0, 2 * C, udom, cst, wc, warp, t & 31);
+    tc::fence_proxy_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tb = tbase_s;
+    const uint32_t tl = tb + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t idf = tc::idesc_tf32(128, NP);
+    const uint32_t idb = tc::idesc_tf32(128, G::NB);
+    const uint32_t b_base = tc::smem_u32(bsm);
+
+    const int lx = x0 - C + l;
+    const bool col_own = (l >= C) && (l < C + G::OW) && (lx < W);
+    const bool out_col = (l < G::OW) && (x0 + l < W);
+
+    double e_acc = 0.0;
+    constexpr int NC8 = G::KT / 8, NF8 = NP / 8;
+    constexpr int A0 = C + 1, A1 = M - A0;                 // col2im rows: wg0 a < A0, wg1 a >= A0
+    float acc[A0 > A1 ? A0 : A1];
+#pragma unroll
+    for (int k = 0; k < (A0 > A1 ? A0 : A1); ++k) acc[k] = 0.f;
+    float* gout = args.g + (size_t)gslot * args.g_slot_stride + (size_t)b * HW;
+    float* hand = sm + G::SM_HAND;
+    float* zls = sm + G::SM_ZL;
+
+#pragma unroll 1
+    for (int j = 0; j <= G::RR; ++j) {
+        float uq = 0.f;
+        if (j < G::RR) {
+            const float* up = us + j * G::UP + l;
+            const float vc = up[C * G::UP + C];
+            uq = vc + cst;
+            if (wg == 0) tc_im2col<M, G::UP, PT::IM[0], PT::IM[1]>(up, vc, tl + GB::COL_AHI, tl + GB::COL_ALO);
+            else if (wg == 1) tc_im2col<M, G::UP, PT::IM[1], PT::IM[2]>(up, vc, tl + GB::COL_AHI, tl + GB::COL_ALO);
+            else tc_im2col<M, G::UP, PT::IM[2], PT::IM[3]>(up, vc, tl + GB::COL_AHI, tl + GB::COL_ALO);
+        }
+        if (j > 0) {
+            tc::mbar_wait(&mbar_b, (uint32_t)((j - 1) & 1));
+            tc::fence_after_sync();
+            if (wg == 0) tc_z_to_smem<L, PT::ZC[0], PT::ZC[1]>(tl + GB::COL_Z, zs, l);
+            else if (wg == 1) tc_z_to_smem<L, PT::ZC[1], PT::ZC[2]>(tl + GB::COL_Z, zs, l);
+            else tc_z_to_smem<L, PT::ZC[2], PT::ZC[3]>(tl + GB::COL_Z, zs, l);
+        }
+        tc::wait_st();
+        tc::fence_before_sync();
+        __syncthreads();
+        if (warp == 0 && j < G::RR) {
+            tc::fence_after_sync();
+#pragma unroll
+            for (int s = 0; s < NC8; ++s) {
+                const uint32_t off = (uint32_t)(s * 2 * NP * 16);
+                const uint64_t bh = tc::sdesc_kmajor(b_base + off, NP * 16, 128);
+                const uint64_t bl = tc::sdesc_kmajor(b_base + GB::BF_FLOATS * 4 + off, NP * 16, 128);
+                tc::mma_tf32_ts_warp(tb + GB::COL_D, tb + GB::COL_AHI + s * 8, bl, idf, s > 0);
+                tc::mma_tf32_ts_warp(tb + GB::COL_D, tb + GB::COL_ALO + s * 8, bh, idf, 1);
+            }
+#pragma unroll
+            for (int s = 0; s < NC8; ++s) {
+                const uint32_t off = (uint32_t)(s * 2 * NP * 16);
+                const uint64_t bh = tc::sdesc_kmajor(b_base + off, NP * 16, 128);
+                tc::mma_tf32_ts_warp(tb + GB::COL_D, tb + GB::COL_AHI + s * 8, bh, idf, 1);
+            }
+            tc::mma_commit_warp(&mbar_f);
+        }
+        if (j > 0 && wg < 2) {
+            const int jz = j - 1;
+            if (wg == 0) {
+#pragma unroll
+                for (int a = 0; a < A0; ++a) {
+                    float sa = 0.f;
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) sa += zs[(a * M + bb) * L + l + bb];
+                    acc[a] += sa;
+                }
+                const int o = jz - (A0 - 1);
+                if (o >= 0) hand[(o & 7) * L + l] = acc[A0 - 1];
+#pragma unroll
+                for (int k = A0 - 1; k > 0; --k) acc[k] = acc[k - 1];
+                acc[0] = 0.f;
+            } else {
+                const float* zl = zls + (jz & 1) * 3 * L;
+#pragma unroll
+                for (int k = 0; k < A1; ++k) {
+                    const int a = A0 + k;
+                    float sa = 0.f;
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) {
+                        const int tap = a * M + bb;
+                        sa += tap < G::NB ? zs[tap * L + l + bb] : (zl[l + bb] + zl[L + l + bb]) + zl[2 * L + l + bb];
+                    }
+                    acc[k] += sa;
+                }
+                const int o = jz - 2 * C;
+                if (o >= 0 && o < R && out_col && y0 + o < H) {
+                    const float s_tot = acc[A1 - 1] + hand[(o & 7) * L + l];
+                    const float u = udom ? 1.0f : us[(o + 2 * C) * G::UP + l + 2 * C] + cst;
+                    gout[(size_t)(y0 + o) * W + x0 + l] = u * s_tot;
+                }
+#pragma unroll
+                for (int k = A1 - 1; k > 0; --k) acc[k] = acc[k - 1];
+                acc[0] = 0.f;
+            }
+        }
+        if (j < G::RR) {
+            tc::mbar_wait(&mbar_f, (uint32_t)(j & 1));
+            tc::fence_after_sync();
+            const bool own = col_own && (j >= C) && (j < C + R) && (y0 - C + j < H);
+            float zl;
+            const float el = wg == 0
+                ? tc_epilogue<PT::EP[0], PT::EP[1]>(tl + GB::COL_D, tl + GB::COL_PHI, tl + GB::COL_PLO, uq, cc.sumk, cc.thl, cc.kbl, zl)
+                : wg == 1
+                ? tc_epilogue<PT::EP[1], PT::EP[2]>(tl + GB::COL_D, tl + GB::COL_PHI, tl + GB::COL_PLO, uq, cc.sumk, cc.thl, cc.kbl, zl)
+                : tc_epilogue<PT::EP[2], PT::EP[3]>(tl + GB::COL_D, tl + GB::COL_PHI, tl + GB::COL_PLO, uq, cc.sumk, cc.thl, cc.kbl, zl);
+            zls[(j & 1) * 3 * L + wg * L + l] = zl;
+            if (own) e_acc += (double)el;
+            tc::wait_st();
+            tc::fence_before_sync();
+            __syncthreads();
+            if (warp == 0) {
+                tc::fence_after_sync();
+#pragma unroll
+                for (int s = 0; s < NF8; ++s) {
+                    const uint32_t off = (uint32_t)(s * 2 * G::NB * 16);
+                    const uint64_t bh = tc::sdesc_kmajor(b_base + 2 * GB::BF_FLOATS * 4 + off, G::NB * 16, 128);
+                    const uint64_t bl = tc::sdesc_kmajor(b_base + (2 * GB::BF_FLOATS + GB::BB_FLOATS) * 4 + off,
+                                                         G::NB * 16, 128);
+                    tc::mma_tf32_ts_warp(tb + GB::COL_Z, tb + GB::COL_PHI + s * 8, bl, idb, s > 0);
+                    tc::mma_tf32_ts_warp(tb + GB::COL_Z, tb + GB::COL_PLO + s * 8, bh, idb, 1);
+                }
+#pragma unroll
+                for (int s = 0; s < NF8; ++s) {
+                    const uint32_t off = (uint32_t)(s * 2 * G::NB * 16);
+                    const uint64_t bh = tc::sdesc_kmajor(b_base + 2 * GB::BF_FLOATS * 4 + off, G::NB * 16, 128);
+                    tc::mma_tf32_ts_warp(tb + GB::COL_Z, tb + GB::COL_PHI + s * 8, bh, idb, 1);
+                }
+                tc::mma_commit_warp(&mbar_b);
+            }
+        }
+    }
+    const double e = block_sum_d(e_acc, red);
+    if (t == 0) args.epart[(size_t)b * args.ntiles * args.groups + blockIdx.x] = e;
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<GB::TCOLS>(tb);
 }
 
 }  // namespace foe
