@@ -32,6 +32,7 @@ namespace {
 thread_local std::string g_err;
 std::atomic<long long> g_launches{0};  // kernels launched by this library (process-wide)
 thread_local bool t_capturing = false;   // graph capture: replays are counted instead
+thread_local bool t_slab_member = false; // ipiano_slabs_create is creating its member states
 inline void count_launch(long long n) {
     if (!t_capturing) g_launches.fetch_add(n, std::memory_order_relaxed);
 }
@@ -192,6 +193,7 @@ struct ipiano_state {
     int tiles_x = 0, ntiles = 0, groups = 1, nchunks = 0, nblk2 = 0;
     int pxt2 = 8;                 // pixels per thread of K2 (nblk2 = HW / (kThreads pxt2) blocks)
     int kind = FOE_STENCIL_FFMA;  // resolved stencil of this state (K1 or K8)
+    int tc_rem = 0, tc_spt = 0;   // K8 column packing of this state's plan
     int solver = FOE_SOLVER_GRAPH;  // resolved trial-loop driver
     int pgrid = 0;                // persistent driver: co-resident CTAs
     unsigned int* bar = nullptr;  // persistent driver: grid barrier counter
@@ -455,8 +457,10 @@ int choose_groups(const foe_model* md, int ntiles, int B, int requested) {
 struct Plan {
     int kind = FOE_STENCIL_FFMA;
     int tiles_x = 0, ntiles = 0, groups = 1;
+    int tc_rem = 0, tc_spt = 0;   // K8 column packing (K1Args::tc_rem / tc_spt)
 };
-Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref, int req_groups) {
+Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref, int req_groups,
+                  bool allow_pack = true) {
     Plan p;
     const int ow = 128 - (md->m - 1);
     bool tc = md->tc_np != 0 && pref != FOE_STENCIL_FFMA;
@@ -464,8 +468,19 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
         tc = (long long)div_up(W, ow) * div_up(H_grid, kTcR) * B >= 2LL * md->nsm;
     if (tc) {
         p.kind = FOE_STENCIL_TENSOR;
-        p.tiles_x = div_up(W, ow);
-        p.ntiles = p.tiles_x * div_up(H, kTcR);
+        // full tiles of ow columns per 64-row band; the remainder columns of several bands share
+        // one packed tile (default schedule, not for row slabs, whose energy partials are per band)
+        int nfull = W / ow, rem = W - nfull * ow, spt = 0;
+        if (rem > 0 && allow_pack && H_grid == H && tc_variant() == 3) {
+            spt = 128 / (rem + 2 * (md->m - 1));
+            if (spt < 2) spt = 0;
+        }
+        if (rem > 0 && spt == 0) { nfull += 1; rem = 0; }
+        const int nbands = div_up(H, kTcR);
+        p.tiles_x = nfull;
+        p.ntiles = nbands * nfull + (rem > 0 ? div_up(nbands, spt) : 0);
+        p.tc_rem = rem;
+        p.tc_spt = spt;
         p.groups = 1;
     } else {
         p.kind = FOE_STENCIL_FFMA;
@@ -492,7 +507,7 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
     ta.tiles_x = a.tiles_x;
     count_launch(1);
     constexpr int T4 = foe::Tc4Geom<7, 48, kTcR>::THREADS;
-    const int var = tc_variant();
+    const int var = a.tc_rem > 0 ? 3 : tc_variant();   // packed tiles: the default schedule only
     if (var >= 41 && md->tc_np == 48) {   // profiling knockouts (FOE_K8_VARIANT=k1..k4), results invalid
         static bool attr = false;
         if (!attr) {
@@ -564,7 +579,8 @@ bool is_device_ptr(const void* p) {
 // the gradient planes gparts[groups][B][HW].
 foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int W, int groups,
                         double* epart, float* gparts, bool hvp, const double* v, const float* gw,
-                        cudaStream_t s, int kind = FOE_STENCIL_FFMA, int tiles_x_tc = 0, int ntiles_tc = 0) {
+                        cudaStream_t s, int kind = FOE_STENCIL_FFMA, int tiles_x_tc = 0, int ntiles_tc = 0,
+                        int tc_rem = 0, int tc_spt = 0) {
     K1Args a{};
     a.w = w;
     a.w_slot_stride = 0;
@@ -589,6 +605,8 @@ foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int 
             a.tiles_x = tiles_x_tc;
             a.ntiles = ntiles_tc;
             a.groups = 1;
+            a.tc_rem = tc_rem;
+            a.tc_spt = tc_spt;
         }
         return launch_prior(md, kind, a, B, s);
     }
@@ -626,7 +644,7 @@ foe_status foe_energy_grad(const foe_model* md, const double* w, const float* f,
     if (!direct) CK(cudaMallocAsync((void**)&gparts, sizeof(float) * groups * B * HW, s));
     CK(cudaMallocAsync((void**)&dred, sizeof(double) * B * 2, s));
     st = run_k1_plain(md, w, B, H, W, groups, epart, direct ? grad : gparts, false, nullptr, nullptr, s, pl.kind,
-                      pl.tiles_x, pl.ntiles);
+                      pl.tiles_x, pl.ntiles, pl.tc_rem, pl.tc_spt);
     if (st != FOE_OK) return st;
     if (grad && !direct) {
         const size_t n = (size_t)B * HW;
@@ -804,6 +822,8 @@ K1Args state_k1_args(const ipiano_state* st, int which_cur) {
     a.nf = st->model->nf;
     a.nchunks = st->nchunks;
     a.udom = st->model->term == FOE_DATA_IDIV;
+    a.tc_rem = st->tc_rem;
+    a.tc_spt = st->tc_spt;
     return a;
 }
 
@@ -1144,9 +1164,11 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     const bool want_persist = cfg.solver == FOE_SOLVER_PERSISTENT ||
                               (cfg.solver == FOE_SOLVER_AUTO && cfg.stencil != FOE_STENCIL_TENSOR && npx <= (1LL << 18));
     const int pref = want_persist ? FOE_STENCIL_FFMA : cfg.stencil;
-    const Plan pl = plan_stencil(md, B, H, W, H, pref, cfg.filter_groups);
+    const Plan pl = plan_stencil(md, B, H, W, H, pref, cfg.filter_groups, !t_slab_member);
     st->kind = pl.kind;
     st->tiles_x = pl.tiles_x;
+    st->tc_rem = pl.tc_rem;
+    st->tc_spt = pl.tc_spt;
     st->ntiles = pl.ntiles;
     st->nchunks = div_up(md->nf, Tr<7>::NC);
     st->groups = pl.groups;
@@ -1861,7 +1883,8 @@ foe_status ipiano_slabs_create(const foe_model* md, const float* f, int H_global
         return fail(FOE_ERR_UNSUPPORTED, "no tensor-core stencil for %d filters of %dx%d", md->nf, md->m, md->m);
     }
     // one plan for the whole scene, so that every slab (and every slab count) runs the same kernel
-    const Plan pl = plan_stencil(md, 1, H_global / nslabs, W, H_global, pref, cfg_in ? cfg_in->filter_groups : 0);
+    const Plan pl = plan_stencil(md, 1, H_global / nslabs, W, H_global, pref, cfg_in ? cfg_in->filter_groups : 0,
+                                 /*allow_pack=*/false);
     const int groups = pl.groups;
     g->nb_local = g->Hs / foe::kBandRows;
     g->nb_global = H_global / foe::kBandRows;
@@ -1885,8 +1908,10 @@ foe_status ipiano_slabs_create(const foe_model* md, const float* f, int H_global
     const size_t HWs = (size_t)g->Hs * W;
     for (int j = 0; j < nmem; ++j) {
         ipiano_state* st = nullptr;
+        t_slab_member = true;   // per-band energy partials: no K8 column packing
         foe_status r = ipiano_state_create(md, f + (size_t)j * HWs, 1, g->Hs, W, lambda, &lipschitz_init, &cfg,
                                            stream, &st);
+        t_slab_member = false;
         if (r != FOE_OK) return cleanup(r);
         cudaStreamSynchronize(st->s);
         cudaStreamDestroy(st->s);

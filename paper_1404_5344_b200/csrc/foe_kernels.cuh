@@ -78,6 +78,10 @@ struct K1Args {
     // Data model of the iterate: 0 = w-domain (models (8)/(10): u = e^w, grad_w F = u (.) s),
     // 1 = u-domain (model (6): the iterate is u, grad_u F = s)
     int udom;
+    // K8 column packing (0 = none): each 64-row band has tiles_x full tiles of 128 - 2C output
+    // columns; the last tc_rem columns of tc_spt consecutive bands share one tile (strips of
+    // tc_rem + 4C lanes), instead of one mostly idle tile per band
+    int tc_rem, tc_spt;
     // HVP only
     const double* v;        // [B][H][W]
     const float* gw;        // [B][H][W] gradient at w
@@ -788,6 +792,71 @@ struct K2Args {
     int idiv;              // model (6) in u: closed-form prox of (lam/2)(u^2 - 2 f^2 log u), lam = lam1
 };
 
+// Test partials of one trial (a10): <g, D>, ||D||^2, G(w+), ||w||^2, max |w+| (or the domain
+// flag of model (6)), max Newton iterations, prox failures.
+struct K2Acc {
+    double gd = 0, dd = 0, Gp = 0, ww = 0, wmax = 0, nit = 0, fail = 0;
+};
+
+// One pixel of K2 (a8-a10): inertial point, prox, and its contribution to the test partials.
+// Shared by k_inertial_prox and the fused K8 trial kernel; the inertial point is written with
+// explicit roundings so that both compile to the same arithmetic (bitwise-equal w+).
+__device__ __forceinline__ double k2_pixel(double wv, double wpv, double gv, double f, double alpha, double beta,
+                                           double l1, double l2, const SolverParams& sp, int idiv, K2Acc& acc) {
+    const double what = __fma_rn(beta, __dsub_rn(wv, wpv), __fma_rn(-alpha, gv, wv));
+    double z, em, ep;
+    int it;
+    if (idiv) {
+        // u = (u^ + sqrt(u^2 + 4 (1 + tau lam) tau lam f^2)) / (2 (1 + tau lam))
+        const double tl = alpha * l1;
+        z = (what + sqrt(fma(what, what, 4.0 * (1.0 + tl) * tl * f * f))) / (2.0 * (1.0 + tl));
+        em = 0.0; ep = 0.0; it = 0;
+    } else {
+        it = prox_newton(what, f, alpha, l1, l2, sp.newton_tol, sp.newton_cap, z, em, ep);
+    }
+    const double d = z - wv;
+    acc.gd += gv * d;
+    acc.dd += d * d;
+    const double f2 = f * f;
+    if (idiv) {
+        acc.Gp += 0.5 * l1 * (z * z - 2.0 * f2 * log(z));                 // Eq.(5)
+        acc.wmax = fmax(acc.wmax, z > 0.0 ? 0.0 : INFINITY);              // the iterate must stay > 0
+    } else {
+        acc.Gp += 0.5 * l1 * (2.0 * z + f2 * em) + 0.5 * l2 * (ep - 2.0 * f2 * z);
+        acc.wmax = fmax(acc.wmax, fabs(z));
+    }
+    acc.ww += wv * wv;
+    if (it < 0) acc.fail += 1.0; else acc.nit = fmax(acc.nit, (double)it);
+    if (!(z == z)) acc.wmax = INFINITY;
+    return z;
+}
+
+// fixed-order CTA reduction of the 7 test partials (sums; slots 4 and 5 max) -> out[0..7]
+// (out[7] = 0); every thread of the CTA calls it
+__device__ __forceinline__ void k2_block_partials(const K2Acc& acc, double* out) {
+    double v[7] = {acc.gd, acc.dd, acc.Gp, acc.ww, acc.wmax, acc.nit, acc.fail};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+            const double t = __shfl_xor_sync(0xffffffffu, v[k], o);
+            v[k] = (k == 4 || k == 5) ? fmax(v[k], t) : v[k] + t;
+        }
+    __shared__ double wred[32][8];
+    const int nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int k = 0; k < 7; ++k) wred[threadIdx.x >> 5][k] = v[k];
+    __syncthreads();
+    if (threadIdx.x < 7) {
+        const int k = threadIdx.x;
+        double t = wred[0][k];
+        for (int i = 1; i < nw; ++i) t = (k == 4 || k == 5) ? fmax(t, wred[i][k]) : t + wred[i][k];
+        out[k] = t;
+        if (k == 0) out[7] = 0.0;
+    }
+}
+
 // pixel block bx of image b (kThreads * PXT pixels); the caller syncs the CTA between blocks
 template <int PXT>
 __device__ __forceinline__ void inertial_prox_blk(const K2Args& a, const int bx, const int b) {
@@ -800,7 +869,7 @@ __device__ __forceinline__ void inertial_prox_blk(const K2Args& a, const int bx,
     double* wn = a.w + (size_t)c.cand * a.w_slot_stride + (size_t)b * a.HW;
     const float* g = a.g + (size_t)c.gcur * a.g_slot_stride + (size_t)b * a.HW;
     const float* ft = a.ft + (size_t)b * a.HW;
-    double gd = 0, dd = 0, Gp = 0, ww = 0, wmax = 0, nit = 0, fail = 0;
+    K2Acc acc;
     const size_t base = (size_t)bx * (kThreads * PXT);
 #pragma unroll 2
     for (int k = 0; k < PXT; ++k) {
@@ -808,63 +877,15 @@ __device__ __forceinline__ void inertial_prox_blk(const K2Args& a, const int bx,
         if (p >= a.HW) break;
         float gs = g[p];
         for (int q = 1; q < a.groups; ++q) gs += g[(size_t)q * a.g_group_stride + p];
-        const double gv = (double)gs;
-        const double wv = w[p];
-        const double what = wv - alpha * gv + beta * (wv - wp[p]);
-        const double f = (double)ft[p];
-        double z, em, ep;
-        int it;
-        if (a.idiv) {
-            // u = (u^ + sqrt(u^2 + 4 (1 + tau lam) tau lam f^2)) / (2 (1 + tau lam))
-            const double tl = alpha * l1;
-            z = (what + sqrt(fma(what, what, 4.0 * (1.0 + tl) * tl * f * f))) / (2.0 * (1.0 + tl));
-            em = 0.0; ep = 0.0; it = 0;
-        } else {
-            it = prox_newton(what, f, alpha, l1, l2, a.sp.newton_tol, a.sp.newton_cap, z, em, ep);
-        }
+        const double z = k2_pixel(w[p], wp[p], (double)gs, (double)ft[p], alpha, beta, l1, l2, a.sp, a.idiv, acc);
         wn[p] = z;
         if (a.halo_up != nullptr) {
             if (p < a.halo_px) a.halo_up[p] = z;
             else if (p >= a.HW - a.halo_px) a.halo_dn[p - (a.HW - a.halo_px)] = z;
         }
-        const double d = z - wv;
-        gd += gv * d;
-        dd += d * d;
-        const double f2 = f * f;
-        if (a.idiv) {
-            Gp += 0.5 * l1 * (z * z - 2.0 * f2 * log(z));                 // Eq.(5)
-            wmax = fmax(wmax, z > 0.0 ? 0.0 : INFINITY);                  // the iterate must stay > 0
-        } else {
-            Gp += 0.5 * l1 * (2.0 * z + f2 * em) + 0.5 * l2 * (ep - 2.0 * f2 * z);
-            wmax = fmax(wmax, fabs(z));
-        }
-        ww += wv * wv;
-        if (it < 0) fail += 1.0; else nit = fmax(nit, (double)it);
-        if (!(z == z)) wmax = INFINITY;
     }
     if (a.halo_sys_fence) __threadfence_system();
-    // one fixed-order block reduction of the 7 partials (sums, except slots 4/5 = max)
-    double v[7] = {gd, dd, Gp, ww, wmax, nit, fail};
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-        for (int k = 0; k < 7; ++k) {
-            const double t = __shfl_xor_sync(0xffffffffu, v[k], o);
-            v[k] = (k == 4 || k == 5) ? fmax(v[k], t) : v[k] + t;
-        }
-    __shared__ double wred[kThreads / 32][8];
-    if ((threadIdx.x & 31) == 0)
-#pragma unroll
-        for (int k = 0; k < 7; ++k) wred[threadIdx.x >> 5][k] = v[k];
-    __syncthreads();
-    if (threadIdx.x < 7) {
-        const int k = threadIdx.x;
-        double t = wred[0][k];
-        for (int i = 1; i < kThreads / 32; ++i) t = (k == 4 || k == 5) ? fmax(t, wred[i][k]) : t + wred[i][k];
-        double* out = a.ppart + ((size_t)b * a.nblk + bx) * kNumPart;
-        out[k] = t;
-        if (k == 0) out[7] = 0.0;
-    }
+    k2_block_partials(acc, a.ppart + ((size_t)b * a.nblk + bx) * kNumPart);
 }
 
 template <int PXT>

@@ -128,6 +128,35 @@ __device__ __forceinline__ void tc_stage_u(float* us, const double* w, const dou
     }
 }
 
+// u tile staging of a PACKED tile: strip s (lanes [s SP, s SP + SP), SP = rem + 4C) holds the
+// last rem output columns (x0r ..) of band band0 + s; columns past the strips and strips past
+// the last band are filled with c (u - c = 0)
+template <int UY, int UX, int UP, int NWARPS>
+__device__ __forceinline__ void tc_stage_u_packed(float* us, const double* w, int H, int W, int R, int x0r, int c2,
+                                                  int SP, int spt, int band0, int nbands, bool udom, float cst,
+                                                  double wc, int warp, int lane) {
+    constexpr int NX = (UX + 31) / 32;
+    int gx[NX], yb[NX];
+    bool ok[NX];
+#pragma unroll
+    for (int k = 0; k < NX; ++k) {
+        const int ux = lane + 32 * k, st = ux / SP, band = band0 + st;
+        ok[k] = ux < UX && st < spt && band < nbands;
+        gx[k] = wrap_idx(x0r - c2 + (ux - st * SP), W);
+        yb[k] = band * R - c2;
+    }
+    for (int uy = warp; uy < UY; uy += NWARPS) {
+        double v[NX];
+#pragma unroll
+        for (int k = 0; k < NX; ++k) v[k] = ok[k] ? w[(size_t)wrap_idx(yb[k] + uy, H) * W + gx[k]] : wc;
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            const int ux = lane + 32 * k;
+            if (ux < UX) us[uy * UP + ux] = udom ? (float)(v[k] - (double)cst) : cst * expm1f((float)(v[k] - wc));
+        }
+    }
+}
+
 // ---- per-row thread work of K8, on compile-time chunk ranges (one call per warp group) ------
 // im2col chunks [C0, C1) of 8 taps: U = u(window) - u_q split into tf32 hi / lo, to TMEM
 template <int M, int UP, int C0, int C1>
@@ -234,14 +263,31 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
     const int H = args.H, W = args.W;
     const size_t HW = (size_t)H * W;
     const int tile = blockIdx.x;
-    const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
-    const int y0 = ty * R, x0 = tx * G::OW;
     const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
     // warp index broadcast from lane 0: provably warp-uniform, so TMEM addresses and the warp
     // group branch stay in uniform registers (no per-op R2UR / collective fix-up code)
     const int t = threadIdx.x, warp = __shfl_sync(0xffffffffu, t >> 5, 0);
     const int wg = warp >> 2;                                   // warp group (0, 1)
     const int l = (warp & 3) * 32 + (t & 31);                   // TMEM lane = response pixel
+    // tile geometry: a full tile (band ty, columns x0 ..), or a packed tile whose lane strips
+    // carry the remainder columns of several bands (args.tc_rem > 0).  Per lane: its strip's
+    // band origin sy0, its column ocol inside the strip / tile, and whether the strip exists.
+    const int nbands = (H + R - 1) / R;
+    const int nnorm = nbands * ta.tiles_x;
+    const bool packed = tile >= nnorm;
+    int y0, x0, sy0, ocol;
+    bool svalid = true;
+    const int SP = args.tc_rem + 4 * C;                         // strip pitch in lanes (packed)
+    if (!packed) {
+        const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
+        y0 = ty * R; x0 = tx * G::OW; sy0 = y0; ocol = l;
+    } else {
+        const int band0 = (tile - nnorm) * args.tc_spt;
+        const int st = l / SP;
+        ocol = l - st * SP;
+        svalid = st < args.tc_spt && band0 + st < nbands;
+        y0 = band0 * R; x0 = ta.tiles_x * G::OW; sy0 = (band0 + st) * R;
+    }
 
     // ---- prologue: TMEM, mbarrier, B images, u tile ------------------------------------
     if (warp == 0) tc::tmem_alloc<G::TCOLS>(&tbase_s);
@@ -256,7 +302,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
 #pragma unroll 4
         for (int i = t; i < G::B_FLOATS / 4; i += 256) dst[i] = __ldg(src + i);
     }
-    const int yc = min(y0 + R / 2, H - 1), xc = min(x0 + G::OW / 2, W - 1);
+    const int yc = min(y0 + R / 2, H - 1), xc = min(x0 + (packed ? args.tc_rem : G::OW) / 2, W - 1);
     // u - c = c (e^{w - w_c} - 1) with c = e^{w_c} at a pixel of the tile: one fp64 exp per CTA,
     // then fp32 expm1 of the small fp64 difference -- accurate relative to u - c (what the
     // stencil needs), and far cheaper than K1's fp64 exp per staged pixel
@@ -268,7 +314,9 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
         ths[t] = __ldg(ta.theta_ln2 + t);
     }
     const double* halo = args.halo;
-    tc_stage_u<G::UY, G::UX, G::UP, 8>(us, w, halo, H, W, y0, x0, 2 * C, udom, cst, wc, warp, t & 31);
+    if (!packed) tc_stage_u<G::UY, G::UX, G::UP, 8>(us, w, halo, H, W, y0, x0, 2 * C, udom, cst, wc, warp, t & 31);
+    else tc_stage_u_packed<G::UY, G::UX, G::UP, 8>(us, w, H, W, R, x0, 2 * C, SP, args.tc_spt, y0 / R, nbands, udom,
+                                                   cst, wc, warp, t & 31);
     tc::fence_proxy_async_smem();
     tc::fence_before_sync();
     __syncthreads();
@@ -281,9 +329,9 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
     const float* kbl = bsm + 2 * G::BF_FLOATS + 2 * G::BB_FLOATS;   // last tap of Kb
 
     // energy ownership of this lane's response column, output column of this thread
-    const int lx = x0 - C + l;                                  // image column of response lane l
-    const bool col_own = (l >= C) && (l < C + G::OW) && (lx < W);
-    const bool out_col = (l < G::OW) && (x0 + l < W);           // output column l of the tile
+    const int ow = packed ? args.tc_rem : G::OW;                // output columns of this lane's strip
+    const bool col_own = svalid && (ocol >= C) && (ocol < C + ow) && (x0 - C + ocol < W);
+    const bool out_col = svalid && (ocol < ow) && (x0 + ocol < W);   // output column ocol of the strip
 
     double e_acc = 0.0;
     // Two warp groups share every row: wg 0 takes the first half of the tap chunks (im2col,
@@ -377,10 +425,10 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
                 }
                 // (a6) row o = jz - 2C is complete: g = u (.) s
                 const int o = jz - 2 * C;
-                if (o >= 0 && o < R && out_col && y0 + o < H) {
+                if (o >= 0 && o < R && out_col && sy0 + o < H) {
                     const float s_tot = acc[A1 - 1] + hand[(o & 7) * L + l];
                     const float u = udom ? 1.0f : us[(o + 2 * C) * G::UP + l + 2 * C] + cst;   // W = diag(e^w)
-                    gout[(size_t)(y0 + o) * W + x0 + l] = u * s_tot;
+                    gout[(size_t)(sy0 + o) * W + x0 + ocol] = u * s_tot;
                 }
 #pragma unroll
                 for (int k = A1 - 1; k > 0; --k) acc[k] = acc[k - 1];
@@ -391,7 +439,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
             tc::mbar_wait(&mbar_f, (uint32_t)(j & 1));
             tc::fence_after_sync();
             // (a4, a7) responses r = R + u_q sum k, rho (owned responses), rho'/2 -> P (hi/lo)
-            const bool own = col_own && (j >= C) && (j < C + R) && (y0 - C + j < H);
+            const bool own = col_own && (j >= C) && (j < C + R) && (sy0 - C + j < H);
             float zl;
             const float el = wg == 0
                 ? tc_epilogue<0, HF8>(tl + G::COL_D, tl + G::COL_PHI, tl + G::COL_PLO, uq, cc.sumk, cc.thl, cc.kbl, zl)

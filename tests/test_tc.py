@@ -43,6 +43,9 @@ def _cuda(a, dtype):
     (7, 48, 1, 256, 256),   # c2 geometry
     (5, 24, 1, 130, 129),   # c1 bank, m = 5 (N_f padded to 32)
     (5, 32, 2, 70, 300),
+    # column packing: the remainder columns of several 64-row bands share one tile
+    (7, 48, 2, 209, 512),   # c4 width (4 full tiles + 24 columns), 4 bands -> 2 packed tiles, last with 1 strip
+    (7, 48, 1, 64, 1000),   # one band: a packed tile with a single valid strip
 ])
 def test_tc_energy_grad_parity(m, nf, B, H, W):
     k, th = S.random_filter_bank(nf, m, 2000 + m + nf)
