@@ -126,6 +126,9 @@ cudaError_t tc_set_attr() {
     cudaError_t e = cudaFuncSetAttribute(foe::k_prior_grad_tc<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          tc_smem<M, NP>());
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(foe::k_prior_grad_tc<M, NP, kTcR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tc_smem<M, NP>());
+    if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(foe::k_prior_grad_tc4<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              tc4_smem<M, NP>());
     if (e != cudaSuccess) return e;
@@ -194,6 +197,8 @@ struct ipiano_state {
     int pxt2 = 8;                 // pixels per thread of K2 (nblk2 = HW / (kThreads pxt2) blocks)
     int kind = FOE_STENCIL_FFMA;  // resolved stencil of this state (K1 or K8)
     int tc_rem = 0, tc_spt = 0;   // K8 column packing of this state's plan
+    bool fused = false;           // trial = one K8 launch with K2 inside its staging (+ K3)
+    int nblk3 = 0;                // test partials per image K3 sums (K2 blocks, or K8 tiles if fused)
     int solver = FOE_SOLVER_GRAPH;  // resolved trial-loop driver
     int pgrid = 0;                // persistent driver: co-resident CTAs
     unsigned int* bar = nullptr;  // persistent driver: grid barrier counter
@@ -492,7 +497,15 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
 }
 
 // Launch the prior energy+gradient evaluation `a` (tiling fields taken from the plan).
-foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStream_t s) {
+// Fused trial (K2 inside K8): f~, test-partial output, solver parameters
+struct FuseArgs {
+    const float* ft;
+    double* ppart;
+    foe::SolverParams sp;
+};
+
+foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStream_t s,
+                        const FuseArgs* fuse = nullptr) {
     if (kind == FOE_STENCIL_FFMA) {
         k1_dispatch(md->m, false, a, *md->tp, *md->tp2, dim3(a.ntiles * a.groups, B), s);
         CKL("k_prior_grad2");
@@ -506,6 +519,17 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
     ta.theta_ln2 = md->tc_thl;
     ta.tiles_x = a.tiles_x;
     count_launch(1);
+    if (fuse != nullptr) {   // the default schedule only (the state enables fusion with variant 3)
+        ta.ft = fuse->ft;
+        ta.ppart = fuse->ppart;
+        ta.sp = fuse->sp;
+        if (md->tc_np == 48)
+            foe::k_prior_grad_tc<7, 48, kTcR, true><<<dim3(a.ntiles, B), 256, tc_smem<7, 48>(), s>>>(ta, *md->tc_const);
+        else
+            foe::k_prior_grad_tc<5, 32, kTcR, true><<<dim3(a.ntiles, B), 256, tc_smem<5, 32>(), s>>>(ta, *md->tc_const);
+        CKL("k_prior_grad_tc (fused trial)");
+        return FOE_OK;
+    }
     constexpr int T4 = foe::Tc4Geom<7, 48, kTcR>::THREADS;
     const int var = a.tc_rem > 0 ? 3 : tc_variant();   // packed tiles: the default schedule only
     if (var >= 41 && md->tc_np == 48) {   // profiling knockouts (FOE_K8_VARIANT=k1..k4), results invalid
@@ -863,7 +887,7 @@ foe::K3Args state_k3_args(const ipiano_state* st) {
     a3.ppart = st->ppart;
     a3.trace = st->trace;
     a3.ne = st->ntiles * st->groups;
-    a3.nblk = st->nblk2;
+    a3.nblk = st->nblk3;
     a3.estride = 1;
     a3.sp = st->sp;
     return a3;
@@ -871,13 +895,15 @@ foe::K3Args state_k3_args(const ipiano_state* st) {
 
 // One trial round for every active image: K2 -> K1 (candidate) -> K3.
 foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
-    const foe::K2Args a2 = state_k2_args(st);
-    const dim3 g2(st->nblk2, st->B);
-    if (st->pxt2 == 1) foe::k_inertial_prox<1><<<g2, kThreads, 0, s>>>(a2);
-    else if (st->pxt2 == 4) foe::k_inertial_prox<4><<<g2, kThreads, 0, s>>>(a2);
-    else foe::k_inertial_prox<kPxt2><<<g2, kThreads, 0, s>>>(a2);
-    count_launch(1);
-    CKL("k_inertial_prox");
+    if (!st->fused) {
+        const foe::K2Args a2 = state_k2_args(st);
+        const dim3 g2(st->nblk2, st->B);
+        if (st->pxt2 == 1) foe::k_inertial_prox<1><<<g2, kThreads, 0, s>>>(a2);
+        else if (st->pxt2 == 4) foe::k_inertial_prox<4><<<g2, kThreads, 0, s>>>(a2);
+        else foe::k_inertial_prox<kPxt2><<<g2, kThreads, 0, s>>>(a2);
+        count_launch(1);
+        CKL("k_inertial_prox");
+    }
     const K1Args a1 = state_k1_args(st, 0);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (timed) {
@@ -885,7 +911,8 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
         e1 = pool_event(st);
         CK(cudaEventRecord(e0, s));
     }
-    foe_status rl = launch_prior(st->model, st->kind, a1, st->B, s);
+    FuseArgs fz{st->ft, st->ppart, st->sp};
+    foe_status rl = launch_prior(st->model, st->kind, a1, st->B, s, st->fused ? &fz : nullptr);
     if (rl != FOE_OK) return rl;
     if (timed) {
         CK(cudaEventRecord(e1, s));
@@ -896,7 +923,7 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
     foe::k_decide<<<st->B, kThreads, 0, s>>>(a3);
     count_launch(1);
     CKL("k_decide");
-    st->total_launches += 3;
+    st->total_launches += st->fused ? 2 : 3;
     return FOE_OK;
 }
 
@@ -990,8 +1017,9 @@ foe_status launch_rounds(ipiano_state* st, long long rounds) {
     const int reps = div_up(rounds, st->graph_rounds);
     for (int i = 0; i < reps; ++i) {
         CK(cudaGraphLaunch(st->graph, st->s));
-        st->total_launches += 3LL * st->graph_rounds;
-        count_launch(3LL * st->graph_rounds);
+        const long long per = st->fused ? 2 : 3;
+        st->total_launches += per * st->graph_rounds;
+        count_launch(per * st->graph_rounds);
     }
     return FOE_OK;
 }
@@ -1173,6 +1201,10 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     st->nchunks = div_up(md->nf, Tr<7>::NC);
     st->groups = pl.groups;
     st->pxt2 = kPxt2;
+    if (const char* px = std::getenv("FOE_K2_PXT")) {   // tuning knob (A/B of K2's pixels per thread)
+        const int v = std::atoi(px);
+        if (v == 1 || v == 4 || v == 8) st->pxt2 = v;
+    }
     if (want_persist && pl.kind == FOE_STENCIL_FFMA) {
         // K2 items: one pixel per thread while the grid can hold them all, else four
         const int pxt = npx <= 2LL * md->nsm * kThreads ? 1 : 4;
@@ -1189,6 +1221,14 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
         }
     }
     st->nblk2 = div_up((long long)st->HW, (long long)kThreads * st->pxt2);
+    // fused trial kernel (K2 inside K8's staging): K8 default schedule, batch path; opt-in
+    // (FOE_FUSE_K2=1) until it is measured to win
+    {
+        const char* fz = std::getenv("FOE_FUSE_K2");
+        st->fused = pl.kind == FOE_STENCIL_TENSOR && st->solver == FOE_SOLVER_GRAPH && !t_slab_member &&
+                    tc_variant() == 3 && fz != nullptr && fz[0] == '1';
+    }
+    st->nblk3 = st->fused ? pl.ntiles : st->nblk2;
     auto cleanup = [&](foe_status s) { ipiano_state_destroy(st); return s; };
 #define CKS(call)                                                                    \
     do {                                                                             \
@@ -1202,7 +1242,7 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     CKS(cudaMalloc((void**)&st->g, sizeof(float) * 2 * st->groups * n));
     CKS(cudaMalloc((void**)&st->ft, sizeof(float) * n));
     CKS(cudaMalloc((void**)&st->epart, sizeof(double) * B * st->ntiles * st->groups));
-    CKS(cudaMalloc((void**)&st->ppart, sizeof(double) * 2 * B * st->nblk2 * foe::kNumPart));
+    CKS(cudaMalloc((void**)&st->ppart, sizeof(double) * 2 * B * std::max(st->nblk2, st->nblk3) * foe::kNumPart));
     CKS(cudaMalloc((void**)&st->trace, sizeof(double) * B * (cfg.max_iters + 1) * 8));
     CKS(cudaMemset(st->trace, 0, sizeof(double) * B * (cfg.max_iters + 1) * 8));
     CKS(cudaMalloc((void**)&st->ctl, sizeof(ImgCtl) * B * std::max(1, st->pgrid)));

@@ -802,7 +802,8 @@ struct K2Acc {
 // Shared by k_inertial_prox and the fused K8 trial kernel; the inertial point is written with
 // explicit roundings so that both compile to the same arithmetic (bitwise-equal w+).
 __device__ __forceinline__ double k2_pixel(double wv, double wpv, double gv, double f, double alpha, double beta,
-                                           double l1, double l2, const SolverParams& sp, int idiv, K2Acc& acc) {
+                                           double l1, double l2, const SolverParams& sp, int idiv, K2Acc& acc,
+                                           bool own = true) {
     const double what = __fma_rn(beta, __dsub_rn(wv, wpv), __fma_rn(-alpha, gv, wv));
     double z, em, ep;
     int it;
@@ -814,6 +815,7 @@ __device__ __forceinline__ double k2_pixel(double wv, double wpv, double gv, dou
     } else {
         it = prox_newton(what, f, alpha, l1, l2, sp.newton_tol, sp.newton_cap, z, em, ep);
     }
+    if (!own) return z;   // a fused K8 tile's halo pixel: its owning tile counts it
     const double d = z - wv;
     acc.gd += gv * d;
     acc.dd += d * d;

@@ -98,6 +98,11 @@ struct TcArgs {
     const float* theta_ln2;   // [NP] theta_i ln 2 (0 past N_f)
     int tiles_x;              // column tiles of OW
     int nimg;                 // images in the batch (persistent variant: grid = min(items, SMs))
+    // fused trial (K2 inside K8's staging, FUSED instantiation): f~, the test partials
+    // [B][ntiles][8] of the tile's owned pixels, and the solver parameters
+    const float* ft;
+    double* ppart;
+    SolverParams sp;
 };
 
 // u tile staging (a2): UY rows x UX columns of u - c from the fp64 iterate, one warp per row at a
@@ -153,6 +158,54 @@ __device__ __forceinline__ void tc_stage_u_packed(float* us, const double* w, in
         for (int k = 0; k < NX; ++k) {
             const int ux = lane + 32 * k;
             if (ux < UX) us[uy * UP + ux] = udom ? (float)(v[k] - (double)cst) : cst * expm1f((float)(v[k] - wc));
+        }
+    }
+}
+
+// Fused trial staging (K2 inside K8, rows a8-a10 on the staged pixels): for every staged pixel
+// the inertial point and prox of K2 (k2_pixel, the same arithmetic as k_inertial_prox) give w+,
+// staged as u+ - c; pixels the tile owns store w+ and enter the test partials.  Column
+// geometry per lane slot k: image column gx, unwrapped row origin yb (band - 2C), strip origin
+// (ownership window [ox0, ox1) in unwrapped columns, rows [oy0, oy1)).
+struct FuseCtx {
+    const double *w, *wp;
+    double* wn;
+    const float *g, *ft;
+    double alpha, beta, l1, l2;
+};
+template <int UY, int UX, int UP, int NWARPS>
+__device__ __forceinline__ void tc_stage_fused(float* us, const FuseCtx& fc, const SolverParams& sp, int idiv, int H,
+                                               int W, const int (&gx)[(UX + 31) / 32], const int (&yb)[(UX + 31) / 32],
+                                               const bool (&ok)[(UX + 31) / 32], const bool (&cown)[(UX + 31) / 32],
+                                               const int (&oy0)[(UX + 31) / 32], float cst, double wc, int warp,
+                                               int lane, int R, K2Acc& acc) {
+    constexpr int NX = (UX + 31) / 32;
+    for (int uy = warp; uy < UY; uy += NWARPS) {
+        double wv[NX], wpv[NX];
+        float gv[NX], fv[NX];
+        size_t pix[NX];
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            pix[k] = (size_t)wrap_idx(yb[k] + uy, H) * W + gx[k];
+            wv[k] = ok[k] ? fc.w[pix[k]] : wc;
+            wpv[k] = ok[k] ? fc.wp[pix[k]] : wc;
+            gv[k] = ok[k] ? fc.g[pix[k]] : 0.f;
+            fv[k] = ok[k] ? fc.ft[pix[k]] : 1.f;
+        }
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            const int ux = lane + 32 * k;
+            if (ux >= UX) continue;
+            float val = 0.f;
+            if (ok[k]) {
+                const int yu = yb[k] + uy;                     // unwrapped image row
+                const bool own = cown[k] && yu >= oy0[k] && yu < oy0[k] + R && yu < H;
+                const double z = k2_pixel(wv[k], wpv[k], (double)gv[k], (double)fv[k], fc.alpha, fc.beta, fc.l1,
+                                          fc.l2, sp, idiv, acc, own);
+                if (own) fc.wn[pix[k]] = z;
+                val = idiv ? (float)(z - (double)cst) : cst * expm1f((float)(z - wc));
+            }
+            us[uy * UP + ux] = val;
         }
     }
 }
@@ -237,7 +290,9 @@ __device__ __forceinline__ void tc_z_to_smem(uint32_t t_z, float* zs, int l) {
     for (int k = 0; k < (C1 - C0) * 8; ++k) zs[(C0 * 8 + k) * L + l] = z[k];
 }
 
-template <int M, int NP, int R>
+// FUSED: one trial in one kernel -- K2 (inertial point + prox + test partials) on the staged
+// pixels, then the prior energy + gradient at the candidate (ctl required, evaluates ctl.cand)
+template <int M, int NP, int R, bool FUSED = false>
 __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const __grid_constant__ TcConst cc) {
     using G = TcGeom<M, NP, R>;
     constexpr int C = G::C, KT = G::KT, TAPS = G::TAPS, L = G::LANES;
@@ -307,16 +362,72 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
     // then fp32 expm1 of the small fp64 difference -- accurate relative to u - c (what the
     // stencil needs), and far cheaper than K1's fp64 exp per staged pixel
     const bool udom = args.udom != 0;
-    const double wc = w[(size_t)yc * W + xc];
+    FuseCtx fc{};
+    if constexpr (FUSED) {
+        const ImgCtl& c = args.ctl[b];
+        fc.w = args.w + (size_t)c.cur * args.w_slot_stride + (size_t)b * HW;
+        fc.wp = args.w + (size_t)c.prev * args.w_slot_stride + (size_t)b * HW;
+        fc.wn = const_cast<double*>(args.w) + (size_t)c.cand * args.w_slot_stride + (size_t)b * HW;
+        fc.g = args.g + (size_t)c.gcur * args.g_slot_stride + (size_t)b * HW;
+        fc.ft = ta.ft + (size_t)b * HW;
+        fc.alpha = ta.sp.safety * 2.0 * (1.0 - ta.sp.beta) / c.L;
+        fc.beta = ta.sp.beta;
+        fc.l1 = c.lam1;
+        fc.l2 = c.lam2;
+    }
+    __shared__ double zc_s;
+    if constexpr (FUSED) {
+        if (t == 0) {   // the DC centre's w+ (the same k2_pixel as its staged copy)
+            K2Acc dummy;
+            const size_t pc = (size_t)yc * W + xc;
+            zc_s = k2_pixel(fc.w[pc], fc.wp[pc], (double)fc.g[pc], (double)fc.ft[pc], fc.alpha, fc.beta, fc.l1, fc.l2,
+                            ta.sp, udom, dummy, false);
+        }
+        __syncthreads();
+    }
+    const double wc = FUSED ? zc_s : w[(size_t)yc * W + xc];
     const float cst = (float)(udom ? wc : exp(wc));
+    if constexpr (FUSED) {
+        constexpr int NX = (G::UX + 31) / 32;
+        int gx[NX], yb[NX], oy0[NX];
+        bool ok[NX], cown[NX];
+        const int lane = t & 31;
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            const int ux = lane + 32 * k;
+            if (!packed) {
+                const int xu = x0 - 2 * C + ux;
+                ok[k] = ux < G::UX;
+                gx[k] = wrap_idx(xu, W);
+                yb[k] = y0 - 2 * C;
+                oy0[k] = y0;
+                cown[k] = xu >= x0 && xu < x0 + G::OW && xu < W;
+            } else {
+                const int st = ux / SP, band = y0 / R + st;
+                const int xu = x0 - 2 * C + (ux - st * SP);
+                ok[k] = ux < G::UX && st < args.tc_spt && band < nbands;
+                gx[k] = wrap_idx(xu, W);
+                yb[k] = band * R - 2 * C;
+                oy0[k] = band * R;
+                cown[k] = xu >= x0 && xu < W;
+            }
+        }
+        K2Acc acc;
+        tc_stage_fused<G::UY, G::UX, G::UP, 8>(us, fc, ta.sp, udom, H, W, gx, yb, ok, cown, oy0, cst, wc, warp, lane, R,
+                                               acc);
+        __syncthreads();
+        k2_block_partials(acc, ta.ppart + ((size_t)b * args.ntiles + blockIdx.x) * kNumPart);
+    }
     if (t < NP) {
         css[t] = __ldg(ta.sumk + t);
         ths[t] = __ldg(ta.theta_ln2 + t);
     }
     const double* halo = args.halo;
-    if (!packed) tc_stage_u<G::UY, G::UX, G::UP, 8>(us, w, halo, H, W, y0, x0, 2 * C, udom, cst, wc, warp, t & 31);
-    else tc_stage_u_packed<G::UY, G::UX, G::UP, 8>(us, w, H, W, R, x0, 2 * C, SP, args.tc_spt, y0 / R, nbands, udom,
-                                                   cst, wc, warp, t & 31);
+    if constexpr (!FUSED) {
+        if (!packed) tc_stage_u<G::UY, G::UX, G::UP, 8>(us, w, halo, H, W, y0, x0, 2 * C, udom, cst, wc, warp, t & 31);
+        else tc_stage_u_packed<G::UY, G::UX, G::UP, 8>(us, w, H, W, R, x0, 2 * C, SP, args.tc_spt, y0 / R, nbands,
+                                                       udom, cst, wc, warp, t & 31);
+    }
     tc::fence_proxy_async_smem();
     tc::fence_before_sync();
     __syncthreads();
