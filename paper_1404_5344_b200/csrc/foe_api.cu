@@ -135,6 +135,9 @@ cudaError_t tc_set_attr() {
     e = cudaFuncSetAttribute(foe::k_prior_grad_tc6<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              foe::Tc3Geom<M, NP, kTcR>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(foe::k_prior_grad_tc7<M, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             foe::Tc7Geom<M, NP>::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(foe::k_prior_grad_tc5<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 foe::Tc5Geom<M, NP, kTcR>::SMEM_BYTES);
 }
@@ -146,6 +149,7 @@ int tc_variant() {
     if (e && e[0] == '4') return 4;
     if (e && e[0] == '5') return 5;
     if (e && e[0] == '6') return 6;
+    if (e && e[0] == '7') return 7;
     if (e && e[0] == 'k' && e[1] >= '1' && e[1] <= '4') return 40 + (e[1] - '0');   // profiling knockouts
     return 3;
 }
@@ -197,6 +201,7 @@ struct ipiano_state {
     int pxt2 = 8;                 // pixels per thread of K2 (nblk2 = HW / (kThreads pxt2) blocks)
     int kind = FOE_STENCIL_FFMA;  // resolved stencil of this state (K1 or K8)
     int tc_rem = 0, tc_spt = 0;   // K8 column packing of this state's plan
+    int tc_rows = 64;             // K8 output rows per tile
     bool fused = false;           // trial = one K8 launch with K2 inside its staging (+ K3)
     int nblk3 = 0;                // test partials per image K3 sums (K2 blocks, or K8 tiles if fused)
     int solver = FOE_SOLVER_GRAPH;  // resolved trial-loop driver
@@ -463,6 +468,7 @@ struct Plan {
     int kind = FOE_STENCIL_FFMA;
     int tiles_x = 0, ntiles = 0, groups = 1;
     int tc_rem = 0, tc_spt = 0;   // K8 column packing (K1Args::tc_rem / tc_spt)
+    int tc_rows = 64;             // K8 output rows per tile (v7: chosen per problem)
 };
 Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref, int req_groups,
                   bool allow_pack = true) {
@@ -473,19 +479,41 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
         tc = (long long)div_up(W, ow) * div_up(H_grid, kTcR) * B >= 2LL * md->nsm;
     if (tc) {
         p.kind = FOE_STENCIL_TENSOR;
-        // full tiles of ow columns per 64-row band; the remainder columns of several bands share
-        // one packed tile (default schedule, not for row slabs, whose energy partials are per band)
-        int nfull = W / ow, rem = W - nfull * ow, spt = 0;
-        if (rem > 0 && allow_pack && H_grid == H && tc_variant() == 3) {
-            spt = 128 / (rem + 2 * (md->m - 1));
-            if (spt < 2) spt = 0;
+        // full tiles of ow columns per band of R rows; the remainder columns of several bands share
+        // one packed tile (not for row slabs, whose energy partials are per 64-row band).  v7
+        // (streamed u tile) takes R from {64, 128, 256}: fewest waves x response rows per tile.
+        const bool pack_ok = allow_pack && H_grid == H;
+        const int var = tc_variant();
+        const bool v7 = var == 7 && pack_ok;
+        auto tiling = [&](int R, Plan& q) {
+            int nfull = W / ow, rem = W - nfull * ow, spt = 0;
+            if (rem > 0 && pack_ok && (var == 3 || v7)) {
+                spt = 128 / (rem + 2 * (md->m - 1));
+                if (spt < 2) spt = 0;
+            }
+            if (rem > 0 && spt == 0) { nfull += 1; rem = 0; }
+            const int nbands = div_up(H, R);
+            q.tiles_x = nfull;
+            q.ntiles = nbands * nfull + (rem > 0 ? div_up(nbands, spt) : 0);
+            q.tc_rem = rem;
+            q.tc_spt = spt;
+            q.tc_rows = R;
+        };
+        tiling(kTcR, p);
+        const char* rows_env = std::getenv("FOE_K8_ROWS");   // tuning knob: force v7's R
+        if (v7 && rows_env && (std::atoi(rows_env) == 64 || std::atoi(rows_env) == 128 || std::atoi(rows_env) == 256)) {
+            tiling(std::atoi(rows_env), p);
+        } else if (v7) {
+            const long long slots = 2LL * md->nsm;
+            double best = 1e30;
+            for (int R : {64, 128, 256}) {
+                if (R > 64 && R >= 2 * H) break;
+                Plan q;
+                tiling(R, q);
+                const double cost = std::ceil((double)q.ntiles * B / (double)slots) * (R + md->m - 1);
+                if (cost < best - 1e-9) { best = cost; tiling(R, p); }
+            }
         }
-        if (rem > 0 && spt == 0) { nfull += 1; rem = 0; }
-        const int nbands = div_up(H, kTcR);
-        p.tiles_x = nfull;
-        p.ntiles = nbands * nfull + (rem > 0 ? div_up(nbands, spt) : 0);
-        p.tc_rem = rem;
-        p.tc_spt = spt;
         p.groups = 1;
     } else {
         p.kind = FOE_STENCIL_FFMA;
@@ -531,7 +559,17 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
         return FOE_OK;
     }
     constexpr int T4 = foe::Tc4Geom<7, 48, kTcR>::THREADS;
-    const int var = a.tc_rem > 0 ? 3 : tc_variant();   // packed tiles: the default schedule only
+    int var = tc_variant();
+    if (var == 7 && (a.tc_rows <= 0 || a.halo != nullptr)) var = 3;   // v7: batch path with a planned R
+    if (var != 7 && (a.tc_rem > 0 || (a.tc_rows > 0 && a.tc_rows != kTcR))) var = 3;   // packed: v3 / v7 only
+    if (var == 7) {
+        if (md->tc_np == 48)
+            foe::k_prior_grad_tc7<7, 48><<<dim3(a.ntiles, B), 256, foe::Tc7Geom<7, 48>::SMEM_BYTES, s>>>(ta, *md->tc_const);
+        else
+            foe::k_prior_grad_tc7<5, 32><<<dim3(a.ntiles, B), 256, foe::Tc7Geom<5, 32>::SMEM_BYTES, s>>>(ta, *md->tc_const);
+        CKL("k_prior_grad_tc7");
+        return FOE_OK;
+    }
     if (var >= 41 && md->tc_np == 48) {   // profiling knockouts (FOE_K8_VARIANT=k1..k4), results invalid
         static bool attr = false;
         if (!attr) {
@@ -604,7 +642,7 @@ bool is_device_ptr(const void* p) {
 foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int W, int groups,
                         double* epart, float* gparts, bool hvp, const double* v, const float* gw,
                         cudaStream_t s, int kind = FOE_STENCIL_FFMA, int tiles_x_tc = 0, int ntiles_tc = 0,
-                        int tc_rem = 0, int tc_spt = 0) {
+                        int tc_rem = 0, int tc_spt = 0, int tc_rows = kTcR) {
     K1Args a{};
     a.w = w;
     a.w_slot_stride = 0;
@@ -631,6 +669,7 @@ foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int 
             a.groups = 1;
             a.tc_rem = tc_rem;
             a.tc_spt = tc_spt;
+            a.tc_rows = tc_rows;
         }
         return launch_prior(md, kind, a, B, s);
     }
@@ -668,7 +707,7 @@ foe_status foe_energy_grad(const foe_model* md, const double* w, const float* f,
     if (!direct) CK(cudaMallocAsync((void**)&gparts, sizeof(float) * groups * B * HW, s));
     CK(cudaMallocAsync((void**)&dred, sizeof(double) * B * 2, s));
     st = run_k1_plain(md, w, B, H, W, groups, epart, direct ? grad : gparts, false, nullptr, nullptr, s, pl.kind,
-                      pl.tiles_x, pl.ntiles, pl.tc_rem, pl.tc_spt);
+                      pl.tiles_x, pl.ntiles, pl.tc_rem, pl.tc_spt, pl.tc_rows);
     if (st != FOE_OK) return st;
     if (grad && !direct) {
         const size_t n = (size_t)B * HW;
@@ -848,6 +887,7 @@ K1Args state_k1_args(const ipiano_state* st, int which_cur) {
     a.udom = st->model->term == FOE_DATA_IDIV;
     a.tc_rem = st->tc_rem;
     a.tc_spt = st->tc_spt;
+    a.tc_rows = st->tc_rows;
     return a;
 }
 
@@ -1197,6 +1237,7 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     st->tiles_x = pl.tiles_x;
     st->tc_rem = pl.tc_rem;
     st->tc_spt = pl.tc_spt;
+    st->tc_rows = pl.tc_rows;
     st->ntiles = pl.ntiles;
     st->nchunks = div_up(md->nf, Tr<7>::NC);
     st->groups = pl.groups;

@@ -82,6 +82,7 @@ struct K1Args {
     // columns; the last tc_rem columns of tc_spt consecutive bands share one tile (strips of
     // tc_rem + 4C lanes), instead of one mostly idle tile per band
     int tc_rem, tc_spt;
+    int tc_rows;            // K8 v7 (streamed u tile): output rows per tile (v3: the 64 of kTcR)
     // HVP only
     const double* v;        // [B][H][W]
     const float* gw;        // [B][H][W] gradient at w

@@ -1465,4 +1465,294 @@ __global__ void __launch_bounds__(384, 2) k_prior_grad_tc6(const TcArgs ta, cons
     if (warp == 0) tc::tmem_dealloc<GB::TCOLS>(tb);
 }
 
+// =============================================================================================
+// K8 v7: v3's lock-step row loop with the u tile STREAMED through a 16-row shared-memory ring
+// instead of staged whole in the prologue, so that a tile can be any number of rows R (runtime,
+// ta.rows): one new staged row per response row, loaded one iteration ahead (prefetch register)
+// and written before the iteration's second CTA barrier.  Taller tiles cut the halo recompute
+// (R + 2C response rows per R output rows: 1.094 at R = 64, 1.023 at R = 256) and the prologue,
+// and free 32 KB of shared memory.  Column packing as v3 (strips of the remainder columns of
+// tc_spt bands of R rows).  Batch path only (the slab path keeps v3's 64-row bands).
+// =============================================================================================
+template <int M, int NP>
+struct Tc7Geom {
+    using B = TcGeom<M, NP, 64>;
+    static constexpr int C = B::C, KT = B::KT, LANES = B::LANES, OW = B::OW, UX = B::UX, UP = B::UP, NB = B::NB;
+    static constexpr int RING = 16;                       // staged u rows in flight (>= 2C + 3)
+    static_assert(RING >= 2 * C + 3, "ring too small");
+    static constexpr int SM_B = 0;
+    static constexpr int SM_U = SM_B + B::B_FLOATS;
+    static constexpr int SM_Z = SM_U + RING * UP;
+    static constexpr int SM_HAND = SM_Z + B::TAPS * LANES;
+    static constexpr int SM_ZL = SM_HAND + 8 * LANES;
+    static constexpr int SM_FLOATS = SM_ZL + 4 * LANES;
+    static constexpr int SMEM_BYTES = SM_FLOATS * 4 + 64;
+};
+
+// im2col from the ring: rp[a] = row a of the window (lane offset applied)
+template <int M, int C0, int C1>
+__device__ __forceinline__ void tc_im2col_ring(const float* const (&rp)[M], float vc, uint32_t t_hi, uint32_t t_lo) {
+#pragma unroll
+    for (int c8 = C0; c8 < C1; ++c8) {
+        float h[8], lo[8];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+            const int t0 = c8 * 8 + e, t1 = t0 + 1;
+            const float2 u2 = make_float2(t0 < M * M ? rp[t0 / M][t0 % M] : vc, t1 < M * M ? rp[t1 / M][t1 % M] : vc);
+            const float2 v = __fadd2_rn(u2, make_float2(-vc, -vc));
+            float2 hi2, lo2;
+            tc::tf32_split2(v, hi2, lo2);
+            h[e] = hi2.x; h[e + 1] = hi2.y;
+            lo[e] = lo2.x; lo[e + 1] = lo2.y;
+        }
+        tc::tmem_st8(t_hi + c8 * 8, h);
+        tc::tmem_st8(t_lo + c8 * 8, lo);
+    }
+}
+
+template <int M, int NP>
+__global__ void __launch_bounds__(256, 2) k_prior_grad_tc7(const TcArgs ta, const __grid_constant__ TcConst cc) {
+    using G = Tc7Geom<M, NP>;
+    using GB = TcGeom<M, NP, 64>;
+    constexpr int C = G::C, KT = G::KT, L = G::LANES, RING = G::RING;
+    extern __shared__ __align__(128) float sm[];
+    float* bsm = sm + G::SM_B;
+    float* us = sm + G::SM_U;                                   // ring [RING][UP]
+    float* zs = sm + G::SM_Z;
+    __shared__ uint32_t tbase_s;
+    __shared__ __align__(8) uint64_t mbar_f, mbar_b;
+    __shared__ double red[32];
+
+    const K1Args& args = ta.k;
+    const int R = args.tc_rows;                                 // output rows per tile (runtime)
+    const int RR = R + 2 * C;                                   // response rows
+    const int UYR = R + 4 * C;                                  // staged rows
+    const int b = blockIdx.y;
+    int wslot = 0, gslot = 0;
+    if (args.ctl != nullptr) {
+        const ImgCtl& c = args.ctl[b];
+        if (!c.active) return;
+        wslot = args.which_cur ? c.cur : c.cand;
+        gslot = args.which_cur ? c.gcur : c.gcand;
+    }
+    const int H = args.H, W = args.W;
+    const size_t HW = (size_t)H * W;
+    const int tile = blockIdx.x;
+    const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
+    const int t = threadIdx.x, warp = __shfl_sync(0xffffffffu, t >> 5, 0);
+    const int wg = warp >> 2;
+    const int l = (warp & 3) * 32 + (t & 31);
+    const int nbands = (H + R - 1) / R;
+    const int nnorm = nbands * ta.tiles_x;
+    const bool packed = tile >= nnorm;
+    int y0, x0, sy0, ocol;
+    bool svalid = true;
+    const int SP = args.tc_rem + 4 * C;
+    int band0 = 0;
+    if (!packed) {
+        const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
+        y0 = ty * R; x0 = tx * G::OW; sy0 = y0; ocol = l;
+    } else {
+        band0 = (tile - nnorm) * args.tc_spt;
+        const int st = l / SP;
+        ocol = l - st * SP;
+        svalid = st < args.tc_spt && band0 + st < nbands;
+        y0 = band0 * R; x0 = ta.tiles_x * G::OW; sy0 = (band0 + st) * R;
+    }
+
+    if (warp == 0) tc::tmem_alloc<GB::TCOLS>(&tbase_s);
+    if (t == 0) {
+        tc::mbar_init(&mbar_f, 1);
+        tc::mbar_init(&mbar_b, 1);
+        tc::mbar_fence_init();
+    }
+    {
+        const float4* src = reinterpret_cast<const float4*>(ta.bimg);
+        float4* dst = reinterpret_cast<float4*>(bsm);
+#pragma unroll 4
+        for (int i = t; i < GB::B_FLOATS / 4; i += 256) dst[i] = __ldg(src + i);
+    }
+    const int yc = min(y0 + min(R, H) / 2, H - 1), xc = min(x0 + (packed ? args.tc_rem : G::OW) / 2, W - 1);
+    const bool udom = args.udom != 0;
+    const double wc = w[(size_t)yc * W + xc];
+    const float cst = (float)(udom ? wc : exp(wc));
+    // this thread's staged column (t < UX): image column and unwrapped row origin of its strip
+    const bool st_on = t < G::UX;
+    bool st_ok = false;
+    int st_gx = 0, st_yb = 0;
+    if (st_on) {
+        if (!packed) {
+            st_ok = true;
+            st_gx = wrap_idx(x0 - 2 * C + t, W);
+            st_yb = y0 - 2 * C;
+        } else {
+            const int st = t / SP, band = band0 + st;
+            st_ok = st < args.tc_spt && band < nbands;
+            st_gx = wrap_idx(x0 - 2 * C + (t - st * SP), W);
+            st_yb = band * R - 2 * C;
+        }
+    }
+    auto stage_load = [&](int jj) -> double {
+        return (st_ok && jj < UYR) ? w[(size_t)wrap_idx(st_yb + jj, H) * W + st_gx] : wc;
+    };
+    auto stage_store = [&](int jj, double v) {
+        if (st_on && jj < UYR) us[(jj & (RING - 1)) * G::UP + t] = udom ? (float)(v - (double)cst) : cst * expm1f((float)(v - wc));
+    };
+    // prologue: staged rows 0 .. 2C, prefetch of row 2C + 1
+    {
+        double v[2 * C + 1];
+#pragma unroll
+        for (int jj = 0; jj <= 2 * C; ++jj) v[jj] = stage_load(jj);
+#pragma unroll
+        for (int jj = 0; jj <= 2 * C; ++jj) stage_store(jj, v[jj]);
+    }
+    double pf = stage_load(2 * C + 1);
+    tc::fence_proxy_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tb = tbase_s;
+    const uint32_t tl = tb + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t idf = tc::idesc_tf32(128, NP);
+    const uint32_t idb = tc::idesc_tf32(128, G::NB);
+    const uint32_t b_base = tc::smem_u32(bsm);
+
+    const int ow = packed ? args.tc_rem : G::OW;
+    const bool col_own = svalid && (ocol >= C) && (ocol < C + ow) && (x0 - C + ocol < W);
+    const bool out_col = svalid && (ocol < ow) && (x0 + ocol < W);
+
+    double e_acc = 0.0;
+    constexpr int NC8 = KT / 8, H8 = (NC8 + 1) / 2;
+    constexpr int NZ8 = G::NB / 8, HZ8 = (NZ8 + 1) / 2;
+    constexpr int NF8 = NP / 8, HF8 = NF8 / 2;
+    constexpr int A0 = C + 1, A1 = M - A0;
+    float acc[A0 > A1 ? A0 : A1];
+#pragma unroll
+    for (int k = 0; k < (A0 > A1 ? A0 : A1); ++k) acc[k] = 0.f;
+    float* gout = args.g + (size_t)gslot * args.g_slot_stride + (size_t)b * HW;
+    float* hand = sm + G::SM_HAND;
+    float* zls = sm + G::SM_ZL;
+
+#pragma unroll 1
+    for (int j = 0; j <= RR; ++j) {
+        float uq = 0.f;
+        if (j < RR) {
+            const float* rp[M];
+#pragma unroll
+            for (int a = 0; a < M; ++a) rp[a] = us + ((j + a) & (RING - 1)) * G::UP + l;
+            const float vc = rp[C][C];
+            uq = vc + cst;
+            if (wg == 0) tc_im2col_ring<M, 0, H8>(rp, vc, tl + GB::COL_AHI, tl + GB::COL_ALO);
+            else tc_im2col_ring<M, H8, NC8>(rp, vc, tl + GB::COL_AHI, tl + GB::COL_ALO);
+        }
+        if (j > 0) {
+            tc::mbar_wait(&mbar_b, (uint32_t)((j - 1) & 1));
+            tc::fence_after_sync();
+            if (wg == 0) tc_z_to_smem<L, 0, HZ8>(tl + GB::COL_Z, zs, l);
+            else tc_z_to_smem<L, HZ8, NZ8>(tl + GB::COL_Z, zs, l);
+        }
+        tc::wait_st();
+        tc::fence_before_sync();
+        __syncthreads();
+        if (warp == 0 && j < RR) {
+            tc::fence_after_sync();
+#pragma unroll
+            for (int s = 0; s < NC8; ++s) {
+                const uint32_t off = (uint32_t)(s * 2 * NP * 16);
+                const uint64_t bh = tc::sdesc_kmajor(b_base + off, NP * 16, 128);
+                const uint64_t bl = tc::sdesc_kmajor(b_base + GB::BF_FLOATS * 4 + off, NP * 16, 128);
+                tc::mma_tf32_ts_warp(tb + GB::COL_D, tb + GB::COL_AHI + s * 8, bl, idf, s > 0);
+                tc::mma_tf32_ts_warp(tb + GB::COL_D, tb + GB::COL_ALO + s * 8, bh, idf, 1);
+            }
+#pragma unroll
+            for (int s = 0; s < NC8; ++s) {
+                const uint32_t off = (uint32_t)(s * 2 * NP * 16);
+                const uint64_t bh = tc::sdesc_kmajor(b_base + off, NP * 16, 128);
+                tc::mma_tf32_ts_warp(tb + GB::COL_D, tb + GB::COL_AHI + s * 8, bh, idf, 1);
+            }
+            tc::mma_commit_warp(&mbar_f);
+        }
+        if (j > 0) {
+            const int jz = j - 1;
+            if (wg == 0) {
+#pragma unroll
+                for (int a = 0; a < A0; ++a) {
+                    float sa = 0.f;
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) sa += zs[(a * M + bb) * L + l + bb];
+                    acc[a] += sa;
+                }
+                const int o = jz - (A0 - 1);
+                if (o >= 0) hand[(o & 7) * L + l] = acc[A0 - 1];
+#pragma unroll
+                for (int k = A0 - 1; k > 0; --k) acc[k] = acc[k - 1];
+                acc[0] = 0.f;
+            } else {
+                const float* zl = zls + (jz & 1) * 2 * L;
+#pragma unroll
+                for (int k = 0; k < A1; ++k) {
+                    const int a = A0 + k;
+                    float sa = 0.f;
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) {
+                        const int tap = a * M + bb;
+                        sa += tap < G::NB ? zs[tap * L + l + bb] : zl[l + bb] + zl[L + l + bb];
+                    }
+                    acc[k] += sa;
+                }
+                const int o = jz - 2 * C;
+                if (o >= 0 && o < R && out_col && sy0 + o < H) {
+                    const float s_tot = acc[A1 - 1] + hand[(o & 7) * L + l];
+                    const float u = udom ? 1.0f : us[((o + 2 * C) & (RING - 1)) * G::UP + l + 2 * C] + cst;
+                    gout[(size_t)(sy0 + o) * W + x0 + ocol] = u * s_tot;
+                }
+#pragma unroll
+                for (int k = A1 - 1; k > 0; --k) acc[k] = acc[k - 1];
+                acc[0] = 0.f;
+            }
+        }
+        if (j < RR) {
+            // stream the next staged row (needed by im2col(j + 1)), prefetch the one after
+            stage_store(j + 2 * C + 1, pf);
+            pf = stage_load(j + 2 * C + 2);
+            tc::mbar_wait(&mbar_f, (uint32_t)(j & 1));
+            tc::fence_after_sync();
+            const bool own = col_own && (j >= C) && (j < C + R) && (sy0 - C + j < H);
+            float zl;
+            const float el = wg == 0
+                ? tc_epilogue<0, HF8>(tl + GB::COL_D, tl + GB::COL_PHI, tl + GB::COL_PLO, uq, cc.sumk, cc.thl, cc.kbl, zl)
+                : tc_epilogue<HF8, NF8>(tl + GB::COL_D, tl + GB::COL_PHI, tl + GB::COL_PLO, uq, cc.sumk, cc.thl, cc.kbl, zl);
+            zls[(j & 1) * 2 * L + wg * L + l] = zl;
+            if (own) e_acc += (double)el;
+            tc::wait_st();
+            tc::fence_before_sync();
+            __syncthreads();
+            if (warp == 0) {
+                tc::fence_after_sync();
+#pragma unroll
+                for (int s = 0; s < NF8; ++s) {
+                    const uint32_t off = (uint32_t)(s * 2 * G::NB * 16);
+                    const uint64_t bh = tc::sdesc_kmajor(b_base + 2 * GB::BF_FLOATS * 4 + off, G::NB * 16, 128);
+                    const uint64_t bl = tc::sdesc_kmajor(b_base + (2 * GB::BF_FLOATS + GB::BB_FLOATS) * 4 + off,
+                                                         G::NB * 16, 128);
+                    tc::mma_tf32_ts_warp(tb + GB::COL_Z, tb + GB::COL_PHI + s * 8, bl, idb, s > 0);
+                    tc::mma_tf32_ts_warp(tb + GB::COL_Z, tb + GB::COL_PLO + s * 8, bh, idb, 1);
+                }
+#pragma unroll
+                for (int s = 0; s < NF8; ++s) {
+                    const uint32_t off = (uint32_t)(s * 2 * G::NB * 16);
+                    const uint64_t bh = tc::sdesc_kmajor(b_base + 2 * GB::BF_FLOATS * 4 + off, G::NB * 16, 128);
+                    tc::mma_tf32_ts_warp(tb + GB::COL_Z, tb + GB::COL_PHI + s * 8, bh, idb, 1);
+                }
+                tc::mma_commit_warp(&mbar_b);
+            }
+        }
+    }
+    const double e = block_sum_d(e_acc, red);
+    if (t == 0) args.epart[(size_t)b * args.ntiles * args.groups + blockIdx.x] = e;
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<GB::TCOLS>(tb);
+}
+
 }  // namespace foe
