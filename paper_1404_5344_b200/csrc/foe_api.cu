@@ -33,6 +33,7 @@ thread_local std::string g_err;
 std::atomic<long long> g_launches{0};  // kernels launched by this library (process-wide)
 thread_local bool t_capturing = false;   // graph capture: replays are counted instead
 thread_local bool t_slab_member = false; // ipiano_slabs_create is creating its member states
+thread_local int t_force_ncp = 0;        // ... with the whole scene's K1 chunk size
 inline void count_launch(long long n) {
     if (!t_capturing) g_launches.fetch_add(n, std::memory_order_relaxed);
 }
@@ -91,17 +92,22 @@ void k1_launch(const K1Args& a, const TapParams& tp, dim3 grid, cudaStream_t s) 
 }
 
 // K1 v2 (paired FFMA2): NCP filter pairs per shared-memory chunk, SF forward rows per item
+// (chunks of 1 pair for images too small to fill the GPU with 2-pair chunks: plan_stencil)
 constexpr int kNCP = 2, kSF2 = 5;
-template <int M>
-constexpr int smem2_bytes() { return foe::G2<M, kNCP, kSF2>::SMEM_BYTES; }
+template <int M, int NCP = kNCP>
+constexpr int smem2_bytes() { return foe::G2<M, NCP, kSF2>::SMEM_BYTES; }
 template <int M>
 cudaError_t k2g_set_attr() {
-    return cudaFuncSetAttribute(foe::k_prior_grad2<M, kNCP, kSF2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                smem2_bytes<M>());
+    cudaError_t e = cudaFuncSetAttribute(foe::k_prior_grad2<M, kNCP, kSF2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem2_bytes<M>());
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(foe::k_prior_grad2<M, 1, kSF2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem2_bytes<M, 1>());
 }
 template <int M>
 void k2g_launch(const K1Args& a, const foe::TapParams2& tp, dim3 grid, cudaStream_t s) {
-    foe::k_prior_grad2<M, kNCP, kSF2><<<grid, kThreads, smem2_bytes<M>(), s>>>(a, tp);
+    if (a.ncp == 1) foe::k_prior_grad2<M, 1, kSF2><<<grid, kThreads, smem2_bytes<M, 1>(), s>>>(a, tp);
+    else foe::k_prior_grad2<M, kNCP, kSF2><<<grid, kThreads, smem2_bytes<M>(), s>>>(a, tp);
 }
 
 // hvp: the v1 stencil (setup only); gradient/energy: the v2 paired-FMA stencil
@@ -198,6 +204,7 @@ struct ipiano_state {
     ipiano_config cfg_in{};   // the configuration as the caller passed it (ipiano_run's cache key)
     foe::SolverParams sp{};
     int tiles_x = 0, ntiles = 0, groups = 1, nchunks = 0, nblk2 = 0;
+    int ncp = 2;                  // K1: filter pairs per chunk (plan_stencil)
     int pxt2 = 8;                 // pixels per thread of K2 (nblk2 = HW / (kThreads pxt2) blocks)
     int kind = FOE_STENCIL_FFMA;  // resolved stencil of this state (K1 or K8)
     int tc_rem = 0, tc_spt = 0;   // K8 column packing of this state's plan
@@ -446,8 +453,7 @@ void foe_model_destroy(foe_model* model) {
 namespace {
 
 // Choose the number of filter groups (split-N_f) so that a launch fills the machine.
-int choose_groups(const foe_model* md, int ntiles, int B, int requested) {
-    const int nchunks = div_up(md->nf, Tr<7>::NC);
+int choose_groups(const foe_model* md, int ntiles, int B, int requested, int nchunks) {
     if (requested > 0) return std::min(requested, nchunks);
     const long long slots = 2LL * md->nsm;  // 2 CTAs / SM
     double best = 1e30;
@@ -469,6 +475,7 @@ struct Plan {
     int tiles_x = 0, ntiles = 0, groups = 1;
     int tc_rem = 0, tc_spt = 0;   // K8 column packing (K1Args::tc_rem / tc_spt)
     int tc_rows = 64;             // K8 output rows per tile (v7: chosen per problem)
+    int ncp = kNCP, nchunks = 0;  // K1: filter pairs per chunk, chunks
 };
 Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref, int req_groups,
                   bool allow_pack = true) {
@@ -519,7 +526,12 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
         p.kind = FOE_STENCIL_FFMA;
         p.tiles_x = div_up(W, kTile);
         p.ntiles = p.tiles_x * div_up(H, kTile);
-        p.groups = choose_groups(md, p.tiles_x * div_up(H_grid, kTile), B, req_groups);
+        // one filter pair per chunk when 2-pair chunks leave most SMs idle (single small images)
+        const int npairs = (md->nf + 1) / 2;
+        const long long tiles_grid = (long long)p.tiles_x * div_up(H_grid, kTile) * B;
+        p.ncp = t_force_ncp > 0 ? t_force_ncp : tiles_grid * div_up(npairs, kNCP) < md->nsm ? 1 : kNCP;
+        p.nchunks = div_up(npairs, p.ncp);
+        p.groups = choose_groups(md, p.tiles_x * div_up(H_grid, kTile), B, req_groups, p.nchunks);
     }
     return p;
 }
@@ -642,7 +654,7 @@ bool is_device_ptr(const void* p) {
 foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int W, int groups,
                         double* epart, float* gparts, bool hvp, const double* v, const float* gw,
                         cudaStream_t s, int kind = FOE_STENCIL_FFMA, int tiles_x_tc = 0, int ntiles_tc = 0,
-                        int tc_rem = 0, int tc_spt = 0, int tc_rows = kTcR) {
+                        int tc_rem = 0, int tc_spt = 0, int tc_rows = kTcR, int ncp = kNCP, int nchunks2 = 0) {
     K1Args a{};
     a.w = w;
     a.w_slot_stride = 0;
@@ -658,7 +670,11 @@ foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int 
     a.ntiles = a.tiles_x * div_up(H, kTile);
     a.groups = groups;
     a.nf = md->nf;
-    a.nchunks = div_up(md->nf, Tr<7>::NC);
+    a.nchunks = div_up(md->nf, Tr<7>::NC);   // (4 filters = 2 pairs per chunk; the v1 HVP stencil too)
+    if (!hvp && kind == FOE_STENCIL_FFMA && nchunks2 > 0) {
+        a.ncp = ncp;
+        a.nchunks = nchunks2;
+    }
     a.v = v;
     a.gw = gw;
     a.udom = md->term == FOE_DATA_IDIV;
@@ -707,7 +723,7 @@ foe_status foe_energy_grad(const foe_model* md, const double* w, const float* f,
     if (!direct) CK(cudaMallocAsync((void**)&gparts, sizeof(float) * groups * B * HW, s));
     CK(cudaMallocAsync((void**)&dred, sizeof(double) * B * 2, s));
     st = run_k1_plain(md, w, B, H, W, groups, epart, direct ? grad : gparts, false, nullptr, nullptr, s, pl.kind,
-                      pl.tiles_x, pl.ntiles, pl.tc_rem, pl.tc_spt, pl.tc_rows);
+                      pl.tiles_x, pl.ntiles, pl.tc_rem, pl.tc_spt, pl.tc_rows, pl.ncp, pl.nchunks);
     if (st != FOE_OK) return st;
     if (grad && !direct) {
         const size_t n = (size_t)B * HW;
@@ -884,6 +900,7 @@ K1Args state_k1_args(const ipiano_state* st, int which_cur) {
     a.groups = st->groups;
     a.nf = st->model->nf;
     a.nchunks = st->nchunks;
+    a.ncp = st->ncp;
     a.udom = st->model->term == FOE_DATA_IDIV;
     a.tc_rem = st->tc_rem;
     a.tc_spt = st->tc_spt;
@@ -968,29 +985,35 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
 }
 
 // ---- persistent driver (foe_persist.cuh) ----
-template <int M, int PXT>
-const void* persist_kernel() { return (const void*)foe::k_ipiano_persistent<M, kNCP, kSF2, PXT>; }
-const void* persist_kernel_for(int m, int pxt) {
-    if (m == 7) return pxt == 1 ? persist_kernel<7, 1>() : persist_kernel<7, 4>();
-    if (m == 5) return pxt == 1 ? persist_kernel<5, 1>() : persist_kernel<5, 4>();
-    return pxt == 1 ? persist_kernel<3, 1>() : persist_kernel<3, 4>();
+template <int M, int PXT, int NCP>
+const void* persist_kernel() { return (const void*)foe::k_ipiano_persistent<M, NCP, kSF2, PXT>; }
+const void* persist_kernel_for(int m, int pxt, int ncp) {
+    if (m == 7) return pxt == 1 ? (ncp == 1 ? persist_kernel<7, 1, 1>() : persist_kernel<7, 1, 2>())
+                                : (ncp == 1 ? persist_kernel<7, 4, 1>() : persist_kernel<7, 4, 2>());
+    if (m == 5) return pxt == 1 ? (ncp == 1 ? persist_kernel<5, 1, 1>() : persist_kernel<5, 1, 2>())
+                                : (ncp == 1 ? persist_kernel<5, 4, 1>() : persist_kernel<5, 4, 2>());
+    return pxt == 1 ? (ncp == 1 ? persist_kernel<3, 1, 1>() : persist_kernel<3, 1, 2>())
+                    : (ncp == 1 ? persist_kernel<3, 4, 1>() : persist_kernel<3, 4, 2>());
 }
-int smem2_for(int m) { return m == 7 ? smem2_bytes<7>() : m == 5 ? smem2_bytes<5>() : smem2_bytes<3>(); }
+int smem2_for(int m, int ncp) {
+    if (ncp == 1) return m == 7 ? smem2_bytes<7, 1>() : m == 5 ? smem2_bytes<5, 1>() : smem2_bytes<3, 1>();
+    return m == 7 ? smem2_bytes<7>() : m == 5 ? smem2_bytes<5>() : smem2_bytes<3>();
+}
 
 // co-resident CTAs of the persistent kernel on this device (0 if cooperative launch is unsupported)
-int persist_capacity(const foe_model* md, int pxt) {
+int persist_capacity(const foe_model* md, int pxt, int ncp) {
     int coop = 0;
     if (cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, md->dev) != cudaSuccess || !coop) {
         cudaGetLastError();
         return 0;
     }
-    const void* k = persist_kernel_for(md->m, pxt);
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2_for(md->m)) != cudaSuccess) {
+    const void* k = persist_kernel_for(md->m, pxt, ncp);
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2_for(md->m, ncp)) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
     int per_sm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem2_for(md->m)) != cudaSuccess) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kThreads, smem2_for(md->m, ncp)) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -1014,8 +1037,8 @@ foe_status launch_persistent(ipiano_state* st, long long max_rounds) {
     pa.phase_ns = st->phase_ns;
     CK(cudaMemsetAsync(st->bar, 0, sizeof(unsigned int), st->s));
     void* args[] = {(void*)&pa, (void*)st->model->tp2};
-    CK(cudaLaunchCooperativeKernel(persist_kernel_for(st->model->m, st->pxt2), dim3(st->pgrid), dim3(kThreads), args,
-                                   (size_t)smem2_for(st->model->m), st->s));
+    CK(cudaLaunchCooperativeKernel(persist_kernel_for(st->model->m, st->pxt2, st->ncp), dim3(st->pgrid), dim3(kThreads),
+                                   args, (size_t)smem2_for(st->model->m, st->ncp), st->s));
     count_launch(1);
     st->total_launches += 1;
     return FOE_OK;
@@ -1239,7 +1262,8 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     st->tc_spt = pl.tc_spt;
     st->tc_rows = pl.tc_rows;
     st->ntiles = pl.ntiles;
-    st->nchunks = div_up(md->nf, Tr<7>::NC);
+    st->ncp = pl.kind == FOE_STENCIL_FFMA ? pl.ncp : kNCP;
+    st->nchunks = pl.kind == FOE_STENCIL_FFMA ? pl.nchunks : div_up(md->nf, Tr<7>::NC);
     st->groups = pl.groups;
     st->pxt2 = kPxt2;
     if (const char* px = std::getenv("FOE_K2_PXT")) {   // tuning knob (A/B of K2's pixels per thread)
@@ -1249,7 +1273,7 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     if (want_persist && pl.kind == FOE_STENCIL_FFMA) {
         // K2 items: one pixel per thread while the grid can hold them all, else four
         const int pxt = npx <= 2LL * md->nsm * kThreads ? 1 : 4;
-        const int cap = persist_capacity(md, pxt);
+        const int cap = persist_capacity(md, pxt, pl.ncp);
         if (cap > 0) {
             const long long items = std::max((long long)pl.ntiles * pl.groups * B,
                                              (long long)div_up((long long)st->HW, (long long)kThreads * pxt) * B);
@@ -1990,9 +2014,11 @@ foe_status ipiano_slabs_create(const foe_model* md, const float* f, int H_global
     for (int j = 0; j < nmem; ++j) {
         ipiano_state* st = nullptr;
         t_slab_member = true;   // per-band energy partials: no K8 column packing
+        t_force_ncp = pl.ncp;   // and the whole scene's K1 chunking, so slabs are G-invariant
         foe_status r = ipiano_state_create(md, f + (size_t)j * HWs, 1, g->Hs, W, lambda, &lipschitz_init, &cfg,
                                            stream, &st);
         t_slab_member = false;
+        t_force_ncp = 0;
         if (r != FOE_OK) return cleanup(r);
         cudaStreamSynchronize(st->s);
         cudaStreamDestroy(st->s);

@@ -83,6 +83,7 @@ struct K1Args {
     // tc_rem + 4C lanes), instead of one mostly idle tile per band
     int tc_rem, tc_spt;
     int tc_rows;            // K8 v7 (streamed u tile): output rows per tile (v3: the 64 of kTcR)
+    int ncp;                // K1 v2: filter pairs per shared-memory chunk (1 or 2; 0 = 2)
     // HVP only
     const double* v;        // [B][H][W]
     const float* gw;        // [B][H][W] gradient at w

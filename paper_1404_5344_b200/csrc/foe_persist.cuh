@@ -51,20 +51,19 @@ __device__ __forceinline__ unsigned long long global_ns() {
 }
 
 // Sense-free grid barrier on a monotone arrival counter (all CTAs co-resident: cooperative
-// launch).  Release: the arriving thread's fence after the CTA barrier orders the CTA's
-// writes before its arrival; acquire: the fence after the spin orders later reads after it.
+// launch).  The CTA barrier orders the CTA's writes before thread 0's arrival, a release-ordered
+// atomic add at GPU scope publishes them (cumulatively); thread 0 spins with acquire loads, and
+// the closing CTA barrier orders every thread's later reads after that acquire.
 __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks, unsigned int& gen) {
     __syncthreads();
     gen += 1;
     if (threadIdx.x == 0) {
-        __threadfence();
-        atomicAdd(bar, 1u);
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
         const unsigned int target = gen * nblocks;
         unsigned int v;
         do {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
         } while (v < target);
-        __threadfence();
     }
     __syncthreads();
 }
