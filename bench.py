@@ -208,7 +208,17 @@ def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cf
             micro = json.load(fh)
     except Exception:
         pass
-    common = {"achieved": alg_tflops, "unit": "TFLOP/s", "traffic": args.traffic_bytes,
+    traffic, traffic_src = args.traffic_bytes, "--traffic-bytes" if args.traffic_bytes else None
+    if traffic is None:   # DRAM bytes per launch from the committed ncu --set full capture of this kernel
+        try:
+            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+                tr = json.load(fh)
+            key = "persistent" if persistent else ("k8" if stencil == 2 else "k1")
+            if key in tr and (cfg.name == tr[key].get("config")):
+                traffic, traffic_src = tr[key]["bytes_per_launch"], tr[key]["source"]
+        except Exception:
+            pass
+    common = {"achieved": alg_tflops, "unit": "TFLOP/s", "traffic": traffic, "traffic_source": traffic_src,
               "fp32_peak": fp32_peak, "fp32_frac": (alg_tflops / fp32_peak) if alg_tflops else None,
               "k_ms_per_launch": k_ms / max(k_launches, 1), "k_launches": k_launches,
               "k_share_of_step": (k_ms / sum(step_ms)) if step_ms else None}
