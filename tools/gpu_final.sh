@@ -18,7 +18,7 @@ timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --l
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_launch.log 2>&1; echo "ncu-launch rc=$?" >> $OUT/rc.txt
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_prior_grad_tc -s 5 -c 1 \
   -o $OUT/k8 python bench.py --steps 1 --warmup 3 --iters 5 --no-e2e --no-cpu-baseline > $OUT/ncu_k8.log 2>&1; echo "ncu-k8 rc=$?" >> $OUT/rc.txt
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_inertial_prox -s 5 -c 1 \
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_inertial_prox -s 2 -c 1 \
   -o $OUT/k2 python bench.py --steps 1 --warmup 3 --iters 5 --no-e2e --no-cpu-baseline > $OUT/ncu_k2.log 2>&1; echo "ncu-k2 rc=$?" >> $OUT/rc.txt
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_ipiano_persistent -c 1 \
   -o $OUT/kp python bench.py --config c2 --steps 1 --warmup 1 --iters 20 --no-e2e --no-cpu-baseline > $OUT/ncu_kp.log 2>&1; echo "ncu-persistent rc=$?" >> $OUT/rc.txt
