@@ -444,6 +444,7 @@ void foe_model_destroy(foe_model* model) {
     delete model->tp;
     delete model->tp2;
     delete model;
+    cudaGetLastError();   // destroy reports nothing: leave no stale error for the next launch check
 }
 
 }  // extern "C"
@@ -957,6 +958,8 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
         const dim3 g2(st->nblk2, st->B);
         if (st->pxt2 == 1) foe::k_inertial_prox<1><<<g2, kThreads, 0, s>>>(a2);
         else if (st->pxt2 == 4) foe::k_inertial_prox<4><<<g2, kThreads, 0, s>>>(a2);
+        else if (st->pxt2 == 16) foe::k_inertial_prox<16><<<g2, kThreads, 0, s>>>(a2);
+        else if (st->pxt2 == 32) foe::k_inertial_prox<32><<<g2, kThreads, 0, s>>>(a2);
         else foe::k_inertial_prox<kPxt2><<<g2, kThreads, 0, s>>>(a2);
         count_launch(1);
         CKL("k_inertial_prox");
@@ -1185,6 +1188,7 @@ void ipiano_state_destroy(ipiano_state* st) {
     if (st->sync_ev) cudaEventDestroy(st->sync_ev);
     if (st->s) cudaStreamDestroy(st->s);
     delete st;
+    cudaGetLastError();   // (as ipiano_slabs_destroy)
 }
 
 foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H, int W,
@@ -1266,9 +1270,13 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     st->nchunks = pl.kind == FOE_STENCIL_FFMA ? pl.nchunks : div_up(md->nf, Tr<7>::NC);
     st->groups = pl.groups;
     st->pxt2 = kPxt2;
+    // 16 pixels per thread halve the per-pixel share of K2's block reduction (c4: 223 -> 213 us)
+    // when the launch still has >= 4 blocks per SM; slab members keep kPxt2 (whole K2 blocks per
+    // 64-row band for W % 32 == 0)
+    if (!t_slab_member && (long long)B * H * W >= 4LL * md->nsm * kThreads * 16) st->pxt2 = 16;
     if (const char* px = std::getenv("FOE_K2_PXT")) {   // tuning knob (A/B of K2's pixels per thread)
         const int v = std::atoi(px);
-        if (v == 1 || v == 4 || v == 8) st->pxt2 = v;
+        if (v == 1 || v == 4 || v == 8 || v == 16 || v == 32) st->pxt2 = v;
     }
     if (want_persist && pl.kind == FOE_STENCIL_FFMA) {
         // K2 items: one pixel per thread while the grid can hold them all, else four
@@ -1917,6 +1925,7 @@ foe_status foe_comm_create(const void* id, int nranks, int rank, int cuda_device
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
     ncclResult_t r = api.CommInitRank(&c->comm, nranks, uid, rank);
+    cudaGetLastError();   // NCCL's own runtime probes may leave a stale error in this thread
     if (r != ncclSuccess) { delete c; return nccl_fail(r, "ncclCommInitRank", __LINE__); }
     c->nranks = nranks;
     c->rank = rank;
@@ -1930,6 +1939,7 @@ void foe_comm_destroy(foe_comm* c) {
     const NcclApi& api = nccl_api();
     if (c->comm && api.ok) api.CommDestroy(c->comm);
     delete c;
+    cudaGetLastError();   // NCCL's own runtime calls may leave a stale error in this thread
 }
 
 void ipiano_slabs_destroy(ipiano_slabs* g) {
@@ -1950,6 +1960,7 @@ void ipiano_slabs_destroy(ipiano_slabs* g) {
     if (g->sync_ev) cudaEventDestroy(g->sync_ev);
     if (g->s) cudaStreamDestroy(g->s);
     delete g;
+    cudaGetLastError();   // destroy reports nothing: leave no stale error for the next launch check
 }
 
 foe_status ipiano_slabs_create(const foe_model* md, const float* f, int H_global, int W, int nslabs,
