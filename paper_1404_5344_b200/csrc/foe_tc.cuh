@@ -32,6 +32,11 @@
 #include "foe_kernels.cuh"
 #include "tc_ptx.cuh"
 
+// rows of the u tile a warp stages at a time (their loads all in flight before the exponentials)
+#ifndef FOE_STAGE_ROWS
+#define FOE_STAGE_ROWS 2
+#endif
+
 // 1: K8's epilogue takes one MUFU reciprocal per filter pair (the XU pipe is K8's busiest
 // thread-work pipe); 0: one per filter
 #ifndef FOE_K8_PAIR_RCP
@@ -115,20 +120,31 @@ __device__ __forceinline__ void tc_stage_u(float* us, const double* w, const dou
     int gx[NX];
 #pragma unroll
     for (int k = 0; k < NX; ++k) gx[k] = wrap_idx(x0 - c2 + lane + 32 * k, W);
-    for (int uy = warp; uy < UY; uy += NWARPS) {
-        const int y = y0 - c2 + uy;
-        const double* src;
-        if (halo == nullptr) src = w + (size_t)wrap_idx(y, H) * W;
-        else if (y < 0) src = halo + (size_t)(kHalo + y) * W;
-        else if (y >= H) src = halo + (size_t)(kHalo + y - H) * W;
-        else src = w + (size_t)y * W;
-        double v[NX];
+    // FOE_STAGE_ROWS rows per warp in flight (all their loads issued before any exponential)
+    constexpr int NRB = FOE_STAGE_ROWS;
+    for (int uy0 = warp * NRB; uy0 < UY; uy0 += NWARPS * NRB) {
+        double v[NRB][NX];
 #pragma unroll
-        for (int k = 0; k < NX; ++k) v[k] = (lane + 32 * k < UX) ? src[gx[k]] : wc;
+        for (int r = 0; r < NRB; ++r) {
+            const int uy = uy0 + r;
+            const int y = y0 - c2 + uy;
+            const double* src;
+            if (halo == nullptr) src = w + (size_t)wrap_idx(y, H) * W;
+            else if (y < 0) src = halo + (size_t)(kHalo + y) * W;
+            else if (y >= H) src = halo + (size_t)(kHalo + y - H) * W;
+            else src = w + (size_t)y * W;
 #pragma unroll
-        for (int k = 0; k < NX; ++k) {
-            const int ux = lane + 32 * k;
-            if (ux < UX) us[uy * UP + ux] = udom ? (float)(v[k] - (double)cst) : cst * expm1f((float)(v[k] - wc));
+            for (int k = 0; k < NX; ++k) v[r][k] = (uy < UY && lane + 32 * k < UX) ? src[gx[k]] : wc;
+        }
+#pragma unroll
+        for (int r = 0; r < NRB; ++r) {
+            const int uy = uy0 + r;
+            if (uy >= UY) break;
+#pragma unroll
+            for (int k = 0; k < NX; ++k) {
+                const int ux = lane + 32 * k;
+                if (ux < UX) us[uy * UP + ux] = udom ? (float)(v[r][k] - (double)cst) : cst * expm1f((float)(v[r][k] - wc));
+            }
         }
     }
 }
