@@ -85,6 +85,7 @@ struct TcGeom {
     static_assert(NB <= NP && TAPS - NB == 1, "one CUDA-core tap, Z inside D");
     static_assert(TCOLS_USED <= 512, "TMEM budget");
     static_assert(NP % 16 == 0 && KT % 8 == 0, "MMA shape");
+    static_assert((B_FLOATS * 4) % 16 == 0, "B images: one TMA bulk copy (multiple of 16 bytes)");
 };
 
 // Per-filter constants of K8's epilogue, in the kernel-parameter constant bank (FFMA operands
@@ -320,6 +321,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
     float* ths = sm + G::SM_TH;
     __shared__ uint32_t tbase_s;
     __shared__ __align__(8) uint64_t mbar_f, mbar_b;   // forward / backward MMA completion
+    __shared__ __align__(8) uint64_t mbar_bimg;        // TMA bulk copy of the B images
     __shared__ double red[32];
 
     const K1Args& args = ta.k;
@@ -365,13 +367,10 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
     if (t == 0) {
         tc::mbar_init(&mbar_f, 1);
         tc::mbar_init(&mbar_b, 1);
+        tc::mbar_init(&mbar_bimg, 1);
         tc::mbar_fence_init();
-    }
-    {
-        const float4* src = reinterpret_cast<const float4*>(ta.bimg);
-        float4* dst = reinterpret_cast<float4*>(bsm);
-#pragma unroll 4
-        for (int i = t; i < G::B_FLOATS / 4; i += 256) dst[i] = __ldg(src + i);
+        // the B images (taps, hi/lo, K-major) by one TMA bulk copy, overlapped with the u staging
+        tc::bulk_g2s(bsm, ta.bimg, (uint32_t)(G::B_FLOATS * 4), &mbar_bimg);
     }
     const int yc = min(y0 + R / 2, H - 1), xc = min(x0 + (packed ? args.tc_rem : G::OW) / 2, W - 1);
     // u - c = c (e^{w - w_c} - 1) with c = e^{w_c} at a pixel of the tile: one fp64 exp per CTA,
@@ -448,6 +447,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
     tc::fence_before_sync();
     __syncthreads();
     tc::fence_after_sync();
+    tc::mbar_wait(&mbar_bimg, 0);   // B images landed (async proxy; read by the MMAs and kbl below)
     const uint32_t tb = tbase_s;
     const uint32_t tl = tb + ((uint32_t)((warp & 3) * 32) << 16);   // this warp's TMEM lane base
     const uint32_t idf = tc::idesc_tf32(128, NP);              // forward: N = filters

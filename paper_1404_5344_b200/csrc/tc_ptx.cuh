@@ -144,6 +144,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
 }
 
 // arrive (count 1) on an mbarrier from a thread (release at CTA scope)
+// TMA bulk copy (1-D, no tensor map): bytes (multiple of 16, 16-B aligned ends) from global to
+// this CTA's shared memory, completing on mbar; the issuing thread first arms mbar with the
+// byte count (arrive + expect_tx)
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* mbar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(smem_dst)),
+                 "l"(gmem_src), "r"(bytes), "r"(smem_u32(mbar))
+                 : "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
     asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(smem_u32(mbar))
                  : "memory");
