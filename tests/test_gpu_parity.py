@@ -403,3 +403,46 @@ def test_c4_bench_launch_config_full_trajectory_P3():
         assert abs(oracle.psnr(u[b], clean) - oracle.psnr(ref["u"], clean)) <= 0.01
         np.testing.assert_array_equal(tr[b, 1:, 3], ref["trace"][1:, 3])
         np.testing.assert_array_equal(tr[b, 1:, 4], ref["trace"][1:, 4])
+
+
+def test_c4_teacher_forced_P2_every_10():
+    """P2 at the bench's launch configuration (k = 10 on c4): the full c4 batch
+    (64 x 512^2, AUTO stencil -> K8 with packed tiles, K2 at 16 px/thread) advanced one accepted
+    iteration at a time; at iterations 10, 20, 30 the oracle redoes the next iteration of images
+    0 and 37 from the GPU's own state (w_n, w_{n-1}, L_n): update w+ - w within 1e-5 relative L2
+    and the same trial count unless the margin is a near-tie."""
+    cfg = S.config("c4")
+    d = S.make_inputs(cfg)
+    v0 = S.lipschitz_start_vector(cfg.B, cfg.H, cfg.W)
+    md = _model(d["filters"], d["theta"], lam=tuple(d["lambdas"][0]))
+    _, L0 = P.foe_estimate_lipschitz(md, _cuda(d["f"], torch.float32), _cuda(v0, torch.float64), 25)
+    st = P.ipiano_state_create(md, _cuda(d["f"], torch.float32), d["lambdas"], L0,
+                               P.ipiano_config_default(max_iters=31))
+    assert P.ipiano_state_stencil(st) == P.FOE_STENCIL_TENSOR
+    imgs = (0, 37)
+    w_prev = None
+    w_cur = P.ipiano_get_iterate(st, want_u=False)[0].cpu().numpy()[list(imgs)]
+    for n in range(31):
+        if n in (10, 20, 30):
+            L = P.ipiano_get_counters(st)["L"]
+            P.ipiano_step(st)
+            w_next = P.ipiano_get_iterate(st, want_u=False)[0].cpu().numpy()[list(imgs)]
+            tr = P.ipiano_get_trace(st)
+            for k, b in enumerate(imgs):
+                f = d["f"][b]
+                l1, l2 = d["lambdas"][b]
+                F, g = oracle.energy_grad_w(w_cur[k], d["filters"], d["theta"])
+                Lb, trials = L[b], 0
+                while True:
+                    trials += 1
+                    r = oracle.ipiano_trial(w_cur[k], w_prev[k], g, F, Lb, f, d["filters"], d["theta"], l1, l2,
+                                            oracle.make_cfg(Lb, 1))
+                    if r["accepted"]:
+                        break
+                    Lb *= 2
+                assert trials == tr[b, n + 1, 4] or abs(r["margin"]) < 1e-6 * abs(F), (n, b)
+                assert rel_l2(w_next[k] - w_cur[k], r["wplus"] - w_cur[k]) <= 1e-5, (n, b)
+        else:
+            P.ipiano_step(st)
+            w_next = P.ipiano_get_iterate(st, want_u=False)[0].cpu().numpy()[list(imgs)]
+        w_prev, w_cur = w_cur, w_next
