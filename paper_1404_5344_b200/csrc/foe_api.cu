@@ -367,6 +367,17 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
         return fail(FOE_ERR_CUDA, "libfoe is built for sm_100a (B200); device %d is sm_%d%d", cuda_device,
                     prop.major, prop.minor);
     CK(cudaSetDevice(cuda_device));
+    {   // the per-call scratch of foe_energy_grad / foe_hvp / foe_estimate_lipschitz comes from the
+        // device's stream-ordered pool: keep up to 256 MB of it mapped between calls instead of
+        // returning it to the driver at every synchronisation (remapping cost ~0.2-1 ms per call)
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
+            uint64_t keep = 256ull << 20, cur = 0;
+            if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur) == cudaSuccess && cur < keep)
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    }
     if (tc_np(m, n_filters) == 48) CK((tc_set_attr<7, 48>()));
     if (tc_np(m, n_filters) == 32) CK((tc_set_attr<5, 32>()));
     switch (m) {
