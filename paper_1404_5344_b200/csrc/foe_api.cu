@@ -34,6 +34,7 @@ std::atomic<long long> g_launches{0};  // kernels launched by this library (proc
 thread_local bool t_capturing = false;   // graph capture: replays are counted instead
 thread_local bool t_slab_member = false; // ipiano_slabs_create is creating its member states
 thread_local int t_force_ncp = 0;        // ... with the whole scene's K1 chunk size
+thread_local int t_force_pxt = 0;        // ... and the group's K2 pixels per thread
 inline void count_launch(long long n) {
     if (!t_capturing) g_launches.fetch_add(n, std::memory_order_relaxed);
 }
@@ -1285,6 +1286,7 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     // when the launch still has >= 4 blocks per SM; slab members keep kPxt2 (whole K2 blocks per
     // 64-row band for W % 32 == 0)
     if (!t_slab_member && (long long)B * H * W >= 4LL * md->nsm * kThreads * 16) st->pxt2 = 16;
+    if (t_slab_member && t_force_pxt > 0) st->pxt2 = t_force_pxt;
     if (const char* px = std::getenv("FOE_K2_PXT")) {   // tuning knob (A/B of K2's pixels per thread)
         const int v = std::atoi(px);
         if (v == 1 || v == 4 || v == 8 || v == 16 || v == 32) st->pxt2 = v;
@@ -1662,7 +1664,7 @@ struct ipiano_slabs {
     const foe_comm* comm = nullptr;        // nullptr: all slabs in this process
     int nslabs = 1, first = 0;             // global slab index of members[0]
     int Hs = 0, W = 0, Hg = 0;             // slab rows, columns, scene rows
-    int nb_local = 0, nb_global = 0, e_per_band = 0, bpb = 0;
+    int nb_local = 0, nb_global = 0, e_per_band = 0, bpb = 0, pxt = 8;
     std::vector<ipiano_state*> members;    // slabs owned by this process, in ring order
     double* band_all = nullptr;            // [nb_global][kNumPart]
     double* halo = nullptr;                // [members][2][kHalo][W] received ghost rows
@@ -1722,7 +1724,8 @@ foe_status slab_k2(ipiano_slabs* g, int j) {
     a2.halo_sys_fence = g->p2p && g->comm && g->comm->nranks > 1;
     a2.halo_px = (size_t)foe::kHalo * g->W;
     a2.idiv = st->model->term == FOE_DATA_IDIV;
-    foe::k_inertial_prox<kPxt2><<<dim3(st->nblk2, 1), kThreads, 0, g->s>>>(a2);
+    if (st->pxt2 == 16) foe::k_inertial_prox<16><<<dim3(st->nblk2, 1), kThreads, 0, g->s>>>(a2);
+    else foe::k_inertial_prox<kPxt2><<<dim3(st->nblk2, 1), kThreads, 0, g->s>>>(a2);
     count_launch(1);
     CKL("k_inertial_prox (slab)");
     return FOE_OK;
@@ -1843,7 +1846,7 @@ foe_status slab_init(ipiano_slabs* g, const float* f, double L_init, cudaStream_
         double *up_dst, *dn_dst;
         halo_dst(g, (int)j, up_dst, dn_dst);
         foe::k_init<<<dim3(st->nblk2, 1), kThreads, 0, g->s>>>(f + j * HWs, st->ft, st->w, HWs, st->ppart, st->nblk2,
-                                                                st->ctl, HWs, kPxt2, up_dst, dn_dst,
+                                                                st->ctl, HWs, st->pxt2, up_dst, dn_dst,
                                                                 (size_t)foe::kHalo * g->W, st->model->term == FOE_DATA_IDIV);
         count_launch(1);
         CKL("k_init (slab)");
@@ -2016,7 +2019,10 @@ foe_status ipiano_slabs_create(const foe_model* md, const float* f, int H_global
     g->nb_local = g->Hs / foe::kBandRows;
     g->nb_global = H_global / foe::kBandRows;
     g->e_per_band = pl.tiles_x * groups;   // K1 and K8 tiles are both 64 rows high: one tile row per band
-    g->bpb = foe::kBandRows * W / (kThreads * kPxt2);
+    // K2 blocks never straddle a 64-row band: 16 pixels per thread when W % 64 == 0 (c5: 8192),
+    // else kPxt2 = 8 (W % 32 == 0 is required)
+    g->pxt = W % 64 == 0 ? 16 : kPxt2;
+    g->bpb = foe::kBandRows * W / (kThreads * g->pxt);
     CK(cudaStreamCreateWithFlags(&g->s, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g->sync_ev, cudaEventDisableTiming));
     const size_t he = halo_elems(g);
@@ -2037,10 +2043,12 @@ foe_status ipiano_slabs_create(const foe_model* md, const float* f, int H_global
         ipiano_state* st = nullptr;
         t_slab_member = true;   // per-band energy partials: no K8 column packing
         t_force_ncp = pl.ncp;   // and the whole scene's K1 chunking, so slabs are G-invariant
+        t_force_pxt = g->pxt;   // and its K2 block size
         foe_status r = ipiano_state_create(md, f + (size_t)j * HWs, 1, g->Hs, W, lambda, &lipschitz_init, &cfg,
                                            stream, &st);
         t_slab_member = false;
         t_force_ncp = 0;
+        t_force_pxt = 0;
         if (r != FOE_OK) return cleanup(r);
         cudaStreamSynchronize(st->s);
         cudaStreamDestroy(st->s);
