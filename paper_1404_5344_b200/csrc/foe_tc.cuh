@@ -525,12 +525,21 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
             //   s[o][ox] += sum_b Z[(jz, ox + b), (a, b)];  acc[k] holds row jz - (a0 + k)
             const int jz = j - 1;
             if (wg == 0) {
+                // two filter rows per FP32x2 add (a, a + 1)
 #pragma unroll
-                for (int a = 0; a < A0; ++a) {
+                for (int a = 0; a + 1 < A0; a += 2) {
+                    float2 sa = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb)
+                        sa = __fadd2_rn(sa, make_float2(zs[(a * M + bb) * L + l + bb], zs[((a + 1) * M + bb) * L + l + bb]));
+                    acc[a] += sa.x;
+                    acc[a + 1] += sa.y;
+                }
+                if constexpr (A0 % 2 == 1) {
                     float sa = 0.f;
 #pragma unroll
-                    for (int bb = 0; bb < M; ++bb) sa += zs[(a * M + bb) * L + l + bb];
-                    acc[a] += sa;
+                    for (int bb = 0; bb < M; ++bb) sa += zs[((A0 - 1) * M + bb) * L + l + bb];
+                    acc[A0 - 1] += sa;
                 }
                 const int o = jz - (A0 - 1);                    // wg0's share of row o is complete
                 if (o >= 0) hand[(o & 7) * L + l] = acc[A0 - 1];
@@ -539,8 +548,21 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_tc(const TcArgs ta, const
                 acc[0] = 0.f;
             } else {
                 const float* zl = zls + (jz & 1) * 2 * L;
+                // rows A0 .. M-2 in FP32x2 pairs (all their taps are in Z), the last row (it holds
+                // the CUDA-core tap) scalar
+                constexpr int NPR = (A1 - 1) / 2;
 #pragma unroll
-                for (int k = 0; k < A1; ++k) {
+                for (int q = 0; q < NPR; ++q) {
+                    const int a = A0 + 2 * q;
+                    float2 sa = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb)
+                        sa = __fadd2_rn(sa, make_float2(zs[(a * M + bb) * L + l + bb], zs[((a + 1) * M + bb) * L + l + bb]));
+                    acc[2 * q] += sa.x;
+                    acc[2 * q + 1] += sa.y;
+                }
+#pragma unroll
+                for (int k = 2 * NPR; k < A1; ++k) {
                     const int a = A0 + k;
                     float sa = 0.f;
 #pragma unroll
