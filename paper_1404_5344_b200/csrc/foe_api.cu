@@ -539,10 +539,14 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
         p.kind = FOE_STENCIL_FFMA;
         p.tiles_x = div_up(W, kTile);
         p.ntiles = p.tiles_x * div_up(H, kTile);
-        // one filter pair per chunk when 2-pair chunks leave most SMs idle (single small images)
+        // one filter pair per chunk for latency-bound launches (fewer than 8 two-pair work items per
+        // SM: single small images; measured on the persistent driver: c2 9.23 -> 8.62 ms, c3 26.76 ->
+        // 26.39 ms per solve), two pairs when the launch is throughput-bound (less staging per flop)
         const int npairs = (md->nf + 1) / 2;
         const long long tiles_grid = (long long)p.tiles_x * div_up(H_grid, kTile) * B;
-        p.ncp = t_force_ncp > 0 ? t_force_ncp : tiles_grid * div_up(npairs, kNCP) < md->nsm ? 1 : kNCP;
+        p.ncp = t_force_ncp > 0 ? t_force_ncp : tiles_grid * div_up(npairs, kNCP) < 8LL * md->nsm ? 1 : kNCP;
+        if (const char* e = std::getenv("FOE_K1_NCP"))   // tuning knob (A/B of the chunk size)
+            if (t_force_ncp == 0 && (e[0] == '1' || e[0] == '2')) p.ncp = e[0] - '0';
         p.nchunks = div_up(npairs, p.ncp);
         p.groups = choose_groups(md, p.tiles_x * div_up(H_grid, kTile), B, req_groups, p.nchunks);
     }
