@@ -26,6 +26,13 @@ namespace foe {
 constexpr int kMaxFilters = 64;
 constexpr int kMaxTaps = 3136;
 constexpr int kThreads = 256;
+#ifndef FOE_K2_UNROLL
+#define FOE_K2_UNROLL 2   // K2 pixels in flight per thread
+#endif
+#ifndef FOE_K2_CTAS
+#define FOE_K2_CTAS 4     // K2 CTAs per SM (64 registers)
+#endif
+constexpr int kK2Unroll = FOE_K2_UNROLL;
 constexpr int kTile = 64;  // output tile side of K1
 constexpr int kNumPart = 8;  // K2 block partials
 constexpr int kHalo = 6;     // ghost rows per side of a row slab (2C for m <= 7)
@@ -875,7 +882,7 @@ __device__ __forceinline__ void inertial_prox_blk(const K2Args& a, const int bx,
     const float* ft = a.ft + (size_t)b * a.HW;
     K2Acc acc;
     const size_t base = (size_t)bx * (kThreads * PXT);
-#pragma unroll 2
+#pragma unroll kK2Unroll
     for (int k = 0; k < PXT; ++k) {
         const size_t p = base + (size_t)k * kThreads + threadIdx.x;
         if (p >= a.HW) break;
@@ -893,7 +900,7 @@ __device__ __forceinline__ void inertial_prox_blk(const K2Args& a, const int bx,
 }
 
 template <int PXT>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, FOE_K2_CTAS)
 k_inertial_prox(const K2Args a) {  // (4 CTAs/SM: <= 64 registers; 3 -> 4 gave 253 -> 222 us, 5 spills)
     inertial_prox_blk<PXT>(a, blockIdx.x, blockIdx.y);
 }
