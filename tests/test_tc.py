@@ -192,3 +192,23 @@ def test_tc_fused_trial_matches_unfused(monkeypatch):
     np.testing.assert_allclose(t0[:, :, 1], t1[:, :, 1], rtol=1e-12)
     for b in range(3):
         assert rel_l2(w1[b], w0[b]) <= 1e-12
+
+
+@pytest.mark.parametrize("variant", ["4", "5", "6", "7"])
+def test_tc_schedule_variants_parity(variant, monkeypatch):
+    """The measured K8 schedules kept as FOE_K8_VARIANT options (warp-specialised,
+    persistent, three warp groups, streamed ring) meet the same bars as the default."""
+    monkeypatch.setenv("FOE_K8_VARIANT", variant)
+    k, th = S.random_filter_bank(48, 7, 2100)
+    rng = np.random.default_rng(2101)
+    B, H, W = 2, 150, 260
+    f = np.stack([S.add_speckle(S.piecewise_smooth_scene(H, W, 60 + b), 3, 70 + b) for b in range(B)])
+    w = np.log(np.maximum(f.astype(np.float64), 1.0)) + 0.01 * rng.standard_normal(f.shape)
+    md = P.foe_model_create(k, th, lam=(310.0, 0.008))
+    P.foe_model_set_stencil(md, TENSOR)
+    Fg, _, g = P.foe_energy_grad(md, _cuda(w, torch.float64))
+    g = g.cpu().numpy()
+    for b in range(B):
+        Fo, go = oracle.energy_grad_w(w[b], k, th)
+        assert rel_l2(g[b], go) <= 1e-5, (variant, b, rel_l2(g[b], go))
+        assert Fg[b] == pytest.approx(Fo, rel=1e-6)
