@@ -163,3 +163,20 @@ def test_persistent_contracts():
     w_prof = P.ipiano_get_iterate(st, want_u=False)[0].cpu().numpy()
     _, w_pers, _, _, _ = _run(md, d, L0, 2, P.FOE_SOLVER_PERSISTENT)
     assert rel_l2(w_prof, w_pers) <= 1e-12
+
+
+def test_persistent_bitwise_deterministic_and_per_image_stops():
+    # the redundant per-CTA decisions and fixed-order reductions: two solves are bitwise equal;
+    # with rel_change_tol, images of a batch stop at different iterations and the others go on
+    cfg, d, md, L0 = _inputs("c4", B=3, H=80, W=96, iters=60)
+    free = _run(md, d, L0, 60, P.FOE_SOLVER_PERSISTENT)
+    relchg = free[3][:, 1:, 7]                      # ||w_n - w_{n-1}|| / max(||w_{n-1}||, 1) per image
+    tol = float(np.sort(relchg[:, 0])[1])           # the middle image's first change: the image with
+                                                    # the smallest first step stops at once, the others run on
+    runs = [_run(md, d, L0, 60, P.FOE_SOLVER_PERSISTENT, rel_change_tol=tol) for _ in range(2)]
+    np.testing.assert_array_equal(runs[0][1], runs[1][1])
+    np.testing.assert_array_equal(runs[0][3], runs[1][3])
+    iters = runs[0][4]["iters"]
+    assert len(set(iters.tolist())) > 1, (iters, relchg[:, :4])
+    g = _run(md, d, L0, 60, P.FOE_SOLVER_GRAPH, rel_change_tol=tol)
+    _same_trajectory(g, runs[0])
