@@ -16,6 +16,13 @@
 
 // 1: round the low part of each 3xTF32 split to tf32 (unbiased); 0: let the tensor core drop its
 // low bits (3 fewer FP32x2 operations per value pair)
+// 1: the 3xTF32 split of the thread-built operands with integer rounding (hi = (bits + 2^12) &
+// ~(2^13 - 1) on the ALU pipe, lo = x - hi): the same round-to-nearest hi as the Veltkamp split
+// below, a shorter dependency chain and the FMA pipe left to the arithmetic (K8 1.212 -> 1.185 ms,
+// K8 vs K1 unchanged at 2.95e-6); 0: the paired-FP32 Veltkamp split
+#ifndef FOE_TF32_SPLIT_INT
+#define FOE_TF32_SPLIT_INT 1
+#endif
 #ifndef FOE_TF32_LO_ROUND
 #define FOE_TF32_LO_ROUND 0
 #endif
@@ -205,6 +212,13 @@ __device__ __forceinline__ float2 fmul2_nocontract(float2 a, float2 b) {
 }
 
 __device__ __forceinline__ void tf32_split2(float2 x, float2& hi, float2& lo) {
+#if FOE_TF32_SPLIT_INT
+    // hi = x rounded to tf32 by integer ops (ALU pipe), lo = x - hi exact (left to the TC)
+    hi = make_float2(__uint_as_float((__float_as_uint(x.x) + 0x1000u) & 0xFFFFE000u),
+                     __uint_as_float((__float_as_uint(x.y) + 0x1000u) & 0xFFFFE000u));
+    lo = __fadd2_rn(x, make_float2(-hi.x, -hi.y));
+    return;
+#endif
     const float2 s = make_float2(8193.0f, 8193.0f);
     const float2 c = fmul2_nocontract(x, s);
     const float2 t = __fadd2_rn(c, make_float2(-x.x, -x.y));
