@@ -90,9 +90,8 @@ def lib():
             L.orc_ipiano_trial.argtypes = [dp, dp, dp, C.c_double, C.c_double, dp, C.c_int, C.c_int,
                                            dp, dp, C.c_int, C.c_int, C.c_double, C.c_double,
                                            C.POINTER(OrcCfg), dp, dp, dp, dp]
-            L.orc_ipiano_run_ex.argtypes = [fp, C.c_int, C.c_int, dp, dp, C.c_int, C.c_int,
-                                            C.c_double, C.c_double, C.POINTER(OrcCfg), C.c_double,
-                                            C.POINTER(C.c_byte), dp, dp, ip, ip, ip]
+            L.orc_ipiano_run.argtypes = [fp, C.c_int, C.c_int, dp, dp, C.c_int, C.c_int,
+                                         C.c_double, C.c_double, C.POINTER(OrcCfg), dp, dp, ip, ip]
             L.orc_estimate_lipschitz.argtypes = [fp, C.c_int, C.c_int, dp, dp, C.c_int, C.c_int,
                                                  dp, C.c_int, dp]
             L.orc_estimate_lipschitz.restype = C.c_double
@@ -239,23 +238,19 @@ def ipiano_trial(w, wprev, g, F, L, f, filters, theta, l1, l2, cfg: OrcCfg):
                 newton=int(out[6]), ww=out[7])
 
 
-def ipiano_run(f, filters, theta, l1, l2, cfg: OrcCfg, follow=None, follow_eps=1e-6):
-    """Algorithm C-0 on one image; returns dict(w, u, trace, iters, trials, status, followed)."""
+def ipiano_run(f, filters, theta, l1, l2, cfg: OrcCfg):
+    """Algorithm C-0 on one image; returns dict(w, u, trace, iters, trials, status)."""
     f = np.ascontiguousarray(f, np.float32)
     H, W = f.shape
     k, th = _d(filters), _d(theta)
     w = np.empty((H, W))
     trace = np.zeros((cfg.max_iters + 1, TR_FIELDS))
-    it, tt, nf = C.c_int(), C.c_int(), C.c_int()
-    fol = None
-    if follow is not None:
-        fol_arr = np.ascontiguousarray(follow, np.int8)
-        fol = fol_arr.ctypes.data_as(C.POINTER(C.c_byte))
-    st = lib().orc_ipiano_run_ex(_ptr(f, C.c_float), H, W, _ptr(k), _ptr(th), k.shape[0],
-                                 k.shape[1], float(l1), float(l2), C.byref(cfg), float(follow_eps),
-                                 fol, _ptr(w), _ptr(trace), C.byref(it), C.byref(tt), C.byref(nf))
+    it, tt = C.c_int(), C.c_int()
+    st = lib().orc_ipiano_run(_ptr(f, C.c_float), H, W, _ptr(k), _ptr(th), k.shape[0],
+                              k.shape[1], float(l1), float(l2), C.byref(cfg), _ptr(w), _ptr(trace),
+                              C.byref(it), C.byref(tt))
     return dict(w=w, u=np.exp(w), trace=trace[: it.value + 1], iters=it.value, trials=tt.value,
-                status=st, followed=nf.value)
+                status=st)
 
 
 def estimate_lipschitz(f, filters, theta, v0, iters=25):

@@ -342,14 +342,11 @@ int orc_ipiano_trial(const double* w, const double* wprev, const double* g, doub
 
 /* Full run of algorithm C-0 on one image.  f is the fp32 observation; ft = max(f,1)
  * [R-4]; w^0 = log ft; w^{-1} = w^0 [R-8]; L = L_init.  Writes the final w and the
- * trace [(max_iters+1)][TR_FIELDS].  force (may be NULL): decision-follow mode, see
- * orc_ipiano_run_ex.  Returns ORC_OK or an error code; *iters_run / *total_trials
- * report progress either way. */
-int orc_ipiano_run_ex(const float* f, int H, int W, const double* k, const double* theta,
-                      int nf, int m, double l1, double l2, const orc_cfg* cfg,
-                      double follow_eps, const signed char* follow,
-                      double* w_out, double* trace, int* iters_run, int* total_trials,
-                      int* n_followed)
+ * trace [(max_iters+1)][TR_FIELDS].  Returns ORC_OK or an error code; *iters_run /
+ * *total_trials report progress either way. */
+int orc_ipiano_run(const float* f, int H, int W, const double* k, const double* theta,
+                   int nf, int m, double l1, double l2, const orc_cfg* cfg,
+                   double* w_out, double* trace, int* iters_run, int* total_trials)
 {
     const size_t N = (size_t)H * W;
     double* ft = (double*)malloc(sizeof(double) * N);
@@ -358,7 +355,7 @@ int orc_ipiano_run_ex(const float* f, int H, int W, const double* k, const doubl
     double* wn = (double*)malloc(sizeof(double) * N);
     double* g = (double*)malloc(sizeof(double) * N);
     double* gn = (double*)malloc(sizeof(double) * N);
-    int st = ORC_OK, n = 0, trials_total = 0, followed = 0, trial_idx = 0;
+    int st = ORC_OK, n = 0, trials_total = 0;
     for (size_t p = 0; p < N; ++p) {
         ft[p] = fmax((double)f[p], 1.0);                  /* f~ = max(f,1)   [R-4] */
         w[p] = log(ft[p]);                                /* w^0 = log f~          */
@@ -381,15 +378,7 @@ int orc_ipiano_run_ex(const float* f, int H, int W, const double* k, const doubl
             int ts = orc_ipiano_trial(w, wp, g, F, L, ft, H, W, k, theta, nf, m, l1, l2, cfg,
                                       NULL, wn, gn, out);
             if (ts != ORC_OK) { st = ts; break; }
-            int acc = out[5] != 0.0;
-            /* decision-follow (P3 fallback): adopt the other side's
-             * decision only on a near-tie |margin| < follow_eps * |F| */
-            if (follow && isfinite(out[4]) && fabs(out[4]) < follow_eps * fabs(F)) {
-                int want = follow[trial_idx] > 0;
-                if (want != acc) { acc = want; ++followed; }
-            }
-            ++trial_idx;
-            if (acc) break;
+            if (out[5] != 0.0) break;
             if (trials > cfg->max_backtracks) { st = ORC_ERR_BACKTRACK; break; }
             L *= cfg->backtrack_factor;                   /* double L_n */
         }
@@ -415,18 +404,10 @@ int orc_ipiano_run_ex(const float* f, int H, int W, const double* k, const doubl
     memcpy(w_out, w, sizeof(double) * N);
     if (iters_run) *iters_run = n;
     if (total_trials) *total_trials = trials_total;
-    if (n_followed) *n_followed = followed;
     free(ft); free(w); free(wp); free(wn); free(g); free(gn);
     return st;
 }
 
-int orc_ipiano_run(const float* f, int H, int W, const double* k, const double* theta,
-                   int nf, int m, double l1, double l2, const orc_cfg* cfg,
-                   double* w_out, double* trace, int* iters_run, int* total_trials)
-{
-    return orc_ipiano_run_ex(f, H, W, k, theta, nf, m, l1, l2, cfg, 0.0, NULL,
-                             w_out, trace, iters_run, total_trials, NULL);
-}
 
 /* Lipschitz estimate [R-10]: |Rayleigh quotient| after `iters` power-iteration steps
  * on the prior Hessian at w^0 = log max(f,1), from the start vector v0 (an input):
@@ -544,7 +525,7 @@ int orc_ipiano_trial_u(const double* u, const double* uprev, const double* g, do
 }
 
 /* Full run of model (6): u^0 = f~, u^{-1} = u^0 [R-8], L = L_init; the
- * same backtracking, acceptance, trace and stopping rules as orc_ipiano_run_ex.  The
+ * same backtracking, acceptance, trace and stopping rules as orc_ipiano_run.  The
  * guard [R-11] becomes: an accepted iterate must be finite and positive. */
 int orc_ipiano_run_u(const float* f, int H, int W, const double* k, const double* theta,
                      int nf, int m, double lam, const orc_cfg* cfg,

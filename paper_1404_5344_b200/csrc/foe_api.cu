@@ -127,38 +127,9 @@ constexpr int kTcR = 64;
 template <int M, int NP>
 constexpr int tc_smem() { return foe::TcGeom<M, NP, kTcR>::SMEM_BYTES; }
 template <int M, int NP>
-constexpr int tc4_smem() { return foe::Tc4Geom<M, NP, kTcR>::SMEM_BYTES; }
-template <int M, int NP>
 cudaError_t tc_set_attr() {
-    cudaError_t e = cudaFuncSetAttribute(foe::k_prior_grad_tc<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         tc_smem<M, NP>());
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(foe::k_prior_grad_tc<M, NP, kTcR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tc_smem<M, NP>());
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(foe::k_prior_grad_tc4<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tc4_smem<M, NP>());
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(foe::k_prior_grad_tc6<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             foe::Tc3Geom<M, NP, kTcR>::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(foe::k_prior_grad_tc7<M, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             foe::Tc7Geom<M, NP>::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(foe::k_prior_grad_tc5<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                foe::Tc5Geom<M, NP, kTcR>::SMEM_BYTES);
-}
-// K8 variant (ncu, one c4 launch): 3 = two lock-step CTAs per SM (default, 1.43 ms), 4 = warp-
-// specialised single-CTA pipeline (1.49 ms; FOE_K8_VARIANT=4), 5 = the pipeline persistent over
-// tiles (no gain over 4; FOE_K8_VARIANT=5)
-int tc_variant() {
-    const char* e = std::getenv("FOE_K8_VARIANT");   // read per launch (A/B in one process)
-    if (e && e[0] == '4') return 4;
-    if (e && e[0] == '5') return 5;
-    if (e && e[0] == '6') return 6;
-    if (e && e[0] == '7') return 7;
-    if (e && e[0] == 'k' && e[1] >= '1' && e[1] <= '4') return 40 + (e[1] - '0');   // profiling knockouts
-    return 3;
+    return cudaFuncSetAttribute(foe::k_prior_grad_tc<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                tc_smem<M, NP>());
 }
 // the banks K8 has an instantiation for: (m, padded N_f)
 int tc_np(int m, int nf) {
@@ -188,6 +159,8 @@ struct foe_model {
     float* tc_thl = nullptr;
     foe::TcConst* tc_const = nullptr;  // per-filter epilogue constants, passed by value to K8
     int stencil = FOE_STENCIL_AUTO; // foe_energy_grad's choice
+    bool persist_phases = false;
+    cudaMemPool_t pool = nullptr;   // private stream-ordered pool of the per-call scratch    // FOE_PERSIST_PHASES=1 (read once here): persistent-driver phase timings
     // ipiano_run's reusable workspace (one solver state + host-I/O staging buffers), kept for
     // repeated calls of the same shape and configuration; guarded by run_mu (a concurrent call
     // falls back to a private workspace)
@@ -210,8 +183,7 @@ struct ipiano_state {
     int kind = FOE_STENCIL_FFMA;  // resolved stencil of this state (K1 or K8)
     int tc_rem = 0, tc_spt = 0;   // K8 column packing of this state's plan
     int tc_rows = 64;             // K8 output rows per tile
-    bool fused = false;           // trial = one K8 launch with K2 inside its staging (+ K3)
-    int nblk3 = 0;                // test partials per image K3 sums (K2 blocks, or K8 tiles if fused)
+    int nblk3 = 0;                // test partials per image K3 sums (= the K2 blocks)
     int solver = FOE_SOLVER_GRAPH;  // resolved trial-loop driver
     int pgrid = 0;                // persistent driver: co-resident CTAs
     unsigned int* bar = nullptr;  // persistent driver: grid barrier counter
@@ -368,17 +340,6 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
         return fail(FOE_ERR_CUDA, "libfoe is built for sm_100a (B200); device %d is sm_%d%d", cuda_device,
                     prop.major, prop.minor);
     CK(cudaSetDevice(cuda_device));
-    {   // the per-call scratch of foe_energy_grad / foe_hvp / foe_estimate_lipschitz comes from the
-        // device's stream-ordered pool: keep up to 256 MB of it mapped between calls instead of
-        // returning it to the driver at every synchronisation (remapping cost ~0.2-1 ms per call)
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
-            uint64_t keep = 256ull << 20, cur = 0;
-            if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur) == cudaSuccess && cur < keep)
-                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-        cudaGetLastError();
-    }
     if (tc_np(m, n_filters) == 48) CK((tc_set_attr<7, 48>()));
     if (tc_np(m, n_filters) == 32) CK((tc_set_attr<5, 32>()));
     switch (m) {
@@ -395,10 +356,30 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
     std::memset(md->tp, 0, sizeof(TapParams));
     std::memset(md->tp2, 0, sizeof(foe::TapParams2));
     md->dev = cuda_device;
+    {   // the per-call scratch of foe_energy_grad / foe_hvp / foe_estimate_lipschitz / ipiano_run comes
+        // from a stream-ordered pool private to the model (the device's default pool and its release
+        // threshold are left alone): up to 256 MB stay mapped between calls instead of going back to
+        // the driver at every synchronisation (remapping cost ~0.2-1 ms per call)
+        cudaMemPoolProps pp{};
+        pp.allocType = cudaMemAllocationTypePinned;
+        pp.location.type = cudaMemLocationTypeDevice;
+        pp.location.id = cuda_device;
+        if (cudaMemPoolCreate(&md->pool, &pp) != cudaSuccess) {
+            delete md->tp; delete md->tp2; delete md;
+            return fail(FOE_ERR_CUDA, "cudaMemPoolCreate failed");
+        }
+        uint64_t keep = 256ull << 20;
+        cudaMemPoolSetAttribute(md->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        cudaGetLastError();
+    }
     md->nf = n_filters;
     md->m = m;
     md->nsm = prop.multiProcessorCount;
     md->term = term;
+    {
+        const char* ph = std::getenv("FOE_PERSIST_PHASES");   // diagnostics only, read once
+        md->persist_phases = ph != nullptr && ph[0] == '1';
+    }
     md->lam[0] = lam[0];
     md->lam[1] = lam[1];
     for (int i = 0; i < n_filters; ++i) {
@@ -452,6 +433,8 @@ void foe_model_destroy(foe_model* model) {
     if (model->tc_bimg) cudaFree(model->tc_bimg);
     if (model->tc_sumk) cudaFree(model->tc_sumk);
     if (model->tc_thl) cudaFree(model->tc_thl);
+    // outstanding stream-ordered frees are honoured: the pool is released once they land
+    if (model->pool) cudaMemPoolDestroy(model->pool);
     delete model->tc_const;
     delete model->tp;
     delete model->tp2;
@@ -503,37 +486,18 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
         // one packed tile (not for row slabs, whose energy partials are per 64-row band).  v7
         // (streamed u tile) takes R from {64, 128, 256}: fewest waves x response rows per tile.
         const bool pack_ok = allow_pack && H_grid == H;
-        const int var = tc_variant();
-        const bool v7 = var == 7 && pack_ok;
-        auto tiling = [&](int R, Plan& q) {
-            int nfull = W / ow, rem = W - nfull * ow, spt = 0;
-            if (rem > 0 && pack_ok && (var == 3 || v7)) {
-                spt = 128 / (rem + 2 * (md->m - 1));
-                if (spt < 2) spt = 0;
-            }
-            if (rem > 0 && spt == 0) { nfull += 1; rem = 0; }
-            const int nbands = div_up(H, R);
-            q.tiles_x = nfull;
-            q.ntiles = nbands * nfull + (rem > 0 ? div_up(nbands, spt) : 0);
-            q.tc_rem = rem;
-            q.tc_spt = spt;
-            q.tc_rows = R;
-        };
-        tiling(kTcR, p);
-        const char* rows_env = std::getenv("FOE_K8_ROWS");   // tuning knob: force v7's R
-        if (v7 && rows_env && (std::atoi(rows_env) == 64 || std::atoi(rows_env) == 128 || std::atoi(rows_env) == 256)) {
-            tiling(std::atoi(rows_env), p);
-        } else if (v7) {
-            const long long slots = 2LL * md->nsm;
-            double best = 1e30;
-            for (int R : {64, 128, 256}) {
-                if (R > 64 && R >= 2 * H) break;
-                Plan q;
-                tiling(R, q);
-                const double cost = std::ceil((double)q.ntiles * B / (double)slots) * (R + md->m - 1);
-                if (cost < best - 1e-9) { best = cost; tiling(R, p); }
-            }
+        int nfull = W / ow, rem = W - nfull * ow, spt = 0;
+        if (rem > 0 && pack_ok) {
+            spt = 128 / (rem + 2 * (md->m - 1));
+            if (spt < 2) spt = 0;
         }
+        if (rem > 0 && spt == 0) { nfull += 1; rem = 0; }
+        const int nbands = div_up(H, kTcR);
+        p.tiles_x = nfull;
+        p.ntiles = nbands * nfull + (rem > 0 ? div_up(nbands, spt) : 0);
+        p.tc_rem = rem;
+        p.tc_spt = spt;
+        p.tc_rows = kTcR;
         p.groups = 1;
     } else {
         p.kind = FOE_STENCIL_FFMA;
@@ -545,8 +509,6 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
         const int npairs = (md->nf + 1) / 2;
         const long long tiles_grid = (long long)p.tiles_x * div_up(H_grid, kTile) * B;
         p.ncp = t_force_ncp > 0 ? t_force_ncp : tiles_grid * div_up(npairs, kNCP) < 8LL * md->nsm ? 1 : kNCP;
-        if (const char* e = std::getenv("FOE_K1_NCP"))   // tuning knob (A/B of the chunk size)
-            if (t_force_ncp == 0 && (e[0] == '1' || e[0] == '2')) p.ncp = e[0] - '0';
         p.nchunks = div_up(npairs, p.ncp);
         p.groups = choose_groups(md, p.tiles_x * div_up(H_grid, kTile), B, req_groups, p.nchunks);
     }
@@ -554,15 +516,7 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
 }
 
 // Launch the prior energy+gradient evaluation `a` (tiling fields taken from the plan).
-// Fused trial (K2 inside K8): f~, test-partial output, solver parameters
-struct FuseArgs {
-    const float* ft;
-    double* ppart;
-    foe::SolverParams sp;
-};
-
-foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStream_t s,
-                        const FuseArgs* fuse = nullptr) {
+foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStream_t s) {
     if (kind == FOE_STENCIL_FFMA) {
         k1_dispatch(md->m, false, a, *md->tp, *md->tp2, dim3(a.ntiles * a.groups, B), s);
         CKL("k_prior_grad2");
@@ -576,67 +530,10 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
     ta.theta_ln2 = md->tc_thl;
     ta.tiles_x = a.tiles_x;
     count_launch(1);
-    if (fuse != nullptr) {   // the default schedule only (the state enables fusion with variant 3)
-        ta.ft = fuse->ft;
-        ta.ppart = fuse->ppart;
-        ta.sp = fuse->sp;
-        if (md->tc_np == 48)
-            foe::k_prior_grad_tc<7, 48, kTcR, true><<<dim3(a.ntiles, B), 256, tc_smem<7, 48>(), s>>>(ta, *md->tc_const);
-        else
-            foe::k_prior_grad_tc<5, 32, kTcR, true><<<dim3(a.ntiles, B), 256, tc_smem<5, 32>(), s>>>(ta, *md->tc_const);
-        CKL("k_prior_grad_tc (fused trial)");
-        return FOE_OK;
-    }
-    constexpr int T4 = foe::Tc4Geom<7, 48, kTcR>::THREADS;
-    int var = tc_variant();
-    if (var == 7 && (a.tc_rows <= 0 || a.halo != nullptr)) var = 3;   // v7: batch path with a planned R
-    if (var != 7 && (a.tc_rem > 0 || (a.tc_rows > 0 && a.tc_rows != kTcR))) var = 3;   // packed: v3 / v7 only
-    if (var == 7) {
-        if (md->tc_np == 48)
-            foe::k_prior_grad_tc7<7, 48><<<dim3(a.ntiles, B), 256, foe::Tc7Geom<7, 48>::SMEM_BYTES, s>>>(ta, *md->tc_const);
-        else
-            foe::k_prior_grad_tc7<5, 32><<<dim3(a.ntiles, B), 256, foe::Tc7Geom<5, 32>::SMEM_BYTES, s>>>(ta, *md->tc_const);
-        CKL("k_prior_grad_tc7");
-        return FOE_OK;
-    }
-    if (var >= 41 && md->tc_np == 48) {   // profiling knockouts (FOE_K8_VARIANT=k1..k4), results invalid
-        static bool attr = false;
-        if (!attr) {
-            attr = true;
-            cudaFuncSetAttribute(foe::k_prior_grad_tc4<7, 48, kTcR, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc4_smem<7, 48>());
-            cudaFuncSetAttribute(foe::k_prior_grad_tc4<7, 48, kTcR, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc4_smem<7, 48>());
-            cudaFuncSetAttribute(foe::k_prior_grad_tc4<7, 48, kTcR, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc4_smem<7, 48>());
-            cudaFuncSetAttribute(foe::k_prior_grad_tc4<7, 48, kTcR, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc4_smem<7, 48>());
-        }
-        const dim3 gr(a.ntiles, B);
-        if (var == 41) foe::k_prior_grad_tc4<7, 48, kTcR, 1><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
-        if (var == 42) foe::k_prior_grad_tc4<7, 48, kTcR, 2><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
-        if (var == 43) foe::k_prior_grad_tc4<7, 48, kTcR, 3><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
-        if (var == 44) foe::k_prior_grad_tc4<7, 48, kTcR, 4><<<gr, T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
-    } else if (var == 6) {
-        if (md->tc_np == 48)
-            foe::k_prior_grad_tc6<7, 48, kTcR><<<dim3(a.ntiles, B), 384, foe::Tc3Geom<7, 48, kTcR>::SMEM_BYTES, s>>>(ta, *md->tc_const);
-        else
-            foe::k_prior_grad_tc6<5, 32, kTcR><<<dim3(a.ntiles, B), 384, foe::Tc3Geom<5, 32, kTcR>::SMEM_BYTES, s>>>(ta, *md->tc_const);
-    } else if (var == 5) {
-        ta.nimg = B;
-        const int items = a.ntiles * B;
-        const int grid = std::max(1, std::min(items, md->nsm));
-        constexpr int T5 = foe::Tc5Geom<7, 48, kTcR>::THREADS;
-        if (md->tc_np == 48)
-            foe::k_prior_grad_tc5<7, 48, kTcR><<<dim3(grid, 1), T5, foe::Tc5Geom<7, 48, kTcR>::SMEM_BYTES, s>>>(ta, *md->tc_const);
-        else
-            foe::k_prior_grad_tc5<5, 32, kTcR><<<dim3(grid, 1), T5, foe::Tc5Geom<5, 32, kTcR>::SMEM_BYTES, s>>>(ta, *md->tc_const);
-    } else if (var >= 4) {
-        if (md->tc_np == 48)
-            foe::k_prior_grad_tc4<7, 48, kTcR><<<dim3(a.ntiles, B), T4, tc4_smem<7, 48>(), s>>>(ta, *md->tc_const);
-        else
-            foe::k_prior_grad_tc4<5, 32, kTcR><<<dim3(a.ntiles, B), T4, tc4_smem<5, 32>(), s>>>(ta, *md->tc_const);
-    } else if (md->tc_np == 48) {
+    if (md->tc_np == 48)
         foe::k_prior_grad_tc<7, 48, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<7, 48>(), s>>>(ta, *md->tc_const);
-    } else {
+    else
         foe::k_prior_grad_tc<5, 32, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<5, 32>(), s>>>(ta, *md->tc_const);
-    }
     CKL("k_prior_grad_tc");
     return FOE_OK;
 }
@@ -735,10 +632,10 @@ foe_status foe_energy_grad(const foe_model* md, const double* w, const float* f,
     double* dpart = nullptr;
     double* dlam = nullptr;
     const int nblk = div_up((long long)HW, (long long)kThreads * kPxt2);
-    CK(cudaMallocAsync((void**)&epart, sizeof(double) * B * ne, s));
+    CK(cudaMallocFromPoolAsync((void**)&epart, sizeof(double) * B * ne, md->pool, s));
     const bool direct = (groups == 1 && grad != nullptr);
-    if (!direct) CK(cudaMallocAsync((void**)&gparts, sizeof(float) * groups * B * HW, s));
-    CK(cudaMallocAsync((void**)&dred, sizeof(double) * B * 2, s));
+    if (!direct) CK(cudaMallocFromPoolAsync((void**)&gparts, sizeof(float) * groups * B * HW, md->pool, s));
+    CK(cudaMallocFromPoolAsync((void**)&dred, sizeof(double) * B * 2, md->pool, s));
     st = run_k1_plain(md, w, B, H, W, groups, epart, direct ? grad : gparts, false, nullptr, nullptr, s, pl.kind,
                       pl.tiles_x, pl.ntiles, pl.tc_rem, pl.tc_spt, pl.tc_rows, pl.ncp, pl.nchunks);
     if (st != FOE_OK) return st;
@@ -757,8 +654,8 @@ foe_status foe_energy_grad(const foe_model* md, const double* w, const float* f,
             lam[2 * b] = lambda_per_image ? lambda_per_image[2 * b] : md->lam[0];
             lam[2 * b + 1] = md->term != FOE_DATA_COMBINED ? 0.0 : (lambda_per_image ? lambda_per_image[2 * b + 1] : md->lam[1]);
         }
-        CK(cudaMallocAsync((void**)&dlam, sizeof(double) * 2 * B, s));
-        CK(cudaMallocAsync((void**)&dpart, sizeof(double) * B * nblk, s));
+        CK(cudaMallocFromPoolAsync((void**)&dlam, sizeof(double) * 2 * B, md->pool, s));
+        CK(cudaMallocFromPoolAsync((void**)&dpart, sizeof(double) * B * nblk, md->pool, s));
         CK(cudaMemcpyAsync(dlam, lam.data(), sizeof(double) * 2 * B, cudaMemcpyHostToDevice, s));
         foe::k_data_energy<<<dim3(nblk, B), kThreads, 0, s>>>(w, f, dlam, dpart, nblk, HW, kPxt2,
                                                                md->term == FOE_DATA_IDIV);
@@ -798,8 +695,8 @@ foe_status foe_hvp(const foe_model* md, const double* w, const double* v, int B,
     const int tiles = div_up(W, kTile) * div_up(H, kTile);
     double* epart = nullptr;
     float* gw = nullptr;
-    CK(cudaMallocAsync((void**)&epart, sizeof(double) * B * tiles, s));
-    CK(cudaMallocAsync((void**)&gw, sizeof(float) * n, s));
+    CK(cudaMallocFromPoolAsync((void**)&epart, sizeof(double) * B * tiles, md->pool, s));
+    CK(cudaMallocFromPoolAsync((void**)&gw, sizeof(float) * n, md->pool, s));
     st = run_k1_plain(md, w, B, H, W, 1, epart, gw, false, nullptr, nullptr, s);
     if (st == FOE_OK) st = run_k1_plain(md, w, B, H, W, 1, epart, hv, true, v, gw, s);
     CK(cudaFreeAsync(epart, s));
@@ -820,13 +717,13 @@ foe_status foe_estimate_lipschitz(const foe_model* md, const float* f, int B, in
     const int nblk = div_up((long long)HW, (long long)kThreads * kPxt2);
     double *w0 = nullptr, *v = nullptr, *epart = nullptr, *part = nullptr, *sums = nullptr;
     float *gw = nullptr, *h = nullptr;
-    CK(cudaMallocAsync((void**)&w0, sizeof(double) * n, s));
-    CK(cudaMallocAsync((void**)&v, sizeof(double) * n, s));
-    CK(cudaMallocAsync((void**)&gw, sizeof(float) * n, s));
-    CK(cudaMallocAsync((void**)&h, sizeof(float) * n, s));
-    CK(cudaMallocAsync((void**)&epart, sizeof(double) * B * tiles, s));
-    CK(cudaMallocAsync((void**)&part, sizeof(double) * B * nblk * 3, s));
-    CK(cudaMallocAsync((void**)&sums, sizeof(double) * B * 3, s));
+    CK(cudaMallocFromPoolAsync((void**)&w0, sizeof(double) * n, md->pool, s));
+    CK(cudaMallocFromPoolAsync((void**)&v, sizeof(double) * n, md->pool, s));
+    CK(cudaMallocFromPoolAsync((void**)&gw, sizeof(float) * n, md->pool, s));
+    CK(cudaMallocFromPoolAsync((void**)&h, sizeof(float) * n, md->pool, s));
+    CK(cudaMallocFromPoolAsync((void**)&epart, sizeof(double) * B * tiles, md->pool, s));
+    CK(cudaMallocFromPoolAsync((void**)&part, sizeof(double) * B * nblk * 3, md->pool, s));
+    CK(cudaMallocFromPoolAsync((void**)&sums, sizeof(double) * B * 3, md->pool, s));
     const int eb = div_up((long long)n, 256);
     foe::k_log_ftilde<<<eb, 256, 0, s>>>(f, w0, n, md->term == FOE_DATA_IDIV);
     count_launch(1);
@@ -969,13 +866,12 @@ foe::K3Args state_k3_args(const ipiano_state* st) {
 
 // One trial round for every active image: K2 -> K1 (candidate) -> K3.
 foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
-    if (!st->fused) {
+    {
         const foe::K2Args a2 = state_k2_args(st);
         const dim3 g2(st->nblk2, st->B);
         if (st->pxt2 == 1) foe::k_inertial_prox<1><<<g2, kThreads, 0, s>>>(a2);
         else if (st->pxt2 == 4) foe::k_inertial_prox<4><<<g2, kThreads, 0, s>>>(a2);
         else if (st->pxt2 == 16) foe::k_inertial_prox<16><<<g2, kThreads, 0, s>>>(a2);
-        else if (st->pxt2 == 32) foe::k_inertial_prox<32><<<g2, kThreads, 0, s>>>(a2);
         else foe::k_inertial_prox<kPxt2><<<g2, kThreads, 0, s>>>(a2);
         count_launch(1);
         CKL("k_inertial_prox");
@@ -987,8 +883,7 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
         e1 = pool_event(st);
         CK(cudaEventRecord(e0, s));
     }
-    FuseArgs fz{st->ft, st->ppart, st->sp};
-    foe_status rl = launch_prior(st->model, st->kind, a1, st->B, s, st->fused ? &fz : nullptr);
+    foe_status rl = launch_prior(st->model, st->kind, a1, st->B, s);
     if (rl != FOE_OK) return rl;
     if (timed) {
         CK(cudaEventRecord(e1, s));
@@ -999,7 +894,7 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
     foe::k_decide<<<st->B, kThreads, 0, s>>>(a3);
     count_launch(1);
     CKL("k_decide");
-    st->total_launches += st->fused ? 2 : 3;
+    st->total_launches += 3;
     return FOE_OK;
 }
 
@@ -1099,7 +994,7 @@ foe_status launch_rounds(ipiano_state* st, long long rounds) {
     const int reps = div_up(rounds, st->graph_rounds);
     for (int i = 0; i < reps; ++i) {
         CK(cudaGraphLaunch(st->graph, st->s));
-        const long long per = st->fused ? 2 : 3;
+        const long long per = 3;
         st->total_launches += per * st->graph_rounds;
         count_launch(per * st->graph_rounds);
     }
@@ -1291,10 +1186,6 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     // 64-row band for W % 32 == 0)
     if (!t_slab_member && (long long)B * H * W >= 4LL * md->nsm * kThreads * 16) st->pxt2 = 16;
     if (t_slab_member && t_force_pxt > 0) st->pxt2 = t_force_pxt;
-    if (const char* px = std::getenv("FOE_K2_PXT")) {   // tuning knob (A/B of K2's pixels per thread)
-        const int v = std::atoi(px);
-        if (v == 1 || v == 4 || v == 8 || v == 16 || v == 32) st->pxt2 = v;
-    }
     if (want_persist && pl.kind == FOE_STENCIL_FFMA) {
         // K2 items: one pixel per thread while the grid can hold them all, else four
         const int pxt = npx <= 2LL * md->nsm * kThreads ? 1 : 4;
@@ -1311,14 +1202,7 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
         }
     }
     st->nblk2 = div_up((long long)st->HW, (long long)kThreads * st->pxt2);
-    // fused trial kernel (K2 inside K8's staging): K8 default schedule, batch path; opt-in
-    // (FOE_FUSE_K2=1) until it is measured to win
-    {
-        const char* fz = std::getenv("FOE_FUSE_K2");
-        st->fused = pl.kind == FOE_STENCIL_TENSOR && st->solver == FOE_SOLVER_GRAPH && !t_slab_member &&
-                    tc_variant() == 3 && fz != nullptr && fz[0] == '1';
-    }
-    st->nblk3 = st->fused ? pl.ntiles : st->nblk2;
+    st->nblk3 = st->nblk2;
     auto cleanup = [&](foe_status s) { ipiano_state_destroy(st); return s; };
 #define CKS(call)                                                                    \
     do {                                                                             \
@@ -1332,14 +1216,13 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     CKS(cudaMalloc((void**)&st->g, sizeof(float) * 2 * st->groups * n));
     CKS(cudaMalloc((void**)&st->ft, sizeof(float) * n));
     CKS(cudaMalloc((void**)&st->epart, sizeof(double) * B * st->ntiles * st->groups));
-    CKS(cudaMalloc((void**)&st->ppart, sizeof(double) * 2 * B * std::max(st->nblk2, st->nblk3) * foe::kNumPart));
+    CKS(cudaMalloc((void**)&st->ppart, sizeof(double) * 2 * B * st->nblk2 * foe::kNumPart));
     CKS(cudaMalloc((void**)&st->trace, sizeof(double) * B * (cfg.max_iters + 1) * 8));
     CKS(cudaMemset(st->trace, 0, sizeof(double) * B * (cfg.max_iters + 1) * 8));
     CKS(cudaMalloc((void**)&st->ctl, sizeof(ImgCtl) * B * std::max(1, st->pgrid)));
     if (st->solver == FOE_SOLVER_PERSISTENT) {
         CKS(cudaMalloc((void**)&st->bar, sizeof(unsigned int)));
-        const char* ph = std::getenv("FOE_PERSIST_PHASES");
-        if (ph && ph[0] == '1') {
+        if (md->persist_phases) {
             CKS(cudaMalloc((void**)&st->phase_ns, sizeof(unsigned long long) * 4 * foe::kPhaseRounds));
             CKS(cudaMemset(st->phase_ns, 0, sizeof(unsigned long long) * 4 * foe::kPhaseRounds));
         }
@@ -1538,7 +1421,7 @@ foe_status ipiano_run(const foe_model* md, const float* f, int B, int H, int W, 
             df = md->io_buf;
             du = md->io_buf + md->io_n;
         } else {
-            CK(cudaMallocAsync((void**)&df, sizeof(float) * 2 * n, s));
+            CK(cudaMallocFromPoolAsync((void**)&df, sizeof(float) * 2 * n, md->pool, s));
             du = df + n;
         }
     }

@@ -59,11 +59,12 @@ __device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nbl
     gen += 1;
     if (threadIdx.x == 0) {
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        // modular target and a wrap-safe comparison: the counter may wrap past 2^32 on long solves
         const unsigned int target = gen * nblocks;
         unsigned int v;
         do {
             asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-        } while (v < target);
+        } while ((int)(v - target) < 0);
     }
     __syncthreads();
 }

@@ -166,49 +166,3 @@ def test_tc_slabs_bitwise_g_invariant():
         np.testing.assert_array_equal(tr, outs[0][1])
     ref = oracle.ipiano_run(f, k, th, 160.0, 0.004, oracle.make_cfg(2.0 ** 18, 15))
     assert rel_l2(np.exp(outs[0][0]), ref["u"]) <= 1e-4
-
-
-def test_tc_fused_trial_matches_unfused(monkeypatch):
-    """The fused trial kernel (FOE_FUSE_K2=1: K2's inertial point + prox computed inside K8's
-    staging, the test partials per tile) against the default K2 -> K8 sequence: the same w+
-    arithmetic (k2_pixel), so identical decisions and iterates equal to fp64 rounding of the
-    reordered test sums; packed and ragged tiles (3 images of 150 x 260, mixed looks)."""
-    cfg = S.config("c4", B=3, H=150, W=260, iters=12)
-    d = S.make_inputs(cfg)
-    md = P.foe_model_create(d["filters"], d["theta"], lam=tuple(d["lambdas"][0]))
-    L0 = np.full(3, 2.0 ** 17)
-    runs = []
-    for fuse in ("0", "1"):
-        monkeypatch.setenv("FOE_FUSE_K2", fuse)
-        st = P.ipiano_state_create(md, _cuda(d["f"], torch.float32), d["lambdas"], L0,
-                                   P.ipiano_config_default(max_iters=cfg.iters, stencil=TENSOR))
-        P.ipiano_solve(st)
-        runs.append((P.ipiano_get_iterate(st, want_u=False)[0].cpu().numpy(), P.ipiano_get_trace(st),
-                     P.ipiano_get_counters(st)))
-    (w0, t0, c0), (w1, t1, c1) = runs
-    np.testing.assert_array_equal(c0["trials"], c1["trials"])
-    np.testing.assert_array_equal(t0[:, :, 3], t1[:, :, 3])
-    np.testing.assert_array_equal(t0[:, :, 0], t1[:, :, 0])   # F: the same K8 tiles
-    np.testing.assert_allclose(t0[:, :, 1], t1[:, :, 1], rtol=1e-12)
-    for b in range(3):
-        assert rel_l2(w1[b], w0[b]) <= 1e-12
-
-
-@pytest.mark.parametrize("variant", ["4", "5", "6", "7"])
-def test_tc_schedule_variants_parity(variant, monkeypatch):
-    """The measured K8 schedules kept as FOE_K8_VARIANT options (warp-specialised,
-    persistent, three warp groups, streamed ring) meet the same bars as the default."""
-    monkeypatch.setenv("FOE_K8_VARIANT", variant)
-    k, th = S.random_filter_bank(48, 7, 2100)
-    rng = np.random.default_rng(2101)
-    B, H, W = 2, 150, 260
-    f = np.stack([S.add_speckle(S.piecewise_smooth_scene(H, W, 60 + b), 3, 70 + b) for b in range(B)])
-    w = np.log(np.maximum(f.astype(np.float64), 1.0)) + 0.01 * rng.standard_normal(f.shape)
-    md = P.foe_model_create(k, th, lam=(310.0, 0.008))
-    P.foe_model_set_stencil(md, TENSOR)
-    Fg, _, g = P.foe_energy_grad(md, _cuda(w, torch.float64))
-    g = g.cpu().numpy()
-    for b in range(B):
-        Fo, go = oracle.energy_grad_w(w[b], k, th)
-        assert rel_l2(g[b], go) <= 1e-5, (variant, b, rel_l2(g[b], go))
-        assert Fg[b] == pytest.approx(Fo, rel=1e-6)
