@@ -18,6 +18,8 @@
 #include "foe.h"
 #include "foe_kernels.cuh"
 #include "foe_tc.cuh"
+#include "foe_th.cuh"
+#include <cuda_fp16.h>
 #include "foe_eval.cuh"
 #include "foe_persist.cuh"
 
@@ -127,9 +129,14 @@ constexpr int kTcR = 64;
 template <int M, int NP>
 constexpr int tc_smem() { return foe::TcGeom<M, NP, kTcR>::SMEM_BYTES; }
 template <int M, int NP>
+constexpr int th_smem() { return foe::ThGeom<M, NP, kTcR>::SMEM_BYTES; }
+template <int M, int NP>
 cudaError_t tc_set_attr() {
-    return cudaFuncSetAttribute(foe::k_prior_grad_tc<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                tc_smem<M, NP>());
+    cudaError_t e = cudaFuncSetAttribute(foe::k_prior_grad_tc<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         tc_smem<M, NP>());
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                th_smem<M, NP>());
 }
 // the banks K8 has an instantiation for: (m, padded N_f)
 int tc_np(int m, int nf) {
@@ -158,6 +165,10 @@ struct foe_model {
     float* tc_sumk = nullptr;
     float* tc_thl = nullptr;
     foe::TcConst* tc_const = nullptr;  // per-filter epilogue constants, passed by value to K8
+    // K8 (fp16 tensor cores, foe_th.cuh): fp16 hi/lo B images and the epilogue constants
+    unsigned char* th_bimg = nullptr;
+    foe::ThConst* th_const = nullptr;
+    bool th_tf32 = false;           // FOE_K8_TF32=1 (read once at creation): the round-1 TF32 K8
     int stencil = FOE_STENCIL_AUTO; // foe_energy_grad's choice
     bool persist_phases = false;
     cudaMemPool_t pool = nullptr;   // private stream-ordered pool of the per-call scratch    // FOE_PERSIST_PHASES=1 (read once here): persistent-driver phase timings
@@ -260,6 +271,65 @@ foe_status build_tc_images(foe_model* md) {
     CK(cudaMemcpy(md->tc_bimg, img.data(), img.size() * sizeof(float), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(md->tc_sumk, sumk.data(), NP * sizeof(float), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(md->tc_thl, thl.data(), NP * sizeof(float), cudaMemcpyHostToDevice));
+    return FOE_OK;
+}
+
+// K8 fp16 operand images (foe_th.cuh), element (k, n) of a K-major B matrix at half offset
+// chunk(k/16) * 2 N 8 + ((k % 16) / 8) N 8 + n 8 + k % 8, hi image then lo image:
+//   forward  Kf[k][i], k = 16 c + 8 h + e: ring slot 2c + h of the response row's window; slot 0
+//            (A2) carries the row sums ks[e][i] = sum_b fwd_i[e][b], slot 1 + a the taps fwd_i[a][e]
+//            (e < m; fwd = the flipped taps); x s_f
+//   backward Kb[i][t] = 2 theta_i k_i[t] for t < NB (N padded to NBP), x s_b
+// hi = fp16(v), lo = fp16(v - hi) (from the fp64 value); s_f, s_b = 2^(13 - e) with 2^e <= max|v|.
+foe_status build_th_images(foe_model* md) {
+    const int m = md->m, nf = md->nf, NP = md->tc_np, TAPS = m * m;
+    const int NCH = (m + 1) / 2, NB = (TAPS / 8) * 8, NBP = ((NB + 15) / 16) * 16, NKB = NP / 16;
+    const size_t BF = (size_t)NCH * 16 * NP, BB = (size_t)NKB * 16 * NBP;   // halves per image
+    std::vector<double> kf((size_t)NCH * 16 * NP, 0.0), kb((size_t)NP * NBP, 0.0);
+    for (int i = 0; i < nf; ++i) {
+        const float* fw = md->tp->fwd + (size_t)i * TAPS;
+        for (int k = 0; k < NCH * 16; ++k) {
+            const int slot = k / 8, e = k % 8;
+            double v = 0.0;
+            if (slot == 0) {
+                if (e < m) for (int b2 = 0; b2 < m; ++b2) v += (double)fw[e * m + b2];
+            } else if (slot - 1 < m && e < m) {
+                v = (double)fw[(slot - 1) * m + e];
+            }
+            kf[(size_t)k * NP + i] = v;
+        }
+        for (int t = 0; t < NB; ++t) kb[(size_t)i * NBP + t] = (double)md->tp->bwd[(size_t)i * TAPS + t];
+    }
+    auto scale_of = [](const std::vector<double>& v) {
+        double mx = 0.0;
+        for (double x : v) mx = std::max(mx, std::fabs(x));
+        if (!(mx > 0.0)) return 1.0;
+        return std::ldexp(1.0, 13 - std::ilogb(mx));
+    };
+    const double sf = scale_of(kf), sb = scale_of(kb);
+    std::vector<__half> img(2 * BF + 2 * BB, __float2half_rn(0.0f));
+    auto put = [&](size_t base, size_t nimg, int N, int k, int n, double v) {
+        const size_t off = (size_t)(k / 16) * 2 * N * 8 + (size_t)((k % 16) / 8) * N * 8 + (size_t)n * 8 + k % 8;
+        const __half h = __float2half_rn((float)v);
+        img[base + off] = h;
+        img[base + nimg + off] = __float2half_rn((float)(v - (double)__half2float(h)));
+    };
+    for (int k = 0; k < NCH * 16; ++k)
+        for (int i = 0; i < NP; ++i) put(0, BF, NP, k, i, kf[(size_t)k * NP + i] * sf);
+    for (int i = 0; i < NP; ++i)
+        for (int t = 0; t < NBP; ++t) put(2 * BF, BB, NBP, i, t, kb[(size_t)i * NBP + t] * sb);
+    md->th_const = new (std::nothrow) foe::ThConst();
+    if (!md->th_const) return fail(FOE_ERR_OUT_OF_MEMORY, "host allocation");
+    std::memset(md->th_const, 0, sizeof(foe::ThConst));
+    for (int i = 0; i < nf; ++i) {
+        md->th_const->sumk[i] = md->tp->sumk[i];
+        md->th_const->thl[i] = (float)md->tp->theta_ln2[i];
+        md->th_const->kbl[i] = (float)((double)md->tp->bwd[(size_t)i * TAPS + TAPS - 1] * sb);   // x P's 2^14 = Z units
+    }
+    md->th_const->inv_sf = (float)(1.0 / sf);
+    md->th_const->inv_z = (float)(1.0 / (sb * (double)foe::kThPScale));
+    CK(cudaMalloc((void**)&md->th_bimg, img.size() * sizeof(__half)));
+    CK(cudaMemcpy(md->th_bimg, img.data(), img.size() * sizeof(__half), cudaMemcpyHostToDevice));
     return FOE_OK;
 }
 
@@ -379,6 +449,8 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
     {
         const char* ph = std::getenv("FOE_PERSIST_PHASES");   // diagnostics only, read once
         md->persist_phases = ph != nullptr && ph[0] == '1';
+        const char* k8 = std::getenv("FOE_K8_TF32");          // A/B against the round-1 TF32 K8, read once
+        md->th_tf32 = k8 != nullptr && k8[0] == '1';
     }
     md->lam[0] = lam[0];
     md->lam[1] = lam[1];
@@ -409,6 +481,7 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
     md->tc_np = tc_np(m, n_filters);
     if (md->tc_np) {
         foe_status r = build_tc_images(md);
+        if (r == FOE_OK) r = build_th_images(md);
         if (r != FOE_OK) { foe_model_destroy(md); return r; }
     }
     *out = md;
@@ -433,6 +506,8 @@ void foe_model_destroy(foe_model* model) {
     if (model->tc_bimg) cudaFree(model->tc_bimg);
     if (model->tc_sumk) cudaFree(model->tc_sumk);
     if (model->tc_thl) cudaFree(model->tc_thl);
+    if (model->th_bimg) cudaFree(model->th_bimg);
+    delete model->th_const;
     // outstanding stream-ordered frees are honoured: the pool is released once they land
     if (model->pool) cudaMemPoolDestroy(model->pool);
     delete model->tc_const;
@@ -488,7 +563,7 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
         const bool pack_ok = allow_pack && H_grid == H;
         int nfull = W / ow, rem = W - nfull * ow, spt = 0;
         if (rem > 0 && pack_ok) {
-            spt = 128 / (rem + 2 * (md->m - 1));
+            spt = 128 / ((rem + 2 * (md->m - 1) + 7) & ~7);   // strips of a multiple of 8 lanes
             if (spt < 2) spt = 0;
         }
         if (rem > 0 && spt == 0) { nfull += 1; rem = 0; }
@@ -530,11 +605,20 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
     ta.theta_ln2 = md->tc_thl;
     ta.tiles_x = a.tiles_x;
     count_launch(1);
+    if (md->th_tf32) {
+        if (md->tc_np == 48)
+            foe::k_prior_grad_tc<7, 48, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<7, 48>(), s>>>(ta, *md->tc_const);
+        else
+            foe::k_prior_grad_tc<5, 32, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<5, 32>(), s>>>(ta, *md->tc_const);
+        CKL("k_prior_grad_tc");
+        return FOE_OK;
+    }
+    ta.bimg = reinterpret_cast<const float*>(md->th_bimg);
     if (md->tc_np == 48)
-        foe::k_prior_grad_tc<7, 48, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<7, 48>(), s>>>(ta, *md->tc_const);
+        foe::k_prior_grad_th<7, 48, kTcR><<<dim3(a.ntiles, B), 256, th_smem<7, 48>(), s>>>(ta, *md->th_const);
     else
-        foe::k_prior_grad_tc<5, 32, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<5, 32>(), s>>>(ta, *md->tc_const);
-    CKL("k_prior_grad_tc");
+        foe::k_prior_grad_th<5, 32, kTcR><<<dim3(a.ntiles, B), 256, th_smem<5, 32>(), s>>>(ta, *md->th_const);
+    CKL("k_prior_grad_th");
     return FOE_OK;
 }
 

@@ -1,0 +1,440 @@
+// foe_th.cuh -- K8: the fused FoE prior energy + gradient (rows a2-a7 of SURVEY.md 8(a)) on the
+// sm_100a tensor cores, fp16 operands (tcgen05.mma kind::f16, fp32 accumulation in TMEM) in a
+// 3-pass hi/lo split for fp32-level accuracy.
+//
+// grad_w F = W sum_i theta_i K_i^T rho'(K_i e^w) as two GEMMs per response row
+// of 128 pixels (M = 128 TMEM lanes):
+//
+//   forward   R[q, i] = sum_{a,b} Kf[(a,b), i] U_{j+a}[q, b] + sum_a ks[a, i] A2_j[q, a]
+//             U_y[q, b] = (u[y][q+b] - c_{y,G}) s_u     one im2col "row" of u per u row y
+//             A2_j[q, a] = (c_{j+a,G} - c_{j+C,G}) s_u   (ks[a, i] = sum_b Kf[(a,b), i])
+//             so R / (s_u s_f) + c_{j+C,G} sum_t k_i = (K_i u)[q]  exactly in exact arithmetic;
+//             c_{y,G} = u at row y, column 3 + C of the 8-pixel group G of q: the tensor-core
+//             operands are local differences (DC shift per u row and pixel group; the tile-wide
+//             shift of K1 costs the tensor core's coarser fp32 accumulation ~4x in accuracy).
+//   backward  Z[q, t] = sum_i P[q, i] Kb[i, t]    P = rho'(r)/2 = r/(1+r^2), Kb = 2 theta_i k_i
+//             s[p]    = sum_t Z[p + off(t), t]    (col2im through smem; the last tap on CUDA cores)
+//
+// Every u row's im2col U_y (8 halves per pixel: taps b < m, zeros after) is written ONCE into a
+// TMEM ring by the thread of its pixel (tcgen05.st) and read by the M response rows that use
+// it: the ring holds 2 copies of RS = m + 1 slots so that the m + 1 slots of one response row
+// (A2_j in the slot of u row j-1, then U_j .. U_{j+m-1}) are always contiguous columns; each
+// K = 16 MMA reads two adjacent slots.  A operands of both GEMMs come from TMEM (shared-memory
+// A operands at N = 48 are bound by shared-memory bandwidth: 79 vs 35 cycles per MMA measured,
+// tools/probes/f16_probe.cu); B operands (taps) are fp16 hi/lo images in shared memory, K-major,
+// loaded by one TMA bulk copy.  Each product is x_hi y_hi + x_hi y_lo + x_lo y_hi with
+// x_hi = fp16(x), x_lo = fp16(x - x_hi): ~2^-22 relative, with power-of-two scales keeping every
+// operand inside the fp16 range (s_u per tile from the staged tile's range, s_f / s_b per model,
+// P scaled by 2^14).
+//
+// One CTA (256 threads = 2 warp groups x 4 warps; warp w reaches TMEM lanes 32 (w % 4) ..) =
+// an output tile of R rows x (128 - 2C) columns; two CTAs per SM overlap one CTA's MMAs with the
+// other's thread work.  Per response row: build U_{j+m-1} and A2_j -> 3 NCH forward MMAs ->
+// rho, rho' epilogue -> 3 NKB backward MMAs -> Z through smem -> rolling col2im sums.
+#pragma once
+
+#include <cuda_fp16.h>
+
+#include "foe_tc.cuh"
+
+namespace foe {
+
+constexpr float kThPScale = 16384.0f;   // P = rho'/2 in [-1/2, 1/2] is stored x 2^14 (fp16 range)
+
+template <int M, int NP, int R>
+struct ThGeom {
+    static constexpr int C = (M - 1) / 2;
+    static constexpr int TAPS = M * M;
+    static constexpr int LANES = 128;                   // response pixels per row (TMEM lanes)
+    static constexpr int OW = LANES - 2 * C;            // output columns per tile
+    static constexpr int RR = R + 2 * C;                // response rows per tile
+    static constexpr int UY = R + 4 * C;                // staged u rows
+    static constexpr int UX = LANES + 2 * C;            // staged u columns
+    static constexpr int UP = UX + 2;                   // u pitch (floats)
+    static constexpr int NCH = (M + 1) / 2;             // forward K = 16 chunks (two ring slots each)
+    static constexpr int RS = M + 1;                    // ring slots per copy (A2 + m rows)
+    static constexpr int NB = (TAPS / 8) * 8;           // backward taps on the tensor core
+    static constexpr int NBP = ((NB + 15) / 16) * 16;   // ... padded to the MMA's N granularity
+    static constexpr int NKB = NP / 16;                 // backward K = 16 chunks (filters)
+    // TMEM columns: ring hi / lo (2 RS slots x 4 columns each), D (= Z), P hi / lo (fp16 pairs)
+    static constexpr int COL_RH = 0, COL_RL = 2 * RS * 4, COL_D = 4 * RS * 4;
+    static constexpr int ND = NP > NBP ? NP : NBP;
+    static constexpr int COL_Z = COL_D;
+    static constexpr int COL_PH = COL_D + ND, COL_PL = COL_PH + NP / 2;
+    static constexpr int TCOLS_USED = COL_PL + NP / 2;
+    static constexpr int TCOLS = TCOLS_USED <= 128 ? 128 : 256;
+    // B images (bytes): Kf [NCH][2 K-halves][NP][8 halves] hi, lo; Kb [NKB][2][NBP][8] hi, lo
+    static constexpr int BF_BYTES = NCH * 16 * NP * 2;
+    static constexpr int BB_BYTES = NKB * 16 * NBP * 2;
+    static constexpr int B_BYTES = 2 * BF_BYTES + 2 * BB_BYTES;
+    // shared memory (bytes): B images | u tile | Z transpose [NB][LANES] | col2im hand-off ring
+    // [8][LANES] | last-tap partials [2 rows][2 groups][LANES] | tile max per warp
+    static constexpr int SM_B = 0;
+    static constexpr int SM_U = SM_B + B_BYTES;
+    static constexpr int SM_Z = SM_U + UY * UP * 4;
+    static constexpr int SM_HAND = SM_Z + NB * LANES * 4;
+    static constexpr int SM_ZL = SM_HAND + 8 * LANES * 4;
+    static constexpr int SMEM_BYTES = SM_ZL + 4 * LANES * 4 + 64;
+    static_assert(NP % 16 == 0 && NBP <= ND, "MMA shapes");
+    static_assert(TAPS - NB == 1, "one CUDA-core tap");
+    static_assert(TCOLS_USED <= 256, "TMEM budget: two CTAs per SM");
+    static_assert(B_BYTES % 16 == 0 && SM_U % 16 == 0, "B images: one TMA bulk copy");
+};
+
+// Per-filter epilogue constants of K8, in the kernel-parameter constant bank (FFMA operands
+// straight from c[]): sum_t k_i (DC restore), theta_i ln 2 (energy), the last backward tap x s_b
+// (times P's 2^14: Z units); the forward and backward B scales' inverses.  Zero past N_f.
+struct ThConst {
+    float sumk[kMaxFilters];
+    float thl[kMaxFilters];
+    float kbl[kMaxFilters];    // x s_b
+    float inv_sf;   // 1 / s_f
+    float inv_z;    // 1 / (s_b 2^14)
+};
+
+// fp16 hi/lo split of a float pair: hi = rn_fp16(x), lo = rn_fp16(x - hi) (x - hi exact in fp32)
+__device__ __forceinline__ void h2_split(float2 v, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __float22half2_rn(v);
+    const float2 hb = __half22float2(h);
+    const __half2 l = __float22half2_rn(__fadd2_rn(v, make_float2(-hb.x, -hb.y)));
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+
+// (a2, a3) im2col of u row y for this thread's pixel l: the halves [4 WG, 4 WG + 4) of
+// (u[y][l + b] - c_{y,G}) s_u (taps b >= m are 0), written to ring slot s and its copy s + RS
+template <int M, int UP, int RS, int WG>
+__device__ __forceinline__ void th_build_row(const float* us, int y, int l, int xg, float su, uint32_t t_rh,
+                                             uint32_t t_rl, int s) {
+    const float* up = us + y * UP;
+    const float ncs = -up[xg] * su;
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int b = WG * 4 + e;
+        v[e] = b < M ? fmaf(up[l + b], su, ncs) : 0.0f;   // = rn((u - c) s_u): s_u is a power of 2
+    }
+    uint32_t h0, h1, l0, l1;
+    h2_split(make_float2(v[0], v[1]), h0, l0);
+    h2_split(make_float2(v[2], v[3]), h1, l1);
+    const uint32_t c0 = (uint32_t)(s * 4 + WG * 2), c1 = (uint32_t)((s + RS) * 4 + WG * 2);
+    tc::tmem_st2u(t_rh + c0, h0, h1);
+    tc::tmem_st2u(t_rh + c1, h0, h1);
+    tc::tmem_st2u(t_rl + c0, l0, l1);
+    tc::tmem_st2u(t_rl + c1, l0, l1);
+}
+// A2_j: (c_{j+a,G} - c_{j+C,G}) s_u for a in [4 WG, 4 WG + 4) (a >= m: 0), into ring slot s
+template <int M, int UP, int WG>
+__device__ __forceinline__ void th_build_a2(const float* us, int j, int xg, float su, uint32_t t_rh, uint32_t t_rl,
+                                            int s) {
+    constexpr int C = (M - 1) / 2;
+    const float cC = us[(j + C) * UP + xg];
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int a = WG * 4 + e;
+        v[e] = a < M ? (us[(j + a) * UP + xg] - cC) * su : 0.0f;
+    }
+    uint32_t h0, h1, l0, l1;
+    h2_split(make_float2(v[0], v[1]), h0, l0);
+    h2_split(make_float2(v[2], v[3]), h1, l1);
+    const uint32_t c0 = (uint32_t)(s * 4 + WG * 2);
+    tc::tmem_st2u(t_rh + c0, h0, h1);
+    tc::tmem_st2u(t_rl + c0, l0, l1);
+}
+
+// epilogue of filter chunks [F0, F1) of 8: r = R / (s_u s_f) + c sum k; energy
+// sum theta ln2 lg2(1 + r^2); P = 2^14 r / (1 + r^2) (= 2^14 rho'/2) split into fp16 hi / lo pairs,
+// to TMEM (column = filter pair); zlast += P kb_last (Z units)
+template <int F0, int F1>
+__device__ __forceinline__ float th_epilogue(uint32_t t_d, uint32_t t_ph, uint32_t t_pl, float uq, float inv,
+                                             const float* css, const float* ths, const float* kbl, float& zlast) {
+    float r[(F1 - F0) * 8];
+#pragma unroll
+    for (int f8 = F0; f8 < F1; ++f8) tc::tmem_ld8(t_d + f8 * 8, *reinterpret_cast<float(*)[8]>(r + (f8 - F0) * 8));
+    tc::wait_ld();
+    const float2 uq2 = make_float2(uq, uq), one2 = make_float2(1.f, 1.f), inv2 = make_float2(inv, inv);
+    float2 el2 = make_float2(0.f, 0.f), zl2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int f8 = F0; f8 < F1; ++f8) {
+        uint32_t ph[4], pl[4];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+            const int i = f8 * 8 + e;
+            const float2 r2 = make_float2(r[(f8 - F0) * 8 + e], r[(f8 - F0) * 8 + e + 1]);
+            const float2 rv = __ffma2_rn(uq2, make_float2(css[i], css[i + 1]), __fmul2_rn(r2, inv2));
+            const float2 d = __ffma2_rn(rv, rv, one2);
+            el2 = __ffma2_rn(make_float2(ths[i], ths[i + 1]), make_float2(lg2_approx(d.x), lg2_approx(d.y)), el2);
+            // one MUFU reciprocal per filter pair: 1/d_A = d_B / (d_A d_B) (d >= 1; see K1)
+            const float q = rcp_approx(d.x * d.y) * kThPScale;
+            const float2 pv = __fmul2_rn(rv, __fmul2_rn(make_float2(d.y, d.x), make_float2(q, q)));
+            zl2 = __ffma2_rn(pv, make_float2(kbl[i], kbl[i + 1]), zl2);
+            h2_split(pv, ph[e / 2], pl[e / 2]);
+        }
+        tc::tmem_st4u(t_ph + f8 * 4, ph);
+        tc::tmem_st4u(t_pl + f8 * 4, pl);
+    }
+    zlast = zl2.x + zl2.y;
+    return el2.x + el2.y;
+}
+
+template <int M, int NP, int R>
+__global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const __grid_constant__ ThConst cc) {
+    using G = ThGeom<M, NP, R>;
+    constexpr int C = G::C, L = G::LANES, RS = G::RS;
+    extern __shared__ __align__(128) unsigned char smb[];
+    float* us = reinterpret_cast<float*>(smb + G::SM_U);
+    float* zs = reinterpret_cast<float*>(smb + G::SM_Z);
+    float* hand = reinterpret_cast<float*>(smb + G::SM_HAND);   // [8][L] wg0 -> wg1 partial sums
+    float* zls = reinterpret_cast<float*>(smb + G::SM_ZL);      // [2 rows][2 groups][L] last-tap partials
+    __shared__ uint32_t tbase_s;
+    __shared__ __align__(8) uint64_t mbar_f, mbar_b;   // forward / backward MMA completion
+    __shared__ __align__(8) uint64_t mbar_bimg;        // TMA bulk copy of the B images
+    __shared__ double red[32];
+    __shared__ float wmax[8];
+
+    const K1Args& args = ta.k;
+    const int b = blockIdx.y;
+    int wslot = 0, gslot = 0;
+    if (args.ctl != nullptr) {
+        const ImgCtl& c = args.ctl[b];
+        if (!c.active) return;
+        wslot = args.which_cur ? c.cur : c.cand;
+        gslot = args.which_cur ? c.gcur : c.gcand;
+    }
+    const int H = args.H, W = args.W;
+    const size_t HW = (size_t)H * W;
+    const int tile = blockIdx.x;
+    const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
+    const int t = threadIdx.x, warp = __shfl_sync(0xffffffffu, t >> 5, 0);
+    const int wg = warp >> 2;                                   // warp group (0, 1)
+    const int l = (warp & 3) * 32 + (t & 31);                   // TMEM lane = response pixel
+    // tile geometry: a full tile (band ty, columns x0 ..), or a packed tile whose lane strips (of
+    // a multiple of 8 lanes: pixel groups never straddle strips) carry the remainder columns of
+    // several bands (args.tc_rem > 0)
+    const int nbands = (H + R - 1) / R;
+    const int nnorm = nbands * ta.tiles_x;
+    const bool packed = tile >= nnorm;
+    int y0, x0, sy0, ocol;
+    bool svalid = true;
+    const int SP = (args.tc_rem + 4 * C + 7) & ~7;             // strip pitch in lanes (packed)
+    if (!packed) {
+        const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
+        y0 = ty * R; x0 = tx * G::OW; sy0 = y0; ocol = l;
+    } else {
+        const int band0 = (tile - nnorm) * args.tc_spt;
+        const int st = l / SP;
+        ocol = l - st * SP;
+        svalid = st < args.tc_spt && band0 + st < nbands;
+        y0 = band0 * R; x0 = ta.tiles_x * G::OW; sy0 = (band0 + st) * R;
+    }
+
+    // ---- prologue: TMEM, mbarriers, B images, u tile, tile scale, first ring rows ----------
+    if (warp == 0) tc::tmem_alloc<G::TCOLS>(&tbase_s);
+    if (t == 0) {
+        tc::mbar_init(&mbar_f, 1);
+        tc::mbar_init(&mbar_b, 1);
+        tc::mbar_init(&mbar_bimg, 1);
+        tc::mbar_fence_init();
+        tc::bulk_g2s(smb + G::SM_B, ta.bimg, (uint32_t)G::B_BYTES, &mbar_bimg);
+    }
+    const int yc = min(y0 + R / 2, H - 1), xc = min(x0 + (packed ? args.tc_rem : G::OW) / 2, W - 1);
+    const bool udom = args.udom != 0;
+    const double wc = w[(size_t)yc * W + xc];
+    const float cst = (float)(udom ? wc : exp(wc));
+    if (!packed) tc_stage_u<G::UY, G::UX, G::UP, 8>(us, w, args.halo, H, W, y0, x0, 2 * C, udom, cst, wc, warp, t & 31);
+    else tc_stage_u_packed<G::UY, G::UX, G::UP, 8>(us, w, H, W, R, x0, 2 * C, SP, args.tc_spt, y0 / R, nbands, udom,
+                                                   cst, wc, warp, t & 31);
+    tc::fence_before_sync();
+    __syncthreads();
+    // tile scale s_u = 2^(13 - e), 2^e <= 2 max|u - cst| < 2^(e+1): every U and A2 entry (a
+    // difference of two staged values) has magnitude < 2^14 (fp16 max 65504)
+    float m = 0.f;
+    for (int y = warp; y < G::UY; y += 8)
+        for (int x = t & 31; x < G::UX; x += 32) m = fmaxf(m, fabsf(us[y * G::UP + x]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((t & 31) == 0) wmax[warp] = m;
+    __syncthreads();
+    m = wmax[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) m = fmaxf(m, wmax[k]);
+    int e2 = ((int)((__float_as_uint(2.0f * m) >> 23) & 0xffu)) - 127;   // exponent of 2m (-127: 0 / denormal)
+    e2 = max(e2, -47);                                                   // s_u <= 2^60
+    if (!(m < 3.0e38f)) e2 = 13;                                          // non-finite tile: s_u = 1
+    const float su = __uint_as_float((uint32_t)(127 + 13 - e2) << 23);
+    const float inv = cc.inv_sf / su;                                     // exact: powers of 2
+    tc::fence_after_sync();
+    const uint32_t tb = tbase_s;   // (read after the barriers above: the allocating warp wrote it)
+    const uint32_t tl = tb + ((uint32_t)((warp & 3) * 32) << 16);   // this warp's TMEM lane base
+    const uint32_t t_rh = tl + G::COL_RH, t_rl = tl + G::COL_RL;
+    const int xg = (l & ~7) + 3 + C;                            // u column of the pixel group's c
+    // ring rows 0 .. m-2 (row j + m - 1 is built in iteration j)
+#pragma unroll 1
+    for (int y = 0; y < M - 1; ++y) {
+        if (wg == 0) th_build_row<M, G::UP, RS, 0>(us, y, l, xg, su, t_rh, t_rl, y % RS);
+        else th_build_row<M, G::UP, RS, 1>(us, y, l, xg, su, t_rh, t_rl, y % RS);
+    }
+    tc::mbar_wait(&mbar_bimg, 0);   // B images landed (async proxy; read by the MMAs)
+    const uint32_t idf = tc::idesc_f16(128, NP);               // forward: N = filters
+    const uint32_t idb = tc::idesc_f16(128, G::NBP);           // backward: N = taps [0, NB) (+ zero pad)
+    const uint32_t b_base = tc::smem_u32(smb + G::SM_B);
+
+    // energy ownership of this lane's response column, output column of this thread
+    const int ow = packed ? args.tc_rem : G::OW;
+    const bool col_own = svalid && (ocol >= C) && (ocol < C + ow) && (x0 - C + ocol < W);
+    const bool out_col = svalid && (ocol < ow) && (x0 + ocol < W);
+
+    double e_acc = 0.0;
+    constexpr int NZ8 = G::NB / 8, HZ8 = (NZ8 + 1) / 2;    // Z tap chunks: wg0 [0,HZ8), wg1 [HZ8,NZ8)
+    constexpr int NF8 = NP / 8, HF8 = NF8 / 2;             // filter chunks: wg0 [0,HF8), wg1 [HF8,NF8)
+    constexpr int A0 = C + 1, A1 = M - A0;                 // col2im rows: wg0 a < A0, wg1 a >= A0
+    float acc[A0 > A1 ? A0 : A1];
+#pragma unroll
+    for (int k = 0; k < (A0 > A1 ? A0 : A1); ++k) acc[k] = 0.f;
+    float* gout = args.g + (size_t)gslot * args.g_slot_stride + (size_t)b * HW;
+
+    // Software pipeline over response rows (iteration j):
+    //   ring row j+m-1, A2_j | wait MMAb(j-1), Z(j-1) -> smem | sync | issue MMAf(j) |
+    //   col2im(j-1) (overlaps MMAf(j)) | wait MMAf(j), epilogue(j) | sync | issue MMAb(j)
+    // MMAb(j) runs under the next iteration's ring build and Z wait.  The ring slots written in
+    // iteration j (u row j-2's and u row j-1's) were last read by MMAf(j-1), complete by then.
+#pragma unroll 1
+    for (int j = 0; j <= G::RR; ++j) {
+        float uq = 0.f;
+        const int ws = (j + RS - 1) % RS;                       // slot of A2_j (= u row j-1's)
+        if (j < G::RR) {
+            const int yn = j + M - 1;
+            if (wg == 0) {
+                th_build_row<M, G::UP, RS, 0>(us, yn, l, xg, su, t_rh, t_rl, yn % RS);
+                th_build_a2<M, G::UP, 0>(us, j, xg, su, t_rh, t_rl, ws);
+            } else {
+                th_build_row<M, G::UP, RS, 1>(us, yn, l, xg, su, t_rh, t_rl, yn % RS);
+                th_build_a2<M, G::UP, 1>(us, j, xg, su, t_rh, t_rl, ws);
+            }
+            uq = us[(j + C) * G::UP + xg] + cst;                // c_{j+C,G}: the DC restore value
+        }
+        if (j > 0) {
+            tc::mbar_wait(&mbar_b, (uint32_t)((j - 1) & 1));
+            tc::fence_after_sync();
+            if (wg == 0) tc_z_to_smem<L, 0, HZ8>(tl + G::COL_Z, zs, l);
+            else tc_z_to_smem<L, HZ8, NZ8>(tl + G::COL_Z, zs, l);
+        }
+        tc::wait_st();
+        tc::fence_before_sync();
+        __syncthreads();
+        if (warp == 0 && j < G::RR) {
+            tc::fence_after_sync();
+            // the small cross terms first, then hi.hi: the fp32 accumulator loses less of them
+#pragma unroll
+            for (int pass = 0; pass < 3; ++pass) {
+                const uint32_t acol = pass == 1 ? G::COL_RL : G::COL_RH;
+                const uint32_t boff = pass == 0 ? (uint32_t)G::BF_BYTES : 0u;
+#pragma unroll
+                for (int c = 0; c < G::NCH; ++c) {
+                    const uint64_t bd = tc::sdesc_kmajor(b_base + boff + c * 2 * NP * 16, NP * 16, 128);
+                    tc::mma_f16_ts_warp(tb + G::COL_D, tb + acol + 4 * (ws + 2 * c), bd, idf, (pass | c) != 0);
+                }
+            }
+            tc::mma_commit_warp(&mbar_f);
+        }
+        if (j > 0) {
+            // col2im of row jz = j - 1: Z row jz feeds output rows o = jz - a at column ox = l:
+            //   s[o][ox] += sum_b Z[(jz, ox + b), (a, b)];  acc[k] holds row jz - (a0 + k)
+            const int jz = j - 1;
+            if (wg == 0) {
+#pragma unroll
+                for (int a = 0; a + 1 < A0; a += 2) {
+                    float2 sa = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb)
+                        sa = __fadd2_rn(sa, make_float2(zs[(a * M + bb) * L + l + bb], zs[((a + 1) * M + bb) * L + l + bb]));
+                    acc[a] += sa.x;
+                    acc[a + 1] += sa.y;
+                }
+                if constexpr (A0 % 2 == 1) {
+                    float sa = 0.f;
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) sa += zs[((A0 - 1) * M + bb) * L + l + bb];
+                    acc[A0 - 1] += sa;
+                }
+                const int o = jz - (A0 - 1);                    // wg0's share of row o is complete
+                if (o >= 0) hand[(o & 7) * L + l] = acc[A0 - 1];
+#pragma unroll
+                for (int k = A0 - 1; k > 0; --k) acc[k] = acc[k - 1];
+                acc[0] = 0.f;
+            } else {
+                const float* zl = zls + (jz & 1) * 2 * L;
+                constexpr int NPR = (A1 - 1) / 2;
+#pragma unroll
+                for (int q = 0; q < NPR; ++q) {
+                    const int a = A0 + 2 * q;
+                    float2 sa = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb)
+                        sa = __fadd2_rn(sa, make_float2(zs[(a * M + bb) * L + l + bb], zs[((a + 1) * M + bb) * L + l + bb]));
+                    acc[2 * q] += sa.x;
+                    acc[2 * q + 1] += sa.y;
+                }
+#pragma unroll
+                for (int k = 2 * NPR; k < A1; ++k) {
+                    const int a = A0 + k;
+                    float sa = 0.f;
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) {
+                        const int tap = a * M + bb;
+                        sa += tap < G::NB ? zs[tap * L + l + bb] : zl[l + bb] + zl[L + l + bb];
+                    }
+                    acc[k] += sa;
+                }
+                // (a6) row o = jz - 2C is complete: g = u (.) s, s = (Z-unit sum) / (s_b 2^14)
+                const int o = jz - 2 * C;
+                if (o >= 0 && o < R && out_col && sy0 + o < H) {
+                    const float s_tot = acc[A1 - 1] + hand[(o & 7) * L + l];
+                    const float u = udom ? 1.0f : us[(o + 2 * C) * G::UP + l + 2 * C] + cst;   // W = diag(e^w)
+                    gout[(size_t)(sy0 + o) * W + x0 + ocol] = (u * cc.inv_z) * s_tot;
+                }
+#pragma unroll
+                for (int k = A1 - 1; k > 0; --k) acc[k] = acc[k - 1];
+                acc[0] = 0.f;
+            }
+        }
+        if (j < G::RR) {
+            tc::mbar_wait(&mbar_f, (uint32_t)(j & 1));
+            tc::fence_after_sync();
+            // (a4, a7) responses r, rho (owned responses), rho'/2 -> P (fp16 hi/lo)
+            const bool own = col_own && (j >= C) && (j < C + R) && (sy0 - C + j < H);
+            float zl;
+            const float el = wg == 0
+                ? th_epilogue<0, HF8>(tl + G::COL_D, tl + G::COL_PH, tl + G::COL_PL, uq, inv, cc.sumk, cc.thl, cc.kbl, zl)
+                : th_epilogue<HF8, NF8>(tl + G::COL_D, tl + G::COL_PH, tl + G::COL_PL, uq, inv, cc.sumk, cc.thl, cc.kbl, zl);
+            zls[(j & 1) * 2 * L + wg * L + l] = zl;
+            if (own) e_acc += (double)el;
+            tc::wait_st();
+            tc::fence_before_sync();
+            __syncthreads();
+            if (warp == 0) {
+                tc::fence_after_sync();
+#pragma unroll
+                for (int pass = 0; pass < 3; ++pass) {
+                    const uint32_t acol = pass == 1 ? G::COL_PL : G::COL_PH;
+                    const uint32_t boff = 2 * G::BF_BYTES + (pass == 0 ? (uint32_t)G::BB_BYTES : 0u);
+#pragma unroll
+                    for (int kc = 0; kc < G::NKB; ++kc) {
+                        const uint64_t bd = tc::sdesc_kmajor(b_base + boff + kc * 2 * G::NBP * 16, G::NBP * 16, 128);
+                        tc::mma_f16_ts_warp(tb + G::COL_Z, tb + acol + kc * 8, bd, idb, (pass | kc) != 0);
+                    }
+                }
+                tc::mma_commit_warp(&mbar_b);
+            }
+        }
+    }
+    // (a7) per-CTA energy partial (fixed order)
+    const double e = block_sum_d(e_acc, red);
+    if (t == 0) args.epart[(size_t)b * args.ntiles * args.groups + blockIdx.x] = e;
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<G::TCOLS>(tb);
+}
+
+}  // namespace foe
