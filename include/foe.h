@@ -310,6 +310,10 @@ foe_status ipiano_slabs_reset(ipiano_slabs* slabs, const float* f, double lipsch
 /* Runs max_iters accepted iterations (all ranks must call it; trial rounds in CUDA-graph
  * chunks, one host synchronisation per chunk).  FOE_ERR_COMM if slabs disagree. */
 foe_status ipiano_slabs_solve(ipiano_slabs* slabs, void* stream);
+/* Runs accepted iterations until min(target_iters, max_iters) are done (SURVEY.md 8(c) P2
+ * teacher forcing steps a scene this way); ipiano_slabs_solve = advance to max_iters.  All
+ * ranks must call it with the same target.  FOE_ERR_INVALID_ARGUMENT if target_iters < 0. */
+foe_status ipiano_slabs_advance(ipiano_slabs* slabs, int target_iters, void* stream);
 /* u = e^w (and/or w) of the slabs owned by this process: the whole scene when comm == NULL,
  * this rank's slab otherwise (device, [rows][W]). */
 foe_status ipiano_slabs_get_iterate(const ipiano_slabs* slabs, double* w_out, float* u_out, void* stream);

@@ -220,19 +220,20 @@ def make_cfg(lipschitz_init, max_iters, beta=0.4, step_safety=0.95, backtrack_fa
                   max_backtracks, newton_max_iters, newton_tol, rel_change_tol, w_guard)
 
 
-def ipiano_trial(w, wprev, g, F, L, f, filters, theta, l1, l2, cfg: OrcCfg):
-    """One iPiano trial.  Returns dict."""
+def ipiano_trial(w, wprev, g, F, L, f, filters, theta, l1, l2, cfg: OrcCfg, want_gplus=True):
+    """One iPiano trial.  Returns dict.  want_gplus=False
+    skips grad F(w+) (the C routine's gplus output is optional: F(w+) alone decides the test)."""
     w, wprev, g = _d(w), _d(wprev), _d(g)
     ft = ftilde(f)
     k, th = _d(filters), _d(theta)
     what = np.empty_like(w)
     wplus = np.empty_like(w)
-    gplus = np.empty_like(w)
+    gplus = np.empty_like(w) if want_gplus else None
     out = np.empty(8)
     st = lib().orc_ipiano_trial(_ptr(w), _ptr(wprev), _ptr(g), float(F), float(L), _ptr(ft),
                                 w.shape[0], w.shape[1], _ptr(k), _ptr(th), k.shape[0], k.shape[1],
                                 float(l1), float(l2), C.byref(cfg), _ptr(what), _ptr(wplus),
-                                _ptr(gplus), _ptr(out))
+                                _ptr(gplus) if want_gplus else None, _ptr(out))
     return dict(status=st, what=what, wplus=wplus, gplus=gplus, Fplus=out[0], gdelta=out[1],
                 dd=out[2], Gplus=out[3], margin=out[4], accepted=bool(out[5]),
                 newton=int(out[6]), ww=out[7])

@@ -2042,11 +2042,17 @@ foe_status ipiano_slabs_reset(ipiano_slabs* g, const float* f, double lipschitz_
 
 foe_status ipiano_slabs_solve(ipiano_slabs* g, void* stream) {
     if (!g) return fail(FOE_ERR_INVALID_ARGUMENT, "slabs is NULL");
+    return ipiano_slabs_advance(g, g->members[0]->cfg.max_iters, stream);
+}
+
+foe_status ipiano_slabs_advance(ipiano_slabs* g, int target_iters, void* stream) {
+    if (!g) return fail(FOE_ERR_INVALID_ARGUMENT, "slabs is NULL");
+    if (target_iters < 0) return fail(FOE_ERR_INVALID_ARGUMENT, "target_iters=%d must be >= 0", target_iters);
     CK(cudaSetDevice(g->model->dev));
     cudaStream_t user = (cudaStream_t)stream;
     CK(cudaEventRecord(g->sync_ev, user));
     CK(cudaStreamWaitEvent(g->s, g->sync_ev, 0));
-    const int max_iters = g->members[0]->cfg.max_iters;
+    const int max_iters = std::min(target_iters, g->members[0]->cfg.max_iters);
     for (ipiano_state* st : g->members) {
         foe::k_set_target<<<1, 128, 0, g->s>>>(st->ctl, 1, max_iters);
         count_launch(1);

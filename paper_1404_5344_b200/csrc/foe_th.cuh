@@ -6,12 +6,12 @@
 // of 128 pixels (M = 128 TMEM lanes):
 //
 //   forward   R[q, i] = sum_{a,b} Kf[(a,b), i] U_{j+a}[q, b] + sum_a ks[a, i] A2_j[q, a]
-//             U_y[q, b] = (u[y][q+b] - c_{y,G}) s_u     one im2col "row" of u per u row y
-//             A2_j[q, a] = (c_{j+a,G} - c_{j+C,G}) s_u   (ks[a, i] = sum_b Kf[(a,b), i])
-//             so R / (s_u s_f) + c_{j+C,G} sum_t k_i = (K_i u)[q]  exactly in exact arithmetic;
-//             c_{y,G} = u at row y, column 3 + C of the 8-pixel group G of q: the tensor-core
-//             operands are local differences (DC shift per u row and pixel group; the tile-wide
-//             shift of K1 costs the tensor core's coarser fp32 accumulation ~4x in accuracy).
+//             U_y[q, b] = (u[y][q+b] - u[y][q+C]) s_u   one im2col "row" of u per u row y
+//             A2_j[q, a] = (u[j+a][q+C] - u[j+C][q+C]) s_u   (ks[a, i] = sum_b Kf[(a,b), i])
+//             so R / (s_u s_f) + u_q sum_t k_i = (K_i u)[q] exactly in exact arithmetic, u_q =
+//             u[j+C][q+C] the window centre: the tensor-core operands are differences inside
+//             the 7 x 7 window (a per-pixel DC shift: the tile-wide shift of K1 costs the tensor
+//             core's coarser fp32 accumulation ~4x in accuracy), each U_y row still built once.
 //   backward  Z[q, t] = sum_i P[q, i] Kb[i, t]    P = rho'(r)/2 = r/(1+r^2), Kb = 2 theta_i k_i
 //             s[p]    = sum_t Z[p + off(t), t]    (col2im through smem; the last tap on CUDA cores)
 //
@@ -102,7 +102,8 @@ __device__ __forceinline__ void h2_split(float2 v, uint32_t& hi, uint32_t& lo) {
 }
 
 // (a2, a3) im2col of u row y for this thread's pixel l: the halves [4 WG, 4 WG + 4) of
-// (u[y][l + b] - c_{y,G}) s_u (taps b >= m are 0), written to ring slot s and its copy s + RS
+// (u[y][l + b] - u[y][xg]) s_u, xg = l + C (taps b >= m are 0), written to ring slot s and its
+// copy s + RS
 template <int M, int UP, int RS, int WG>
 __device__ __forceinline__ void th_build_row(const float* us, int y, int l, int xg, float su, uint32_t t_rh,
                                              uint32_t t_rl, int s) {
@@ -123,7 +124,7 @@ __device__ __forceinline__ void th_build_row(const float* us, int y, int l, int 
     tc::tmem_st2u(t_rl + c0, l0, l1);
     tc::tmem_st2u(t_rl + c1, l0, l1);
 }
-// A2_j: (c_{j+a,G} - c_{j+C,G}) s_u for a in [4 WG, 4 WG + 4) (a >= m: 0), into ring slot s
+// A2_j: (u[j+a][xg] - u[j+C][xg]) s_u for a in [4 WG, 4 WG + 4) (a >= m: 0), into ring slot s
 template <int M, int UP, int WG>
 __device__ __forceinline__ void th_build_a2(const float* us, int j, int xg, float su, uint32_t t_rh, uint32_t t_rl,
                                             int s) {
@@ -268,7 +269,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
     const uint32_t tb = tbase_s;   // (read after the barriers above: the allocating warp wrote it)
     const uint32_t tl = tb + ((uint32_t)((warp & 3) * 32) << 16);   // this warp's TMEM lane base
     const uint32_t t_rh = tl + G::COL_RH, t_rl = tl + G::COL_RL;
-    const int xg = (l & ~7) + 3 + C;                            // u column of the pixel group's c
+    const int xg = l + C;                                       // u column of the pixel's window centre
     // ring rows 0 .. m-2 (row j + m - 1 is built in iteration j)
 #pragma unroll 1
     for (int y = 0; y < M - 1; ++y) {
@@ -312,7 +313,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
                 th_build_row<M, G::UP, RS, 1>(us, yn, l, xg, su, t_rh, t_rl, yn % RS);
                 th_build_a2<M, G::UP, 1>(us, j, xg, su, t_rh, t_rl, ws);
             }
-            uq = us[(j + C) * G::UP + xg] + cst;                // c_{j+C,G}: the DC restore value
+            uq = us[(j + C) * G::UP + xg] + cst;                // u_q (window centre): the DC restore value
         }
         if (j > 0) {
             tc::mbar_wait(&mbar_b, (uint32_t)((j - 1) & 1));

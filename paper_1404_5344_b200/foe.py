@@ -32,7 +32,7 @@ EXPORTED = (
     "ipiano_get_counters", "ipiano_get_trace", "ipiano_profile", "ipiano_profile_read",
     "ipiano_state_destroy", "ipiano_state_stencil", "ipiano_state_solver", "ipiano_run",
     "foe_model_set_stencil", "foe_comm_unique_id", "foe_comm_create", "foe_comm_destroy", "ipiano_slabs_create", "ipiano_slabs_reset",
-    "ipiano_slabs_solve", "ipiano_slabs_get_iterate", "ipiano_slabs_member", "ipiano_slabs_destroy",
+    "ipiano_slabs_solve", "ipiano_slabs_advance", "ipiano_slabs_get_iterate", "ipiano_slabs_member", "ipiano_slabs_destroy",
     "ipiano_slabs_halo_handle", "ipiano_slabs_connect_peers", "ipiano_slabs_disconnect_peers",
     "foe_psnr", "foe_ssim", "foe_add_speckle",
 )
@@ -110,6 +110,7 @@ def lib():
                                       C.POINTER(IPianoConfig), _vp, _vp, C.POINTER(_vp)]
     L.ipiano_slabs_reset.argtypes = [_vp, _vp, C.c_double, _vp]
     L.ipiano_slabs_solve.argtypes = [_vp, _vp]
+    L.ipiano_slabs_advance.argtypes = [_vp, C.c_int, _vp]
     L.ipiano_slabs_get_iterate.argtypes = [_vp, _vp, _vp, _vp]
     L.ipiano_slabs_member.argtypes = [_vp, C.c_int, C.POINTER(_vp)]
     L.ipiano_slabs_halo_handle.argtypes = [_vp, _vp]
@@ -555,6 +556,11 @@ def ipiano_slabs_reset(slabs: Slabs, f, lipschitz_init: float, stream=None):
 
 def ipiano_slabs_solve(slabs: Slabs, stream=None):
     _check(lib().ipiano_slabs_solve(slabs.handle, _stream(stream)))
+
+
+def ipiano_slabs_advance(slabs: Slabs, target_iters: int, stream=None):
+    """Run accepted iterations until min(target_iters, max_iters) are done (include/foe.h)."""
+    _check(lib().ipiano_slabs_advance(slabs.handle, int(target_iters), _stream(stream)))
 
 
 def ipiano_slabs_get_iterate(slabs: Slabs, want_w=True, want_u=True, stream=None, u_out=None):
