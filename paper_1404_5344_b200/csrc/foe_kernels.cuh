@@ -717,6 +717,16 @@ __device__ __forceinline__ double rcp_f64(double b) {
     return y;
 }
 
+// fp32 Newton steps of the prox after the first (exponential-free) one, before the fp64 step
+#ifndef FOE_K2_F32_STEPS
+#define FOE_K2_F32_STEPS 1
+#endif
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Root of phi(z) = z - what + tau [l1 (1 - f^2 e^{-2z}) + l2 (e^{2z} - f^2)],
 // solved for the increment d = z - what:
 //   phi(d) = d + tau(l1 - l2 f^2) - A e^{-2d} + Bc e^{2d},  A = tau l1 f^2 e^{-2 what},
@@ -732,6 +742,35 @@ __device__ __forceinline__ int prox_newton(double what, double ft, double tau, d
                                            double l2, double tol, int cap, double& z_out,
                                            double& em_out, double& ep_out) {
     const double f2 = ft * ft;
+    // Fast path: three Newton steps on d in fp32 (MUFU exponentials, ~1e-7 relative), then ONE fp64
+    // Newton step from there -- quadratic convergence takes the fp32 error to ~1e-14, accepted by
+    // the same error bound as below; one fp64 exponential pair (at z0 = what + d32) instead of two
+    if (fabs(what) <= 40.0) {
+        const float tl1f2 = (float)(tau * l1 * f2), tl2 = (float)(tau * l2), c0f = (float)(tau * (l1 - l2 * f2));
+        const float wf = (float)what;
+        const float Af = tl1f2 * ex2_approx(-2.8853900817779268f * wf), Bf = tl2 * ex2_approx(2.8853900817779268f * wf);
+        float d = -(c0f - Af + Bf) * rcp_approx(1.0f + 2.0f * (Af + Bf));
+#pragma unroll
+        for (int k = 0; k < FOE_K2_F32_STEPS; ++k) {
+            const float p = ex2_approx(2.8853900817779268f * d), q = rcp_approx(p);
+            const float am = Af * q, bp = Bf * p;
+            d -= (d + c0f - am + bp) * rcp_approx(1.0f + 2.0f * (am + bp));
+        }
+        const double z0 = what + (double)d;
+        double Ep0, Em0;
+        exp2a_pm(z0, Ep0, Em0);                    // e^{2 z0}, e^{-2 z0}
+        const double am = tau * l1 * f2 * Em0, bp = tau * l2 * Ep0;
+        const double phi = (double)d + tau * (l1 - l2 * f2) - am + bp;
+        const double dphi = 1.0 + 2.0 * (am + bp);
+        const double st = phi * rcp_f64(dphi);
+        if (isfinite(st) && (dphi - 1.0) * st * st <= 0.25 * tol && fabs(st) <= 1e-6) {
+            const double e = -2.0 * st;                                  // e^{+-e}, |e| <= 2e-6
+            z_out = z0 - st;
+            ep_out = Ep0 * fma(0.5 * e, e, 1.0 + e);
+            em_out = Em0 * fma(0.5 * e, e, 1.0 - e);
+            return 4;
+        }
+    }
     double Em, Ep;
     if (fabs(what) <= 340.0) {
         exp2a_pm(what, Ep, Em);                    // e^{2 what}, e^{-2 what}
