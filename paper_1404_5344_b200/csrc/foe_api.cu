@@ -124,19 +124,25 @@ void k1_dispatch(int m, bool hvp, const K1Args& a, const TapParams& tp, const fo
     }
 }
 
-// K8 (tensor-core stencil): output tile rows (= the 64-row bands of the slab path)
+// K8 (tensor-core stencil): output tile rows -- 64 (the bands of the slab path, and the batch
+// path when the launch fills the GPU), or 32 / 16 for single images that cannot fill 148 SMs with
+// 64-row tiles (plan_stencil)
 constexpr int kTcR = 64;
-template <int M, int NP>
-constexpr int tc_smem() { return foe::TcGeom<M, NP, kTcR>::SMEM_BYTES; }
-template <int M, int NP>
-constexpr int th_smem() { return foe::ThGeom<M, NP, kTcR>::SMEM_BYTES; }
+template <int M, int NP, int R>
+constexpr int th_smem() { return foe::ThGeom<M, NP, R>::SMEM_BYTES; }
 template <int M, int NP>
 cudaError_t tc_set_attr() {
-    cudaError_t e = cudaFuncSetAttribute(foe::k_prior_grad_tc<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         tc_smem<M, NP>());
+    cudaError_t e = cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         th_smem<M, NP, 64>());
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, kTcR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                th_smem<M, NP>());
+    e = cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             th_smem<M, NP, 32>());
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             th_smem<M, NP, 16>());
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                th_smem<M, NP, 8>());
 }
 // the banks K8 has an instantiation for: (m, padded N_f)
 int tc_np(int m, int nf) {
@@ -159,16 +165,10 @@ struct foe_model {
     double lam[2] = {0, 0};
     TapParams* tp = nullptr;        // host copy, passed by value to the HVP stencil launches
     foe::TapParams2* tp2 = nullptr; // pair-interleaved taps of the paired-FMA stencil
-    // K8: B operand images (tf32 hi/lo, K-major canonical layout), sum k_i, theta_i ln 2
-    int tc_np = 0;                  // padded N_f of the K8 instantiation (0: no K8 for this bank)
-    float* tc_bimg = nullptr;
-    float* tc_sumk = nullptr;
-    float* tc_thl = nullptr;
-    foe::TcConst* tc_const = nullptr;  // per-filter epilogue constants, passed by value to K8
     // K8 (fp16 tensor cores, foe_th.cuh): fp16 hi/lo B images and the epilogue constants
+    int tc_np = 0;                  // padded N_f of the K8 instantiation (0: no K8 for this bank)
     unsigned char* th_bimg = nullptr;
     foe::ThConst* th_const = nullptr;
-    bool th_tf32 = false;           // FOE_K8_TF32=1 (read once at creation): the round-1 TF32 K8
     int stencil = FOE_STENCIL_AUTO; // foe_energy_grad's choice
     bool persist_phases = false;
     cudaMemPool_t pool = nullptr;   // private stream-ordered pool of the per-call scratch    // FOE_PERSIST_PHASES=1 (read once here): persistent-driver phase timings
@@ -220,59 +220,6 @@ struct ipiano_state {
 };
 
 namespace {
-
-float tf32_host(float x) {  // = cvt.rna.tf32.f32 (round to nearest, ties away from zero)
-    uint32_t u;
-    std::memcpy(&u, &x, 4);
-    if ((u & 0x7F800000u) != 0x7F800000u) u = (u + 0x1000u) & 0xFFFFE000u;
-    float r;
-    std::memcpy(&r, &u, 4);
-    return r;
-}
-
-// K8 operand images (foe_tc.cuh): Kf[t][i] = flipped tap t of filter i (K-major: [t/4][i][t%4]),
-// Kb[i][t] = 2 theta_i k_i[t] for t < NB ([i/4][t][i%4]); each as tf32 hi then lo = tf32(v - hi);
-// then the last tap of Kb (t = m*m - 1, done on CUDA cores) as a plain fp32 vector [NP].
-foe_status build_tc_images(foe_model* md) {
-    const int m = md->m, nf = md->nf, NP = md->tc_np;
-    const int KT = ((m * m + 7) / 8) * 8, NB = (m * m / 8) * 8;
-    const size_t BF = (size_t)KT * NP, BB = (size_t)NP * NB;
-    std::vector<float> img(2 * BF + 2 * BB + NP, 0.0f), sumk(NP, 0.0f), thl(NP, 0.0f);
-    for (int i = 0; i < nf; ++i) {
-        for (int t = 0; t < m * m; ++t) {
-            const float vf = md->tp->fwd[i * m * m + t], vb = md->tp->bwd[i * m * m + t];
-            const size_t of = (size_t)(t / 4) * NP * 4 + (size_t)i * 4 + t % 4;
-            const float fh = tf32_host(vf);
-            img[of] = fh;
-            img[BF + of] = tf32_host(vf - fh);
-            if (t < NB) {
-                const size_t ob = (size_t)(i / 4) * NB * 4 + (size_t)t * 4 + i % 4;
-                const float bh = tf32_host(vb);
-                img[2 * BF + ob] = bh;
-                img[2 * BF + BB + ob] = tf32_host(vb - bh);
-            } else {
-                img[2 * BF + 2 * BB + i] = vb;
-            }
-        }
-        sumk[i] = md->tp->sumk[i];
-        thl[i] = (float)md->tp->theta_ln2[i];
-    }
-    md->tc_const = new (std::nothrow) foe::TcConst();
-    if (!md->tc_const) return fail(FOE_ERR_OUT_OF_MEMORY, "host allocation");
-    std::memset(md->tc_const, 0, sizeof(foe::TcConst));
-    for (int i = 0; i < nf; ++i) {
-        md->tc_const->sumk[i] = sumk[i];
-        md->tc_const->thl[i] = thl[i];
-        md->tc_const->kbl[i] = img[2 * BF + 2 * BB + i];
-    }
-    CK(cudaMalloc((void**)&md->tc_bimg, img.size() * sizeof(float)));
-    CK(cudaMalloc((void**)&md->tc_sumk, NP * sizeof(float)));
-    CK(cudaMalloc((void**)&md->tc_thl, NP * sizeof(float)));
-    CK(cudaMemcpy(md->tc_bimg, img.data(), img.size() * sizeof(float), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(md->tc_sumk, sumk.data(), NP * sizeof(float), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(md->tc_thl, thl.data(), NP * sizeof(float), cudaMemcpyHostToDevice));
-    return FOE_OK;
-}
 
 // K8 fp16 operand images (foe_th.cuh), element (k, n) of a K-major B matrix at half offset
 // chunk(k/16) * 2 N 8 + ((k % 16) / 8) N 8 + n 8 + k % 8, hi image then lo image:
@@ -449,8 +396,6 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
     {
         const char* ph = std::getenv("FOE_PERSIST_PHASES");   // diagnostics only, read once
         md->persist_phases = ph != nullptr && ph[0] == '1';
-        const char* k8 = std::getenv("FOE_K8_TF32");          // A/B against the round-1 TF32 K8, read once
-        md->th_tf32 = k8 != nullptr && k8[0] == '1';
     }
     md->lam[0] = lam[0];
     md->lam[1] = lam[1];
@@ -480,8 +425,7 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
     }
     md->tc_np = tc_np(m, n_filters);
     if (md->tc_np) {
-        foe_status r = build_tc_images(md);
-        if (r == FOE_OK) r = build_th_images(md);
+        foe_status r = build_th_images(md);
         if (r != FOE_OK) { foe_model_destroy(md); return r; }
     }
     *out = md;
@@ -503,14 +447,10 @@ void foe_model_destroy(foe_model* model) {
     if (!model) return;
     if (model->run_state) ipiano_state_destroy(model->run_state);
     if (model->io_buf) cudaFree(model->io_buf);
-    if (model->tc_bimg) cudaFree(model->tc_bimg);
-    if (model->tc_sumk) cudaFree(model->tc_sumk);
-    if (model->tc_thl) cudaFree(model->tc_thl);
     if (model->th_bimg) cudaFree(model->th_bimg);
     delete model->th_const;
     // outstanding stream-ordered frees are honoured: the pool is released once they land
     if (model->pool) cudaMemPoolDestroy(model->pool);
-    delete model->tc_const;
     delete model->tp;
     delete model->tp2;
     delete model;
@@ -552,27 +492,51 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
                   bool allow_pack = true) {
     Plan p;
     const int ow = 128 - (md->m - 1);
-    bool tc = md->tc_np != 0 && pref != FOE_STENCIL_FFMA;
-    if (tc && pref == FOE_STENCIL_AUTO)
-        tc = (long long)div_up(W, ow) * div_up(H_grid, kTcR) * B >= 2LL * md->nsm;
-    if (tc) {
-        p.kind = FOE_STENCIL_TENSOR;
-        // full tiles of ow columns per band of R rows; the remainder columns of several bands share
-        // one packed tile (not for row slabs, whose energy partials are per 64-row band).  v7
-        // (streamed u tile) takes R from {64, 128, 256}: fewest waves x response rows per tile.
-        const bool pack_ok = allow_pack && H_grid == H;
+    const bool pack_ok = allow_pack && H_grid == H;
+    // K8 tiling with R output rows: full tiles of ow columns per band of R rows; the remainder
+    // columns of several bands share one packed tile (not for row slabs, whose energy partials are
+    // per 64-row band)
+    auto tiling = [&](int R, Plan& q) {
         int nfull = W / ow, rem = W - nfull * ow, spt = 0;
         if (rem > 0 && pack_ok) {
             spt = 128 / ((rem + 2 * (md->m - 1) + 7) & ~7);   // strips of a multiple of 8 lanes
             if (spt < 2) spt = 0;
         }
         if (rem > 0 && spt == 0) { nfull += 1; rem = 0; }
-        const int nbands = div_up(H, kTcR);
-        p.tiles_x = nfull;
-        p.ntiles = nbands * nfull + (rem > 0 ? div_up(nbands, spt) : 0);
-        p.tc_rem = rem;
-        p.tc_spt = spt;
-        p.tc_rows = kTcR;
+        const int nbands = div_up(H, R);
+        q.tiles_x = nfull;
+        q.ntiles = nbands * nfull + (rem > 0 ? div_up(nbands, spt) : 0);
+        q.tc_rem = rem;
+        q.tc_spt = spt;
+        q.tc_rows = R;
+    };
+    // R: 64 unless a single small image cannot fill the GPU with 64-row tiles; then the R with the
+    // fewest (waves of 2 CTAs per SM) x (response rows + ~8 rows of prologue) -- c3 (512^2): R = 8,
+    // 278 CTAs instead of 35.  Row slabs keep R = 64 (their bands).
+    int bestR = kTcR;
+    if (pack_ok) {
+        double best = 1e30;
+        for (int R : {64, 32, 16, 8}) {
+            Plan q;
+            tiling(R, q);
+            const double waves = std::ceil((double)q.ntiles * B / (2.0 * md->nsm));
+            const double cost = waves * (R + (md->m - 1) + 8);
+            if (cost < best - 1e-9) { best = cost; bestR = R; }
+        }
+    }
+    bool tc = md->tc_np != 0 && pref != FOE_STENCIL_FFMA;
+    if (tc && pref == FOE_STENCIL_AUTO) {
+        if (!pack_ok) {   // row slabs: the whole scene's 64-row tiles fill two CTAs per SM
+            tc = (long long)div_up(W, ow) * div_up(H_grid, kTcR) * B >= 2LL * md->nsm;
+        } else {
+            Plan q;
+            tiling(bestR, q);
+            tc = (long long)q.ntiles * B >= (3LL * md->nsm) / 4;
+        }
+    }
+    if (tc) {
+        p.kind = FOE_STENCIL_TENSOR;
+        tiling(bestR, p);
         p.groups = 1;
     } else {
         p.kind = FOE_STENCIL_FFMA;
@@ -600,24 +564,23 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
     foe::TcArgs ta;
     ta.k = a;
     ta.k.groups = 1;
-    ta.bimg = md->tc_bimg;
-    ta.sumk = md->tc_sumk;
-    ta.theta_ln2 = md->tc_thl;
+    ta.bimg = md->th_bimg;
     ta.tiles_x = a.tiles_x;
     count_launch(1);
-    if (md->th_tf32) {
-        if (md->tc_np == 48)
-            foe::k_prior_grad_tc<7, 48, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<7, 48>(), s>>>(ta, *md->tc_const);
-        else
-            foe::k_prior_grad_tc<5, 32, kTcR><<<dim3(a.ntiles, B), 256, tc_smem<5, 32>(), s>>>(ta, *md->tc_const);
-        CKL("k_prior_grad_tc");
-        return FOE_OK;
+    const dim3 grid(a.ntiles, B);
+    constexpr int T = 256;
+    const int R = a.tc_rows;
+    if (md->tc_np == 48) {
+        if (R == 8) foe::k_prior_grad_th<7, 48, 8><<<grid, T, th_smem<7, 48, 8>(), s>>>(ta, *md->th_const);
+        else if (R == 16) foe::k_prior_grad_th<7, 48, 16><<<grid, T, th_smem<7, 48, 16>(), s>>>(ta, *md->th_const);
+        else if (R == 32) foe::k_prior_grad_th<7, 48, 32><<<grid, T, th_smem<7, 48, 32>(), s>>>(ta, *md->th_const);
+        else foe::k_prior_grad_th<7, 48, 64><<<grid, T, th_smem<7, 48, 64>(), s>>>(ta, *md->th_const);
+    } else {
+        if (R == 8) foe::k_prior_grad_th<5, 32, 8><<<grid, T, th_smem<5, 32, 8>(), s>>>(ta, *md->th_const);
+        else if (R == 16) foe::k_prior_grad_th<5, 32, 16><<<grid, T, th_smem<5, 32, 16>(), s>>>(ta, *md->th_const);
+        else if (R == 32) foe::k_prior_grad_th<5, 32, 32><<<grid, T, th_smem<5, 32, 32>(), s>>>(ta, *md->th_const);
+        else foe::k_prior_grad_th<5, 32, 64><<<grid, T, th_smem<5, 32, 64>(), s>>>(ta, *md->th_const);
     }
-    ta.bimg = reinterpret_cast<const float*>(md->th_bimg);
-    if (md->tc_np == 48)
-        foe::k_prior_grad_th<7, 48, kTcR><<<dim3(a.ntiles, B), 256, th_smem<7, 48>(), s>>>(ta, *md->th_const);
-    else
-        foe::k_prior_grad_th<5, 32, kTcR><<<dim3(a.ntiles, B), 256, th_smem<5, 32>(), s>>>(ta, *md->th_const);
     CKL("k_prior_grad_th");
     return FOE_OK;
 }
@@ -1252,7 +1215,7 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     // trial-loop driver (f4): persistent for problems that cannot fill the GPU
     const long long npx = (long long)B * H * W;
     const bool want_persist = cfg.solver == FOE_SOLVER_PERSISTENT ||
-                              (cfg.solver == FOE_SOLVER_AUTO && cfg.stencil != FOE_STENCIL_TENSOR && npx <= (1LL << 18));
+                              (cfg.solver == FOE_SOLVER_AUTO && cfg.stencil != FOE_STENCIL_TENSOR && npx < (1LL << 18));
     const int pref = want_persist ? FOE_STENCIL_FFMA : cfg.stencil;
     const Plan pl = plan_stencil(md, B, H, W, H, pref, cfg.filter_groups, !t_slab_member);
     st->kind = pl.kind;

@@ -73,15 +73,20 @@ def _same_trajectory(a, b, wtol=1e-12):
 @pytest.mark.parametrize("name,iters", [("c1", 100), ("c2", 60), ("c3", 20)])
 def test_persistent_matches_graph(name, iters):
     cfg, d, md, L0 = _inputs(name)
-    a = _run(md, d, L0, iters, P.FOE_SOLVER_GRAPH)
+    a = _run(md, d, L0, iters, P.FOE_SOLVER_GRAPH, stencil=P.FOE_STENCIL_FFMA)
     b = _run(md, d, L0, iters, P.FOE_SOLVER_PERSISTENT)
     assert a[0] == P.FOE_SOLVER_GRAPH and b[0] == P.FOE_SOLVER_PERSISTENT
     _same_trajectory(a, b)
-    # AUTO resolves to the persistent driver for these single-image configs
+    # AUTO resolves to the persistent FFMA driver for images below 2^18 pixels (c1, c2), and to
+    # the graph driver with the tensor-core stencil in small tiles from there (c3: 512^2)
     c = P.ipiano_config_default(max_iters=1)
     st = P.ipiano_state_create(md, _cuda(d["f"], torch.float32), d["lambdas"], L0, c)
-    assert P.ipiano_state_solver(st) == P.FOE_SOLVER_PERSISTENT
-    assert P.ipiano_state_stencil(st) == P.FOE_STENCIL_FFMA
+    if name == "c3":
+        assert P.ipiano_state_solver(st) == P.FOE_SOLVER_GRAPH
+        assert P.ipiano_state_stencil(st) == P.FOE_STENCIL_TENSOR
+    else:
+        assert P.ipiano_state_solver(st) == P.FOE_SOLVER_PERSISTENT
+        assert P.ipiano_state_stencil(st) == P.FOE_STENCIL_FFMA
 
 
 def test_persistent_P3_c1_against_oracle():
