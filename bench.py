@@ -59,6 +59,9 @@ def parse_args():
     ap.add_argument("--filter-groups", type=int, default=0, help="K1 filter groups per tile (0: automatic)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-p2p", action="store_true", help="c5: ghost rows over ncclSend/Recv instead of K2 peer stores")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="c5: weak = a (1024 N) x 8192 scene, 1024 rows per GPU (SURVEY 8(d)); strong = the "
+                         "fixed 8192^2 scene of BASELINE.json configs[4] cut into N slabs")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=60,
                     help="oracle sample: iterations on one image (~10 s of host CPU work)")
@@ -463,9 +466,11 @@ def main():
 
 
 def run_slabs(args, cfg):
-    """c5 (BASELINE.json configs[4]): one 8192^2 scene cut into N row slabs, one per GPU, with
-    the per-trial 6-row ghost exchange and band-partial all-gather over NCCL (strong scaling:
-    the scene is fixed).  A step = reset from f + `iters` iterations."""
+    """c5 (BASELINE.json configs[4]): one SAR-like scene cut into N row slabs, one per GPU, with
+    the per-trial 6-row ghost exchange and band-partial all-gather over NCCL (DESIGN.md
+    "Multi-GPU").  --scaling weak (default): a (1024 N) x 8192 scene, 1024 rows per GPU (SURVEY
+    8(d) "Scaling"); --scaling strong: the fixed 8192^2 scene.  A step = reset from f + `iters`
+    iterations."""
     import torch
     import foe_synth as S
     import paper_1404_5344_b200 as P
@@ -474,6 +479,8 @@ def run_slabs(args, cfg):
     rank, ws, local = D.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if args.scaling == "weak":
+        cfg = S.config("c5", H=1024 * ws, iters=cfg.iters)
     d = S.make_inputs(cfg)
     f_full = d["f"][0]
     Hg, W = f_full.shape
@@ -565,9 +572,11 @@ def run_slabs(args, cfg):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32",
             "dtype_detail": DTYPE_DETAIL[P.ipiano_state_stencil(member)], "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: {cfg.description}", "H": Hg, "W": W,
+            "config": {"workload": f"{cfg.name}: {cfg.description}" + (
+                           f" (weak scaling: {Hg} x {W} scene, 1024 rows per GPU)" if args.scaling == "weak" else ""),
+                       "H": Hg, "W": W,
                        "filters": f"{cfg.n_filters}x{cfg.m}x{cfg.m}", "iters": cfg.iters,
                        "slab_rows_per_gpu": r1 - r0,
                        "l2": "inputs (8192^2 fp64 state, 1.6 GB) larger than L2; 256 MiB flush between steps",

@@ -288,6 +288,21 @@ foe_status foe_comm_unique_id(void* id_out);
 foe_status foe_comm_create(const void* id, int nranks, int rank, int cuda_device, foe_comm** out);
 void foe_comm_destroy(foe_comm* comm);
 
+/* The ghost-row exchange of one trial as the NCCL point-to-point calls
+ * rank `rank` of `nranks` posts, in this order, on every rank (so that two messages between the
+ * same pair of ranks -- 2 ranks, or 1 rank with itself -- match): plan_out[4][3] = {op, peer
+ * rank, buffer}, op FOE_HALO_SEND / _RECV, buffer FOE_HALO_TOP_ROWS (this slab's first kHalo = 6
+ * rows), _BOTTOM_GHOST (the ghost rows below the slab), _BOTTOM_ROWS (its last 6 rows),
+ * _TOP_GHOST.  Host only (no CUDA call); the library's exchange follows it, and
+ * tests/test_dist.py replays it with gloo.  FOE_ERR_INVALID_ARGUMENT unless 0 <= rank < nranks. */
+#define FOE_HALO_SEND 0
+#define FOE_HALO_RECV 1
+#define FOE_HALO_TOP_ROWS 0
+#define FOE_HALO_BOTTOM_GHOST 1
+#define FOE_HALO_BOTTOM_ROWS 2
+#define FOE_HALO_TOP_GHOST 3
+foe_status foe_slab_exchange_plan(int nranks, int rank, int* plan_out);
+
 typedef struct ipiano_slabs ipiano_slabs;
 
 /* Creates the slab decomposition of ONE scene of H_global x W pixels and initialises it

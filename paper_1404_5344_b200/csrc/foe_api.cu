@@ -555,7 +555,7 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
 }
 
 // Launch the prior energy+gradient evaluation `a` (tiling fields taken from the plan).
-foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStream_t s) {
+foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStream_t s, int ntiles_grid = -1) {
     if (kind == FOE_STENCIL_FFMA) {
         k1_dispatch(md->m, false, a, *md->tp, *md->tp2, dim3(a.ntiles * a.groups, B), s);
         CKL("k_prior_grad2");
@@ -567,7 +567,8 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
     ta.bimg = md->th_bimg;
     ta.tiles_x = a.tiles_x;
     count_launch(1);
-    const dim3 grid(a.ntiles, B);
+    const dim3 grid(ntiles_grid >= 0 ? ntiles_grid : a.ntiles - a.tile_off, B);
+    if (grid.x == 0) return FOE_OK;
     constexpr int T = 256;
     const int R = a.tc_rows;
     if (md->tc_np == 48) {
@@ -1612,7 +1613,9 @@ struct ipiano_slabs {
     bool up_opened = false, dn_opened = false;
     int* barrier_buf = nullptr;            // 1 int: the NCCL all-reduce that orders peer stores before K1
     cudaStream_t s = nullptr;
+    cudaStream_t sx = nullptr;             // the ghost-row exchange, overlapped with interior K8 bands
     cudaEvent_t sync_ev = nullptr;
+    cudaEvent_t ev_k2 = nullptr, ev_x = nullptr;
     cudaGraphExec_t graph = nullptr;
     bool use_graph = true;
 };
@@ -1667,7 +1670,7 @@ foe_status slab_k2(ipiano_slabs* g, int j) {
 
 // X: ghost rows.  Top ghost of slab i = last kHalo rows of slab i-1; bottom ghost = first
 // kHalo rows of slab i+1 (periodic ring).
-foe_status slab_exchange(ipiano_slabs* g) {
+foe_status slab_exchange(ipiano_slabs* g, cudaStream_t xs) {
     const size_t hp = (size_t)foe::kHalo * g->W;
     if (g->comm == nullptr) return FOE_OK;   // K2 stored the rows into the neighbours' ghost buffers
     const NcclApi& api = nccl_api();
@@ -1675,18 +1678,20 @@ foe_status slab_exchange(ipiano_slabs* g) {
         // the peers' K2 stored straight into our ghost rows; a 1-element all-reduce orders every
         // rank's K2 (and its system-scope fence) before any rank's K1
         if (g->comm->nranks > 1)
-            CKN(api.AllReduce(g->barrier_buf, g->barrier_buf, 1, ncclInt32, ncclSum, g->comm->comm, g->s));
+            CKN(api.AllReduce(g->barrier_buf, g->barrier_buf, 1, ncclInt32, ncclSum, g->comm->comm, xs));
         return FOE_OK;
     }
-    const int R = g->comm->nranks, r = g->comm->rank;
-    const int up = (r + R - 1) % R, dn = (r + 1) % R;
-    // One fixed posting order on every rank, so that two messages between the same pair of
-    // ranks (G = 2, or G = 1 to itself) match: send up, recv down, send down, recv up.
+    // One fixed posting order on every rank (foe_slab_exchange_plan, which tests/test_dist.py
+    // replays with gloo), so that two messages between the same pair of ranks (G = 2, or G = 1
+    // to itself) match: send up, recv down, send down, recv up.
+    int plan[4][3];
+    foe_slab_exchange_plan(g->comm->nranks, g->comm->rank, &plan[0][0]);
+    double* buf[4] = {g->halo_send, g->halo + hp, g->halo_send + hp, g->halo};   // FOE_HALO_* ids
     CKN(api.GroupStart());
-    CKN(api.Send(g->halo_send, hp, ncclFloat64, up, g->comm->comm, g->s));          // my top rows
-    CKN(api.Recv(g->halo + hp, hp, ncclFloat64, dn, g->comm->comm, g->s));          // below's top rows
-    CKN(api.Send(g->halo_send + hp, hp, ncclFloat64, dn, g->comm->comm, g->s));     // my bottom rows
-    CKN(api.Recv(g->halo, hp, ncclFloat64, up, g->comm->comm, g->s));               // above's bottom rows
+    for (int k = 0; k < 4; ++k) {
+        if (plan[k][0] == FOE_HALO_SEND) CKN(api.Send(buf[plan[k][2]], hp, ncclFloat64, plan[k][1], g->comm->comm, xs));
+        else CKN(api.Recv(buf[plan[k][2]], hp, ncclFloat64, plan[k][1], g->comm->comm, xs));
+    }
     CKN(api.GroupEnd());
     return FOE_OK;
 }
@@ -1723,8 +1728,13 @@ foe_status slab_round(ipiano_slabs* g, bool timed) {
     foe_status r;
     for (size_t j = 0; j < g->members.size(); ++j)
         if ((r = slab_k2(g, (int)j)) != FOE_OK) return r;
-    if ((r = slab_exchange(g)) != FOE_OK) return r;
-    for (size_t j = 0; j < g->members.size(); ++j) {
+    // K8 in two parts: the interior bands need no ghost rows and run while
+    // the exchange (NCCL on the side stream sx) moves them; the two boundary bands follow it.  The
+    // same tiles with the same arithmetic either way, so the result does not depend on the split.
+    const ipiano_state* s0 = g->members[0];
+    const bool split = s0->kind == FOE_STENCIL_TENSOR && g->nb_local >= 3 && s0->tc_rows == kTcR;
+    const int tx = s0->tiles_x, nb = g->nb_local;
+    auto k8 = [&](int j, int tile_off, int ntiles) -> foe_status {
         ipiano_state* st = g->members[j];
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (timed) {
@@ -1732,13 +1742,33 @@ foe_status slab_round(ipiano_slabs* g, bool timed) {
             e1 = pool_event(st);
             CK(cudaEventRecord(e0, g->s));
         }
-        foe_status rl = launch_prior(st->model, st->kind, slab_k1_args(g, (int)j, 0), 1, g->s);
+        K1Args a = slab_k1_args(g, j, 0);
+        a.tile_off = tile_off;
+        foe_status rl = launch_prior(st->model, st->kind, a, 1, g->s, ntiles);
         if (rl != FOE_OK) return rl;
         if (timed) {
             CK(cudaEventRecord(e1, g->s));
             st->ev_live.emplace_back(e0, e1);
             st->k1_launches += 1;
         }
+        return FOE_OK;
+    };
+    if (split) {
+        CK(cudaEventRecord(g->ev_k2, g->s));
+        CK(cudaStreamWaitEvent(g->sx, g->ev_k2, 0));
+        if ((r = slab_exchange(g, g->sx)) != FOE_OK) return r;
+        CK(cudaEventRecord(g->ev_x, g->sx));
+        for (size_t j = 0; j < g->members.size(); ++j)
+            if ((r = k8((int)j, tx, (nb - 2) * tx)) != FOE_OK) return r;                 // interior bands
+        CK(cudaStreamWaitEvent(g->s, g->ev_x, 0));
+        for (size_t j = 0; j < g->members.size(); ++j) {
+            if ((r = k8((int)j, 0, tx)) != FOE_OK) return r;                             // band 0
+            if ((r = k8((int)j, (nb - 1) * tx, s0->ntiles - (nb - 1) * tx)) != FOE_OK) return r;   // last band
+        }
+    } else {
+        if ((r = slab_exchange(g, g->s)) != FOE_OK) return r;
+        for (size_t j = 0; j < g->members.size(); ++j)
+            if ((r = k8((int)j, 0, -1)) != FOE_OK) return r;
     }
     if ((r = slab_bands(g)) != FOE_OK) return r;
     for (size_t j = 0; j < g->members.size(); ++j) {
@@ -1785,7 +1815,7 @@ foe_status slab_init(ipiano_slabs* g, const float* f, double L_init, cudaStream_
         count_launch(1);
         CKL("k_init (slab)");
     }
-    foe_status r = slab_exchange(g);
+    foe_status r = slab_exchange(g, g->s);
     if (r != FOE_OK) return r;
     for (size_t j = 0; j < g->members.size(); ++j) {
         ipiano_state* st = g->members[j];
@@ -1849,6 +1879,18 @@ foe_status slab_ensure_graph(ipiano_slabs* g) {
 
 extern "C" {
 
+foe_status foe_slab_exchange_plan(int nranks, int rank, int* plan_out) {
+    if (nranks < 1 || rank < 0 || rank >= nranks || !plan_out)
+        return fail(FOE_ERR_INVALID_ARGUMENT, "nranks=%d rank=%d plan_out=%p", nranks, rank, (void*)plan_out);
+    const int up = (rank + nranks - 1) % nranks, dn = (rank + 1) % nranks;
+    const int plan[4][3] = {{FOE_HALO_SEND, up, FOE_HALO_TOP_ROWS},        // my first kHalo rows -> above
+                            {FOE_HALO_RECV, dn, FOE_HALO_BOTTOM_GHOST},    // below's first rows
+                            {FOE_HALO_SEND, dn, FOE_HALO_BOTTOM_ROWS},     // my last rows -> below
+                            {FOE_HALO_RECV, up, FOE_HALO_TOP_GHOST}};      // above's last rows
+    std::memcpy(plan_out, plan, sizeof(plan));
+    return FOE_OK;
+}
+
 foe_status foe_comm_unique_id(void* id_out) {
     if (!id_out) return fail(FOE_ERR_INVALID_ARGUMENT, "id_out is NULL");
     const NcclApi& api = nccl_api();
@@ -1906,7 +1948,11 @@ void ipiano_slabs_destroy(ipiano_slabs* g) {
     if (g->dn_opened && g->peer_dn != g->peer_up) cudaIpcCloseMemHandle(g->peer_dn);
     if (g->barrier_buf) cudaFree(g->barrier_buf);
     if (g->sync_ev) cudaEventDestroy(g->sync_ev);
+    if (g->ev_k2) cudaEventDestroy(g->ev_k2);
+    if (g->ev_x) cudaEventDestroy(g->ev_x);
+    if (g->sx) cudaStreamSynchronize(g->sx);
     if (g->s) cudaStreamDestroy(g->s);
+    if (g->sx) cudaStreamDestroy(g->sx);
     delete g;
     cudaGetLastError();   // destroy reports nothing: leave no stale error for the next launch check
 }
@@ -1958,7 +2004,10 @@ foe_status ipiano_slabs_create(const foe_model* md, const float* f, int H_global
     g->pxt = W % 64 == 0 ? 16 : kPxt2;
     g->bpb = foe::kBandRows * W / (kThreads * g->pxt);
     CK(cudaStreamCreateWithFlags(&g->s, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&g->sx, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g->sync_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&g->ev_k2, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&g->ev_x, cudaEventDisableTiming));
     const size_t he = halo_elems(g);
     if (cudaMalloc((void**)&g->band_all, sizeof(double) * g->nb_global * foe::kNumPart) != cudaSuccess ||
         cudaMalloc((void**)&g->halo, sizeof(double) * he * nmem) != cudaSuccess ||

@@ -89,7 +89,10 @@ struct K1Args {
     // columns; the last tc_rem columns of tc_spt consecutive bands share one tile (strips of
     // tc_rem + 4C lanes), instead of one mostly idle tile per band
     int tc_rem, tc_spt;
-    int tc_rows;            // K8 v7 (streamed u tile): output rows per tile (v3: the 64 of kTcR)
+    int tc_rows;            // K8: output rows per tile (64 / 32 / 16 / 8)
+    // K8 launch over a tile range (row slabs: interior bands before the ghost-row exchange, the
+    // two boundary bands after it): tile = tile_off + blockIdx.x; energy partials by tile index
+    int tile_off;
     int ncp;                // K1 v2: filter pairs per shared-memory chunk (1 or 2; 0 = 2)
     // HVP only
     const double* v;        // [B][H][W]

@@ -205,7 +205,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
     }
     const int H = args.H, W = args.W;
     const size_t HW = (size_t)H * W;
-    const int tile = blockIdx.x;
+    const int tile = args.tile_off + blockIdx.x;
     const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
     const int t = threadIdx.x, warp = __shfl_sync(0xffffffffu, t >> 5, 0);
     const int wg = warp >> 2;                                   // warp group (0, 1)
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
     }
     // (a7) per-CTA energy partial (fixed order)
     const double e = block_sum_d(e_acc, red);
-    if (t == 0) args.epart[(size_t)b * args.ntiles * args.groups + blockIdx.x] = e;
+    if (t == 0) args.epart[(size_t)b * args.ntiles * args.groups + tile] = e;
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc<G::TCOLS>(tb);

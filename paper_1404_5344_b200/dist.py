@@ -86,12 +86,6 @@ def ring_neighbours(rank: int, world_size: int) -> tuple:
     return (rank - 1) % world_size, (rank + 1) % world_size
 
 
-# The posting order of the ghost-row exchange (foe_api.cu slab_exchange): the same on every
-# rank, so that two messages between one pair of ranks (2 ranks, or 1 rank with itself) match.
-HALO_POSTING_ORDER = (("send", "up", "top_rows"), ("recv", "down", "bottom_ghost"),
-                      ("send", "down", "bottom_rows"), ("recv", "up", "top_ghost"))
-
-
 def share_bytes(payload, src: int = 0) -> bytes:
     """Broadcast a small byte string (e.g. the NCCL unique id) from rank src to all ranks."""
     import torch.distributed as dist

@@ -31,7 +31,7 @@ EXPORTED = (
     "ipiano_state_create", "ipiano_state_reset", "ipiano_step", "ipiano_solve", "ipiano_get_iterate",
     "ipiano_get_counters", "ipiano_get_trace", "ipiano_profile", "ipiano_profile_read",
     "ipiano_state_destroy", "ipiano_state_stencil", "ipiano_state_solver", "ipiano_run",
-    "foe_model_set_stencil", "foe_comm_unique_id", "foe_comm_create", "foe_comm_destroy", "ipiano_slabs_create", "ipiano_slabs_reset",
+    "foe_model_set_stencil", "foe_slab_exchange_plan", "foe_comm_unique_id", "foe_comm_create", "foe_comm_destroy", "ipiano_slabs_create", "ipiano_slabs_reset",
     "ipiano_slabs_solve", "ipiano_slabs_advance", "ipiano_slabs_get_iterate", "ipiano_slabs_member", "ipiano_slabs_destroy",
     "ipiano_slabs_halo_handle", "ipiano_slabs_connect_peers", "ipiano_slabs_disconnect_peers",
     "foe_psnr", "foe_ssim", "foe_add_speckle",
@@ -103,6 +103,7 @@ def lib():
                              _vp, _vp, C.c_size_t, _vp]
     L.foe_model_set_stencil.argtypes = [_vp, C.c_int]
     L.foe_comm_unique_id.argtypes = [_vp]
+    L.foe_slab_exchange_plan.argtypes = [C.c_int, C.c_int, _vp]
     L.foe_comm_create.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]
     L.foe_comm_destroy.argtypes = [_vp]
     L.foe_comm_destroy.restype = None
@@ -480,6 +481,18 @@ class Comm:
             self.destroy()
         except Exception:
             pass
+
+
+FOE_HALO_SEND, FOE_HALO_RECV = 0, 1
+FOE_HALO_TOP_ROWS, FOE_HALO_BOTTOM_GHOST, FOE_HALO_BOTTOM_ROWS, FOE_HALO_TOP_GHOST = 0, 1, 2, 3
+
+
+def foe_slab_exchange_plan(nranks: int, rank: int):
+    """The ghost-row exchange the library posts on rank `rank` (include/foe.h): four
+    (op, peer, buffer) triples in posting order.  Host only: no GPU needed."""
+    plan = (C.c_int * 12)()
+    _check(lib().foe_slab_exchange_plan(int(nranks), int(rank), C.cast(plan, _vp)))
+    return [tuple(plan[3 * k: 3 * k + 3]) for k in range(4)]
 
 
 def foe_comm_unique_id() -> bytes:

@@ -3,10 +3,10 @@
 * batch sharding: weak shards are disjoint and keep global image ids; balanced shards
   partition a fixed batch with the same looks mix on every rank;
 * the timing reductions (max / sum over ranks) and the byte broadcast of the NCCL id;
-* the row-slab ring: slab ranges, neighbours, and the ghost-row posting order of
-  foe_api.cu (send up, recv down, send down, recv up) replayed with gloo point-to-point
-  messages: every rank's ghost rows equal the periodic neighbours' boundary rows, for 2
-  ranks (both neighbours are the same peer) and 4;
+* the row-slab ring: slab ranges, neighbours, and the ghost-row exchange plan exported by
+  libfoe (foe_slab_exchange_plan: the order the C code posts its NCCL calls) replayed with gloo
+  point-to-point messages: every rank's ghost rows equal the periodic neighbours' boundary rows,
+  for 2 ranks (both neighbours are the same peer) and 4;
 * the band gather: per-band partials all-gathered in rank order are the scene's band order.
 """
 import os
@@ -33,21 +33,22 @@ def _free_port():
 
 
 def _exchange(slab: np.ndarray, rank: int, ws: int):
-    """Ghost rows by the library's posting order, with gloo isend/irecv."""
-    up, dn = D.ring_neighbours(rank, ws)
-    bufs = {"top_rows": torch.as_tensor(slab[:HALO].copy()), "bottom_rows": torch.as_tensor(slab[-HALO:].copy()),
-            "top_ghost": torch.empty(HALO, slab.shape[1], dtype=torch.float64),
-            "bottom_ghost": torch.empty(HALO, slab.shape[1], dtype=torch.float64)}
+    """Ghost rows by the plan libfoe itself posts (foe_slab_exchange_plan, the C code's exchange
+    order), replayed with gloo isend/irecv."""
+    import paper_1404_5344_b200 as P
+    bufs = {P.FOE_HALO_TOP_ROWS: torch.as_tensor(slab[:HALO].copy()),
+            P.FOE_HALO_BOTTOM_ROWS: torch.as_tensor(slab[-HALO:].copy()),
+            P.FOE_HALO_TOP_GHOST: torch.empty(HALO, slab.shape[1], dtype=torch.float64),
+            P.FOE_HALO_BOTTOM_GHOST: torch.empty(HALO, slab.shape[1], dtype=torch.float64)}
     reqs = []
-    for op, who, name in D.HALO_POSTING_ORDER:
-        peer = up if who == "up" else dn
-        if op == "send":
-            reqs.append(dist.isend(bufs[name], dst=peer))
+    for op, peer, buf in P.foe_slab_exchange_plan(ws, rank):
+        if op == P.FOE_HALO_SEND:
+            reqs.append(dist.isend(bufs[buf], dst=peer))
         else:
-            reqs.append(dist.irecv(bufs[name], src=peer))
+            reqs.append(dist.irecv(bufs[buf], src=peer))
     for r in reqs:
         r.wait()
-    return bufs["top_ghost"].numpy(), bufs["bottom_ghost"].numpy()
+    return bufs[P.FOE_HALO_TOP_GHOST].numpy(), bufs[P.FOE_HALO_BOTTOM_GHOST].numpy()
 
 
 def _worker(rank, ws, port, q):
@@ -141,6 +142,18 @@ def test_slab_ring_four_ranks():
     for rank in range(4):
         assert r[rank]["ghost_ok"] and r[rank]["bands"] == [0.0, 1.0, 2.0, 3.0]
         assert r[rank]["max"] == 4.0 and r[rank]["sum"] == 10.0
+
+
+def test_exchange_plan_is_the_ring_order():
+    """The exported plan: send up, recv down, send down, recv up, peers on the periodic ring."""
+    import paper_1404_5344_b200 as P
+    for ws, rank in ((1, 0), (2, 0), (2, 1), (8, 0), (8, 7)):
+        up, dn = D.ring_neighbours(rank, ws)
+        assert P.foe_slab_exchange_plan(ws, rank) == [
+            (P.FOE_HALO_SEND, up, P.FOE_HALO_TOP_ROWS), (P.FOE_HALO_RECV, dn, P.FOE_HALO_BOTTOM_GHOST),
+            (P.FOE_HALO_SEND, dn, P.FOE_HALO_BOTTOM_ROWS), (P.FOE_HALO_RECV, up, P.FOE_HALO_TOP_GHOST)]
+    with pytest.raises(P.FoeError):
+        P.foe_slab_exchange_plan(2, 2)
 
 
 def test_slab_geometry():
