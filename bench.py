@@ -328,13 +328,15 @@ def main():
     f_dev = torch.as_tensor(d["f"], device=dev)
     v0 = torch.as_tensor(S.lipschitz_start_vector(B, H, W), device=dev)
 
-    # setup: Lipschitz initialisation (R-10), timed separately
+    # setup: Lipschitz initialisation (R-10), timed separately (a warm call: the first call of a
+    # process also pays the lazy loading of the library's kernels, a one-time cost)
+    rho, L0 = P.foe_estimate_lipschitz(md, f_dev, v0, 25)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     rho, L0 = P.foe_estimate_lipschitz(md, f_dev, v0, 25)
     lipschitz_ms = 1e3 * (time.perf_counter() - t0)
     d["L0"] = L0
-    del v0
+    # (v0 stays: the e2e-with-setup leg re-runs the estimate)
 
     solver = {"auto": P.FOE_SOLVER_AUTO, "graph": P.FOE_SOLVER_GRAPH, "persistent": P.FOE_SOLVER_PERSISTENT}[args.solver]
     stencil = {"auto": P.FOE_STENCIL_AUTO, "ffma": P.FOE_STENCIL_FFMA, "tensor": P.FOE_STENCIL_TENSOR}[args.stencil]
@@ -437,6 +439,27 @@ def main():
                "h2d_bytes_per_step": int(f_np.nbytes), "d2h_bytes_per_step": int(u_np.nbytes),
                "ms_per_step": e2e_total / args.steps,
                "call": "ipiano_run (C ABI) with pinned host f and u; state alloc + a1..a13 + copies"}
+        # e2e with the required setup: H2D of f, the Lipschitz estimate (R-10: 25 power steps of
+        # Hessian-vector products on the tensor cores), then ipiano_run with host buffers
+        f_tmp = torch.empty((B, H, W), dtype=torch.float32, device=dev)
+        ews = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            f_tmp.copy_(f_pin, non_blocking=True)
+            _, L_s = P.foe_estimate_lipschitz(md, f_tmp, v0, 25)
+            P.ipiano_run(md, f_np, d["lambdas"], L_s, cfgc, u_out=u_np, want_trace=False)
+            e1.record(stream)
+            e1.synchronize()
+            ews.append(e0.elapsed_time(e1))
+        D.barrier()
+        ews_total = D.max_over_ranks(sum(ews), dev)
+        e2e["with_setup"] = {"value": mp_it_total / (ews_total / 1e3), "unit": UNIT,
+                             "ms_per_step": ews_total / args.steps,
+                             "call": "H2D f + foe_estimate_lipschitz + ipiano_run (host f, u)"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

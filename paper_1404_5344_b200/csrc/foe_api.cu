@@ -138,6 +138,9 @@ cudaError_t tc_set_attr() {
     e = cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              th_smem<M, NP, 32>());
     if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(foe::k_hvp_th<M, NP, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             foe::ThHGeom<M, NP, 64>::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              th_smem<M, NP, 16>());
     if (e != cudaSuccess) return e;
@@ -275,6 +278,13 @@ foe_status build_th_images(foe_model* md) {
     }
     md->th_const->inv_sf = (float)(1.0 / sf);
     md->th_const->inv_z = (float)(1.0 / (sb * (double)foe::kThPScale));
+    double kabs = 0.0;
+    for (int i = 0; i < nf; ++i) {
+        double t = 0.0;
+        for (int k = 0; k < TAPS; ++k) t += std::fabs((double)md->tp->fwd[(size_t)i * TAPS + k]);
+        kabs = std::max(kabs, t);
+    }
+    md->th_const->kabs = (float)kabs;
     CK(cudaMalloc((void**)&md->th_bimg, img.size() * sizeof(__half)));
     CK(cudaMemcpy(md->th_bimg, img.data(), img.size() * sizeof(__half), cudaMemcpyHostToDevice));
     return FOE_OK;
@@ -651,10 +661,43 @@ foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int 
         }
         return launch_prior(md, kind, a, B, s);
     }
+    if (md->tc_np) {
+        // K8h: the HVP on the tensor cores (whole images, 64-row tiles of 128 - 2C columns, no
+        // packing; one CTA per SM)
+        foe::TcArgs ta;
+        ta.k = a;
+        ta.k.groups = 1;
+        ta.k.tiles_x = div_up(W, 128 - (md->m - 1));
+        ta.k.ntiles = ta.k.tiles_x * div_up(H, kTcR);
+        ta.k.tile_off = 0;
+        ta.bimg = md->th_bimg;
+        ta.tiles_x = ta.k.tiles_x;
+        count_launch(1);
+        const dim3 grid(ta.k.ntiles, B);
+        if (md->tc_np == 48)
+            foe::k_hvp_th<7, 48, kTcR><<<grid, 256, foe::ThHGeom<7, 48, kTcR>::SMEM_BYTES, s>>>(ta, *md->th_const);
+        else
+            foe::k_hvp_th<5, 32, kTcR><<<grid, 256, foe::ThHGeom<5, 32, kTcR>::SMEM_BYTES, s>>>(ta, *md->th_const);
+        CKL("k_hvp_th");
+        return FOE_OK;
+    }
     dim3 grid(a.ntiles * groups, B);
     k1_dispatch(md->m, hvp, a, *md->tp, *md->tp2, grid, s);
     CKL("k_prior_grad launch");
     return FOE_OK;
+}
+
+// grad_w F at device w into g [B][H][W] (one plane: groups = 1), on the stencil the model's AUTO
+// plan picks (K8 for the banks it has, so the Lipschitz setup's gradient is a tensor-core one too)
+foe_status grad_direct(const foe_model* md, const double* w, int B, int H, int W, float* g, cudaStream_t s) {
+    const Plan pl = plan_stencil(md, B, H, W, H, FOE_STENCIL_AUTO, 1);
+    double* epart = nullptr;
+    CK(cudaMallocFromPoolAsync((void**)&epart, sizeof(double) * B * (size_t)std::max(pl.ntiles * pl.groups, 1),
+                               md->pool, s));
+    foe_status st = run_k1_plain(md, w, B, H, W, 1, epart, g, false, nullptr, nullptr, s, pl.kind, pl.tiles_x,
+                                 pl.ntiles, pl.tc_rem, pl.tc_spt, pl.tc_rows, pl.ncp, pl.nchunks);
+    CK(cudaFreeAsync(epart, s));
+    return st;
 }
 
 }  // namespace
@@ -745,7 +788,7 @@ foe_status foe_hvp(const foe_model* md, const double* w, const double* v, int B,
     float* gw = nullptr;
     CK(cudaMallocFromPoolAsync((void**)&epart, sizeof(double) * B * tiles, md->pool, s));
     CK(cudaMallocFromPoolAsync((void**)&gw, sizeof(float) * n, md->pool, s));
-    st = run_k1_plain(md, w, B, H, W, 1, epart, gw, false, nullptr, nullptr, s);
+    st = grad_direct(md, w, B, H, W, gw, s);
     if (st == FOE_OK) st = run_k1_plain(md, w, B, H, W, 1, epart, hv, true, v, gw, s);
     CK(cudaFreeAsync(epart, s));
     CK(cudaFreeAsync(gw, s));
@@ -784,7 +827,7 @@ foe_status foe_estimate_lipschitz(const foe_model* md, const float* f, int B, in
     foe::k_normalize<double><<<eb, 256, 0, s>>>(v0, v, sums, 3, 2, HW, B);
     count_launch(1);
     CKL("power-iteration init");
-    st = run_k1_plain(md, w0, B, H, W, 1, epart, gw, false, nullptr, nullptr, s);
+    st = grad_direct(md, w0, B, H, W, gw, s);
     for (int it = 0; it < power_iters && st == FOE_OK; ++it) {
         st = run_k1_plain(md, w0, B, H, W, 1, epart, h, true, v, gw, s);   // h = Hess v
         foe::k_dot3<<<dim3(nblk, B), kThreads, 0, s>>>(v, h, part, nblk, HW, kPxt2);

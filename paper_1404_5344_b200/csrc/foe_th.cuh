@@ -90,6 +90,7 @@ struct ThConst {
     float kbl[kMaxFilters];    // x s_b
     float inv_sf;   // 1 / s_f
     float inv_z;    // 1 / (s_b 2^14)
+    float kabs;     // max_i sum_t |k_i[t]| (bounds |K t| for the HVP's scale)
 };
 
 // fp16 hi/lo split of a float pair: hi = rn_fp16(x), lo = rn_fp16(x - hi) (x - hi exact in fp32)
@@ -436,6 +437,363 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc<G::TCOLS>(tb);
+}
+
+
+// =============================================================================================
+// K8h: the Hessian-vector product of F on the tensor cores (setup: the Lipschitz power iteration,
+// DESIGN.md R-10), the same tiles and operand scheme as K8 with a second forward GEMM:
+//   Hv = v (.) grad F + u (.) sum_i theta_i K_i^T [rho''(K_i u) (.) K_i t],  t = u (.) v   (w domain)
+//   Hv = sum_i theta_i K_i^T [rho''(K_i u) (.) K_i v]                                   (u domain)
+// with rho''(r)/2 = (1 - r^2) / (1 + r^2)^2 as the backward operand P (x 2^14).  T = K t runs on
+// a second TMEM ring of t rows (no DC shift: t has no large common value; its A2 slots are zero),
+// so one CTA per SM owns all 512 TMEM columns.  Whole images only (periodic wrap, no packing).
+template <int M, int NP, int R>
+struct ThHGeom {
+    using G = ThGeom<M, NP, R>;
+    static constexpr int RINGC = 2 * G::RS * 4;                 // one ring: 2 RS slots x 4 columns
+    static constexpr int COL_UH = 0, COL_UL = RINGC, COL_TH = 2 * RINGC, COL_TL = 3 * RINGC;
+    static constexpr int COL_D = 4 * RINGC, COL_DT = COL_D + NP, COL_Z = COL_D;
+    static constexpr int COL_PH = COL_DT + NP, COL_PL = COL_PH + NP / 2;
+    static constexpr int TCOLS = 512;
+    static_assert(COL_PL + NP / 2 <= 512, "TMEM budget");
+    // shared memory: K8's layout + the t tile
+    static constexpr int SM_T = G::SMEM_BYTES;
+    static constexpr int SMEM_BYTES = SM_T + G::UY * G::UP * 4 + 64;
+};
+
+// t tile staging: t = u v (w domain; u = e^w in fp64) or v (u domain), periodic, rounded to fp32
+template <int UY, int UX, int UP, int NWARPS>
+__device__ __forceinline__ void th_stage_t(float* ts, const double* w, const double* vv, int H, int W, int y0,
+                                           int x0, int c2, bool udom, int warp, int lane) {
+    constexpr int NX = (UX + 31) / 32;
+    int gx[NX];
+#pragma unroll
+    for (int k = 0; k < NX; ++k) gx[k] = wrap_idx(x0 - c2 + lane + 32 * k, W);
+    for (int uy = warp; uy < UY; uy += NWARPS) {
+        const size_t row = (size_t)wrap_idx(y0 - c2 + uy, H) * W;
+#pragma unroll
+        for (int k = 0; k < NX; ++k) {
+            const int ux = lane + 32 * k;
+            if (ux < UX) {
+                const size_t gi = row + gx[k];
+                ts[uy * UP + ux] = (float)(udom ? vv[gi] : exp(w[gi]) * vv[gi]);
+            }
+        }
+    }
+}
+
+// t-ring row: the halves [4 WG, 4 WG + 4) of t[y][l + b] s_t (taps b >= m are 0), slot s and s + RS
+template <int M, int UP, int RS, int WG>
+__device__ __forceinline__ void th_build_trow(const float* ts, int y, int l, float st, uint32_t t_h, uint32_t t_l,
+                                              int s) {
+    const float* tp = ts + y * UP;
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int b = WG * 4 + e;
+        v[e] = b < M ? tp[l + b] * st : 0.0f;
+    }
+    uint32_t h0, h1, l0, l1;
+    h2_split(make_float2(v[0], v[1]), h0, l0);
+    h2_split(make_float2(v[2], v[3]), h1, l1);
+    const uint32_t c0 = (uint32_t)(s * 4 + WG * 2), c1 = (uint32_t)((s + RS) * 4 + WG * 2);
+    tc::tmem_st2u(t_h + c0, h0, h1);
+    tc::tmem_st2u(t_h + c1, h0, h1);
+    tc::tmem_st2u(t_l + c0, l0, l1);
+    tc::tmem_st2u(t_l + c1, l0, l1);
+}
+
+// HVP epilogue of filter chunks [F0, F1): r = R / (s_u s_f) + u_q sum k, tv = T / (s_t s_f);
+// P = s_p (1 - r^2) tv / (1 + r^2)^2 (= s_p rho''(r) tv / 2) split into fp16 hi / lo pairs; the
+// caller passes it_s = s_p / (s_t s_f) (s_p: the tile's power of two keeping |P| < 2^14)
+template <int F0, int F1>
+__device__ __forceinline__ void th_hvp_epilogue(uint32_t t_d, uint32_t t_dt, uint32_t t_ph, uint32_t t_pl, float uq,
+                                                float inv, float it_s, const float* css, const float* kbl,
+                                                float& zlast) {
+    float r[(F1 - F0) * 8], tv[(F1 - F0) * 8];
+#pragma unroll
+    for (int f8 = F0; f8 < F1; ++f8) {
+        tc::tmem_ld8(t_d + f8 * 8, *reinterpret_cast<float(*)[8]>(r + (f8 - F0) * 8));
+        tc::tmem_ld8(t_dt + f8 * 8, *reinterpret_cast<float(*)[8]>(tv + (f8 - F0) * 8));
+    }
+    tc::wait_ld();
+    const float2 uq2 = make_float2(uq, uq), one2 = make_float2(1.f, 1.f), inv2 = make_float2(inv, inv);
+    const float2 it2 = make_float2(it_s, it_s);
+    float2 zl2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int f8 = F0; f8 < F1; ++f8) {
+        uint32_t ph[4], pl[4];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+            const int i = f8 * 8 + e, k = (f8 - F0) * 8 + e;
+            const float2 rv = __ffma2_rn(uq2, make_float2(css[i], css[i + 1]), __fmul2_rn(make_float2(r[k], r[k + 1]), inv2));
+            const float2 t2 = __fmul2_rn(make_float2(tv[k], tv[k + 1]), it2);
+            const float2 d = __ffma2_rn(rv, rv, one2);
+            const float2 omr = __ffma2_rn(make_float2(-rv.x, -rv.y), rv, one2);   // 1 - r^2
+            const float q = rcp_approx(d.x * d.y);
+            const float2 id = __fmul2_rn(make_float2(d.y, d.x), make_float2(q, q));   // 1 / d
+            const float2 pv = __fmul2_rn(__fmul2_rn(omr, t2), __fmul2_rn(id, id));
+            zl2 = __ffma2_rn(pv, make_float2(kbl[i], kbl[i + 1]), zl2);
+            h2_split(pv, ph[e / 2], pl[e / 2]);
+        }
+        tc::tmem_st4u(t_ph + f8 * 4, ph);
+        tc::tmem_st4u(t_pl + f8 * 4, pl);
+    }
+    zlast = zl2.x + zl2.y;
+}
+
+template <int M, int NP, int R>
+__global__ void __launch_bounds__(256, 1) k_hvp_th(const TcArgs ta, const __grid_constant__ ThConst cc) {
+    using G = ThGeom<M, NP, R>;
+    using GH = ThHGeom<M, NP, R>;
+    constexpr int C = G::C, L = G::LANES, RS = G::RS;
+    extern __shared__ __align__(128) unsigned char smb[];
+    float* us = reinterpret_cast<float*>(smb + G::SM_U);
+    float* ts = reinterpret_cast<float*>(smb + GH::SM_T);
+    float* zs = reinterpret_cast<float*>(smb + G::SM_Z);
+    float* hand = reinterpret_cast<float*>(smb + G::SM_HAND);
+    float* zls = reinterpret_cast<float*>(smb + G::SM_ZL);
+    __shared__ uint32_t tbase_s;
+    __shared__ __align__(8) uint64_t mbar_f, mbar_b, mbar_bimg;
+    __shared__ float wmax[16];
+
+    const K1Args& args = ta.k;
+    const int b = blockIdx.y;
+    const int H = args.H, W = args.W;
+    const size_t HW = (size_t)H * W;
+    const int tile = blockIdx.x;
+    const double* w = args.w + (size_t)b * HW;
+    const double* vv = args.v + (size_t)b * HW;
+    const int t = threadIdx.x, warp = __shfl_sync(0xffffffffu, t >> 5, 0);
+    const int wg = warp >> 2;
+    const int l = (warp & 3) * 32 + (t & 31);
+    const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
+    const int y0 = ty * R, x0 = tx * G::OW;
+
+    if (warp == 0) tc::tmem_alloc<GH::TCOLS>(&tbase_s);
+    if (t == 0) {
+        tc::mbar_init(&mbar_f, 1);
+        tc::mbar_init(&mbar_b, 1);
+        tc::mbar_init(&mbar_bimg, 1);
+        tc::mbar_fence_init();
+        tc::bulk_g2s(smb + G::SM_B, ta.bimg, (uint32_t)G::B_BYTES, &mbar_bimg);
+    }
+    const int yc = min(y0 + R / 2, H - 1), xc = min(x0 + G::OW / 2, W - 1);
+    const bool udom = args.udom != 0;
+    const double wc = w[(size_t)yc * W + xc];
+    const float cst = (float)(udom ? wc : exp(wc));
+    tc_stage_u<G::UY, G::UX, G::UP, 8>(us, w, nullptr, H, W, y0, x0, 2 * C, udom, cst, wc, warp, t & 31);
+    th_stage_t<G::UY, G::UX, G::UP, 8>(ts, w, vv, H, W, y0, x0, 2 * C, udom, warp, t & 31);
+    tc::fence_before_sync();
+    __syncthreads();
+    // power-of-two scales of the u differences and of t (as K8: magnitudes < 2^14)
+    float mu = 0.f, mt = 0.f;
+    for (int y = warp; y < G::UY; y += 8)
+        for (int x = t & 31; x < G::UX; x += 32) {
+            mu = fmaxf(mu, fabsf(us[y * G::UP + x]));
+            mt = fmaxf(mt, fabsf(ts[y * G::UP + x]));
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mu = fmaxf(mu, __shfl_xor_sync(0xffffffffu, mu, o));
+        mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+    }
+    if ((t & 31) == 0) { wmax[warp] = mu; wmax[8 + warp] = mt; }
+    __syncthreads();
+    tc::fence_after_sync();
+    mu = wmax[0]; mt = wmax[8];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) { mu = fmaxf(mu, wmax[k]); mt = fmaxf(mt, wmax[8 + k]); }
+    auto scale_of = [](float m2) {
+        int e2 = ((int)((__float_as_uint(m2) >> 23) & 0xffu)) - 127;
+        e2 = max(e2, -47);
+        if (!(m2 < 3.0e38f)) e2 = 13;
+        return __uint_as_float((uint32_t)(127 + 13 - e2) << 23);
+    };
+    // |K t| <= sum|k| max|t| and |rho''/2| <= 1/2: s_p from 4 max|t| (unit-norm taps: sum|k| <= 7)
+    const float su = scale_of(2.0f * mu), st = scale_of(mt), sp = scale_of(4.0f * mt * cc.kabs);
+    const float inv = cc.inv_sf / su, inv_t = cc.inv_sf / st * sp;
+    const float inv_zt = cc.inv_z * (kThPScale / sp);            // Z units: s_b s_p
+    const uint32_t tb = tbase_s;
+    const uint32_t tl = tb + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t t_uh = tl + GH::COL_UH, t_ul = tl + GH::COL_UL, t_th = tl + GH::COL_TH, t_tl = tl + GH::COL_TL;
+    const int xg = l + C;
+    {   // the t ring's A2 slots stay zero (no DC shift of t): zero both rings' columns once
+        const uint32_t z4[4] = {0u, 0u, 0u, 0u};
+        for (int c = wg * 4; c < GH::RINGC; c += 8) {
+            tc::tmem_st4u(t_th + c, z4);
+            tc::tmem_st4u(t_tl + c, z4);
+        }
+    }
+    tc::wait_st();
+#pragma unroll 1
+    for (int y = 0; y < M - 1; ++y) {
+        if (wg == 0) {
+            th_build_row<M, G::UP, RS, 0>(us, y, l, xg, su, t_uh, t_ul, y % RS);
+            th_build_trow<M, G::UP, RS, 0>(ts, y, l, st, t_th, t_tl, y % RS);
+        } else {
+            th_build_row<M, G::UP, RS, 1>(us, y, l, xg, su, t_uh, t_ul, y % RS);
+            th_build_trow<M, G::UP, RS, 1>(ts, y, l, st, t_th, t_tl, y % RS);
+        }
+    }
+    tc::mbar_wait(&mbar_bimg, 0);
+    const uint32_t idf = tc::idesc_f16(128, NP);
+    const uint32_t idb = tc::idesc_f16(128, G::NBP);
+    const uint32_t b_base = tc::smem_u32(smb + G::SM_B);
+    const bool out_col = (l < G::OW) && (x0 + l < W);
+
+    constexpr int NZ8 = G::NB / 8, HZ8 = (NZ8 + 1) / 2;
+    constexpr int NF8 = NP / 8, HF8 = NF8 / 2;
+    constexpr int A0 = C + 1, A1 = M - A0;
+    float acc[A0 > A1 ? A0 : A1];
+#pragma unroll
+    for (int k = 0; k < (A0 > A1 ? A0 : A1); ++k) acc[k] = 0.f;
+    float* gout = args.g + (size_t)b * HW;
+
+#pragma unroll 1
+    for (int j = 0; j <= G::RR; ++j) {
+        float uq = 0.f;
+        const int ws = (j + RS - 1) % RS;
+        if (j < G::RR) {
+            const int yn = j + M - 1;
+            if (wg == 0) {
+                th_build_row<M, G::UP, RS, 0>(us, yn, l, xg, su, t_uh, t_ul, yn % RS);
+                th_build_a2<M, G::UP, 0>(us, j, xg, su, t_uh, t_ul, ws);
+                th_build_trow<M, G::UP, RS, 0>(ts, yn, l, st, t_th, t_tl, yn % RS);
+            } else {
+                th_build_row<M, G::UP, RS, 1>(us, yn, l, xg, su, t_uh, t_ul, yn % RS);
+                th_build_a2<M, G::UP, 1>(us, j, xg, su, t_uh, t_ul, ws);
+                th_build_trow<M, G::UP, RS, 1>(ts, yn, l, st, t_th, t_tl, yn % RS);
+            }
+            // the t ring's A2 slot (t row j-1's low copy) back to zero: t has no DC shift
+            tc::tmem_st2u(t_th + ws * 4 + wg * 2, 0u, 0u);
+            tc::tmem_st2u(t_tl + ws * 4 + wg * 2, 0u, 0u);
+            uq = us[(j + C) * G::UP + xg] + cst;
+        }
+        if (j > 0) {
+            tc::mbar_wait(&mbar_b, (uint32_t)((j - 1) & 1));
+            tc::fence_after_sync();
+            if (wg == 0) tc_z_to_smem<L, 0, HZ8>(tl + GH::COL_Z, zs, l);
+            else tc_z_to_smem<L, HZ8, NZ8>(tl + GH::COL_Z, zs, l);
+        }
+        tc::wait_st();
+        tc::fence_before_sync();
+        __syncthreads();
+        if (warp == 0 && j < G::RR) {
+            tc::fence_after_sync();
+#pragma unroll
+            for (int pass = 0; pass < 3; ++pass) {
+                const uint32_t boff = pass == 0 ? (uint32_t)G::BF_BYTES : 0u;
+#pragma unroll
+                for (int c = 0; c < G::NCH; ++c) {
+                    const uint64_t bd = tc::sdesc_kmajor(b_base + boff + c * 2 * NP * 16, NP * 16, 128);
+                    const uint32_t off = 4 * (ws + 2 * c);
+                    tc::mma_f16_ts_warp(tb + GH::COL_D, tb + (pass == 1 ? GH::COL_UL : GH::COL_UH) + off, bd, idf,
+                                        (pass | c) != 0);
+                    tc::mma_f16_ts_warp(tb + GH::COL_DT, tb + (pass == 1 ? GH::COL_TL : GH::COL_TH) + off, bd, idf,
+                                        (pass | c) != 0);
+                }
+            }
+            tc::mma_commit_warp(&mbar_f);
+        }
+        if (j > 0) {
+            const int jz = j - 1;
+            if (wg == 0) {
+#pragma unroll
+                for (int a = 0; a + 1 < A0; a += 2) {
+                    float2 sa = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb)
+                        sa = __fadd2_rn(sa, make_float2(zs[(a * M + bb) * L + l + bb], zs[((a + 1) * M + bb) * L + l + bb]));
+                    acc[a] += sa.x;
+                    acc[a + 1] += sa.y;
+                }
+                if constexpr (A0 % 2 == 1) {
+                    float sa = 0.f;
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) sa += zs[((A0 - 1) * M + bb) * L + l + bb];
+                    acc[A0 - 1] += sa;
+                }
+                const int o = jz - (A0 - 1);
+                if (o >= 0) hand[(o & 7) * L + l] = acc[A0 - 1];
+#pragma unroll
+                for (int k = A0 - 1; k > 0; --k) acc[k] = acc[k - 1];
+                acc[0] = 0.f;
+            } else {
+                const float* zl = zls + (jz & 1) * 2 * L;
+                constexpr int NPR = (A1 - 1) / 2;
+#pragma unroll
+                for (int q = 0; q < NPR; ++q) {
+                    const int a = A0 + 2 * q;
+                    float2 sa = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb)
+                        sa = __fadd2_rn(sa, make_float2(zs[(a * M + bb) * L + l + bb], zs[((a + 1) * M + bb) * L + l + bb]));
+                    acc[2 * q] += sa.x;
+                    acc[2 * q + 1] += sa.y;
+                }
+#pragma unroll
+                for (int k = 2 * NPR; k < A1; ++k) {
+                    const int a = A0 + k;
+                    float sa = 0.f;
+#pragma unroll
+                    for (int bb = 0; bb < M; ++bb) {
+                        const int tap = a * M + bb;
+                        sa += tap < G::NB ? zs[tap * L + l + bb] : zl[l + bb] + zl[L + l + bb];
+                    }
+                    acc[k] += sa;
+                }
+                const int o = jz - 2 * C;
+                if (o >= 0 && o < R && out_col && y0 + o < H) {
+                    const float s_tot = (acc[A1 - 1] + hand[(o & 7) * L + l]) * inv_zt;
+                    const size_t gi = (size_t)(y0 + o) * W + x0 + l;
+                    float val;
+                    if (udom) val = s_tot;
+                    else {
+                        const float u = us[(o + 2 * C) * G::UP + l + 2 * C] + cst;
+                        val = (float)(vv[gi] * (double)args.gw[(size_t)b * HW + gi] + (double)(u * s_tot));
+                    }
+                    gout[gi] = val;
+                }
+#pragma unroll
+                for (int k = A1 - 1; k > 0; --k) acc[k] = acc[k - 1];
+                acc[0] = 0.f;
+            }
+        }
+        if (j < G::RR) {
+            tc::mbar_wait(&mbar_f, (uint32_t)(j & 1));
+            tc::fence_after_sync();
+            float zl;
+            if (wg == 0)
+                th_hvp_epilogue<0, HF8>(tl + GH::COL_D, tl + GH::COL_DT, tl + GH::COL_PH, tl + GH::COL_PL, uq, inv,
+                                        inv_t, cc.sumk, cc.kbl, zl);
+            else
+                th_hvp_epilogue<HF8, NF8>(tl + GH::COL_D, tl + GH::COL_DT, tl + GH::COL_PH, tl + GH::COL_PL, uq, inv,
+                                          inv_t, cc.sumk, cc.kbl, zl);
+            zls[(j & 1) * 2 * L + wg * L + l] = zl;
+            tc::wait_st();
+            tc::fence_before_sync();
+            __syncthreads();
+            if (warp == 0) {
+                tc::fence_after_sync();
+#pragma unroll
+                for (int pass = 0; pass < 3; ++pass) {
+                    const uint32_t acol = pass == 1 ? GH::COL_PL : GH::COL_PH;
+                    const uint32_t boff = 2 * G::BF_BYTES + (pass == 0 ? (uint32_t)G::BB_BYTES : 0u);
+#pragma unroll
+                    for (int kc = 0; kc < G::NKB; ++kc) {
+                        const uint64_t bd = tc::sdesc_kmajor(b_base + boff + kc * 2 * G::NBP * 16, G::NBP * 16, 128);
+                        tc::mma_f16_ts_warp(tb + GH::COL_Z, tb + acol + kc * 8, bd, idb, (pass | kc) != 0);
+                    }
+                }
+                tc::mma_commit_warp(&mbar_b);
+            }
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<GH::TCOLS>(tb);
 }
 
 }  // namespace foe
