@@ -59,6 +59,9 @@ def parse_args():
     ap.add_argument("--filter-groups", type=int, default=0, help="K1 filter groups per tile (0: automatic)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-p2p", action="store_true", help="c5: ghost rows over ncclSend/Recv instead of K2 peer stores")
+    ap.add_argument("--protocol", choices=["none", "fig2"], default="none",
+                    help="fig2: the data-term protocol of the paper's Fig. 2 on synthetic data (GPU PSNR/SSIM of "
+                         "models (8), (6), (10), lambda per model from a grid; paper_1404_5344_b200/fig2.py)")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="c5: weak = a (1024 N) x 8192 scene, 1024 rows per GPU (SURVEY 8(d)); strong = the "
                          "fixed 8192^2 scene of BASELINE.json configs[4] cut into N slabs")
@@ -309,6 +312,15 @@ def main():
         cfg = S.config(args.config, iters=args.iters)
     if args.impl == "reference":
         return run_reference(args, cfg)
+    if args.protocol == "fig2":
+        from paper_1404_5344_b200 import fig2
+        res = fig2.run(iters=args.iters or 300)
+        emit({"protocol": "fig2", "image": res["image"], "noisy": {"psnr": res["noisy"][0], "ssim": res["noisy"][1]},
+              "models": {n: {"lambda": list(m["lam"]), "psnr": m["psnr"], "ssim": m["ssim"]}
+                         for n, m in res["models"].items()},
+              "note": "GPU runs, PSNR/SSIM by foe_psnr/foe_ssim; the fp64 oracle check of the chosen runs is "
+                      "tests/test_fig2_protocol.py"})
+        return 0
     if cfg.name == "c5":
         return run_slabs(args, cfg)
 
