@@ -38,8 +38,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "megapixel-iterations/s of iPiano (FoE grad+prox) and % of B200 FP32 peak"
 DTYPE_DETAIL = {1: "fp32 stencil (FFMA2), fp64 iterate/prox/reductions",
-                2: "fp32-accurate stencil on tensor cores (TF32 x3 hi/lo split, fp32 accumulate), "
-                   "fp64 iterate/prox/reductions"}
+                2: "fp32-accurate stencil on tensor cores (tcgen05 kind::f16: fp16 x3 hi/lo split with "
+                   "power-of-two scales, fp32 accumulate in TMEM), fp64 iterate/prox/reductions"}
 UNIT = "MP-it/s"
 
 
@@ -205,10 +205,11 @@ def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cf
 
     achieved = ALGORITHMIC flops (4 N_f m^2 per pixel per evaluation) / the
     kernel's event-timed duration.  K1 (FFMA2) is bound by the FP32 FMA pipes: peak = SMs x 128
-    lanes x 2 x sm_max_mhz.  K8 (tcgen05 TF32, 3 passes) runs on the tensor cores: peak = the
-    measured sustained bf16 GEMM rate x the nominal TF32/BF16 ratio (1.1/2.25) -- the kernel is
-    timed inside a long step; fp32_frac (against the FP32 FMA peak) is the BASELINE metric's
-    "% of B200 FP32 peak"."""
+    lanes x 2 x sm_max_mhz.  K8 (tcgen05 kind::f16, 3 passes for fp32 accuracy) runs on the tensor
+    cores: peak = the measured sustained bf16 GEMM rate (fp16 and bf16 share the dense rate) -- the
+    kernel is timed inside a long step; frac_fp32_emulated divides by peak / 3 (an fp32-accurate
+    product costs three fp16 products); fp32_frac (against the FP32 FMA peak) is the BASELINE
+    metric's "% of B200 FP32 peak"."""
     import torch
     peaks, peak_src = measured_peaks()
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
@@ -223,7 +224,7 @@ def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cf
     traffic, traffic_src = args.traffic_bytes, "--traffic-bytes" if args.traffic_bytes else None
     if traffic is None:   # DRAM bytes per launch from the committed ncu --set full capture of this kernel
         try:
-            with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+            with open(os.path.join(ROOT, "profiles", "r02_traffic.json")) as fh:
                 tr = json.load(fh)
             key = "persistent" if persistent else ("k8" if stencil == 2 else "k1")
             if key in tr and (cfg.name == tr[key].get("config")):
@@ -236,26 +237,28 @@ def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cf
               "k_share_of_step": (k_ms / sum(step_ms)) if step_ms else None}
     if stencil == 2:
         bf16 = float(peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1400.0)))
-        tf32_peak = bf16 * 1.1 / 2.25
         m, nf = cfg.m, cfg.n_filters
-        kt, np_ = ((m * m + 7) // 8) * 8, ((nf + 15) // 16) * 16
+        np_ = ((nf + 15) // 16) * 16
+        nb = ((m * m // 8) * 8 + 15) // 16 * 16
+        kf = ((m + 1) // 2) * 16                         # forward K: (m + 1) ring slots of 8 halves
         c = (m - 1) // 2
         ow = 128 - 2 * c
-        # executed tensor flops per output pixel: 3 passes x (fwd KT x NP + bwd NP x KT) x 2 per
-        # response pixel, x (64 + 2C) 128-lane response rows per 64 x OW output tile
-        exec_px = 3 * 2 * 2 * kt * np_ * (64 + 2 * c) * 128 / (64 * ow)
+        R = 64
+        # executed tensor flops per output pixel: 3 passes x 2 x (fwd Kf x NP + bwd NP x NB) per
+        # response pixel, x (R + 2C) 128-lane response rows per R x OW output tile
+        exec_px = 3 * 2 * (kf * np_ + np_ * nb) * (R + 2 * c) * 128 / (R * ow)
         alg_px = 4.0 * nf * m * m
         ex = alg_tflops * exec_px / alg_px if alg_tflops else None
-        if micro.get("tf32_tflops", -1) > 0:
-            common["tf32_peak_microbench"] = micro["tf32_tflops"]
-            common["tensor_executed_frac_of_microbench"] = (ex / micro["tf32_tflops"]) if ex else None
         if micro.get("fp32_tflops", -1) > 0:
             common["fp32_peak_microbench"] = micro["fp32_tflops"]
-        return dict(common, bound="tensor", peak=tf32_peak, frac=(alg_tflops / tf32_peak) if alg_tflops else None,
-                    kernel="k_prior_grad_tc (K8: tcgen05 TF32 x3, TMEM accumulators)",
-                    peak_source=f"derived: measured sustained bf16 {bf16:.1f} TFLOP/s x 1.1/2.25 (nominal TF32/BF16), "
-                                f"{peak_src} MEASURED_PEAKS.json",
-                    tensor_executed_tflops=ex, tensor_executed_frac=(ex / tf32_peak) if ex else None)
+        return dict(common, bound="tensor", peak=bf16, frac=(alg_tflops / bf16) if alg_tflops else None,
+                    kernel="k_prior_grad_th (K8: tcgen05 kind::f16 x3, A operands and accumulators in TMEM)",
+                    peak_source=f"measured: sustained bf16 GEMM {bf16:.1f} TFLOP/s ({peak_src} MEASURED_PEAKS.json; "
+                                f"fp16 dense = bf16 dense rate)",
+                    peak_fp32_emulated=bf16 / 3.0,
+                    frac_fp32_emulated=(3.0 * alg_tflops / bf16) if alg_tflops else None,
+                    tensor_executed_tflops=ex, tensor_executed_frac=(ex / bf16) if ex else None,
+                    executed_per_algorithmic=exec_px / alg_px)
     kname = ("k_ipiano_persistent (all trial rounds of a solve in one cooperative launch: K2 + K1 FFMA2 "
              "stencil + K3 per round; timed around ipiano_solve, so achieved covers the whole round)"
              if persistent else "k_prior_grad2 (K1: FFMA2 fused FoE energy+gradient stencil)")

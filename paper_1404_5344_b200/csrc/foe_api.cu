@@ -156,6 +156,25 @@ int tc_np(int m, int nf) {
 
 constexpr int kPxt2 = 8;  // pixels per thread of the pointwise kernels
 
+// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while its
+// predecessor on the stream drains; it calls pdl_wait() before touching the predecessor's output
+// (foe_kernels.cuh).  Used for the graph driver's trial rounds K2 -> K8 -> K3.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchConfig_t c = {};
+    c.gridDim = grid;
+    c.blockDim = block;
+    c.dynamicSmemBytes = smem;
+    c.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    c.attrs = at;
+    c.numAttrs = 1;
+    return cudaLaunchKernelEx(&c, kern, std::forward<Args>(args)...);
+}
+
 int div_up(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 }  // namespace
@@ -565,7 +584,8 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
 }
 
 // Launch the prior energy+gradient evaluation `a` (tiling fields taken from the plan).
-foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStream_t s, int ntiles_grid = -1) {
+foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStream_t s, int ntiles_grid = -1,
+                        bool pdl = false) {
     if (kind == FOE_STENCIL_FFMA) {
         k1_dispatch(md->m, false, a, *md->tp, *md->tp2, dim3(a.ntiles * a.groups, B), s);
         CKL("k_prior_grad2");
@@ -581,6 +601,14 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
     if (grid.x == 0) return FOE_OK;
     constexpr int T = 256;
     const int R = a.tc_rows;
+    if (pdl) {   // the batch path's 64-row tiles (graph trial rounds)
+        if (R == 64 && md->tc_np == 48)
+            CK(launch_pdl(foe::k_prior_grad_th<7, 48, 64>, grid, dim3(T), th_smem<7, 48, 64>(), s, ta, *md->th_const));
+        else if (R == 8 && md->tc_np == 48)
+            CK(launch_pdl(foe::k_prior_grad_th<7, 48, 8>, grid, dim3(T), th_smem<7, 48, 8>(), s, ta, *md->th_const));
+        else pdl = false;
+        if (pdl) return FOE_OK;
+    }
     if (md->tc_np == 48) {
         if (R == 8) foe::k_prior_grad_th<7, 48, 8><<<grid, T, th_smem<7, 48, 8>(), s>>>(ta, *md->th_const);
         else if (R == 16) foe::k_prior_grad_th<7, 48, 16><<<grid, T, th_smem<7, 48, 16>(), s>>>(ta, *md->th_const);
@@ -955,15 +983,16 @@ foe::K3Args state_k3_args(const ipiano_state* st) {
     return a3;
 }
 
-// One trial round for every active image: K2 -> K1 (candidate) -> K3.
+// One trial round for every active image: K2 -> K1 (candidate) -> K3, as programmatic dependent
+// launches (each kernel's launch and independent prologue overlap its predecessor's drain).
 foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
     {
         const foe::K2Args a2 = state_k2_args(st);
-        const dim3 g2(st->nblk2, st->B);
-        if (st->pxt2 == 1) foe::k_inertial_prox<1><<<g2, kThreads, 0, s>>>(a2);
-        else if (st->pxt2 == 4) foe::k_inertial_prox<4><<<g2, kThreads, 0, s>>>(a2);
-        else if (st->pxt2 == 16) foe::k_inertial_prox<16><<<g2, kThreads, 0, s>>>(a2);
-        else foe::k_inertial_prox<kPxt2><<<g2, kThreads, 0, s>>>(a2);
+        const dim3 g2(st->nblk2, st->B), tb(kThreads);
+        if (st->pxt2 == 1) CK(launch_pdl(foe::k_inertial_prox<1>, g2, tb, 0, s, a2));
+        else if (st->pxt2 == 4) CK(launch_pdl(foe::k_inertial_prox<4>, g2, tb, 0, s, a2));
+        else if (st->pxt2 == 16) CK(launch_pdl(foe::k_inertial_prox<16>, g2, tb, 0, s, a2));
+        else CK(launch_pdl(foe::k_inertial_prox<kPxt2>, g2, tb, 0, s, a2));
         count_launch(1);
         CKL("k_inertial_prox");
     }
@@ -974,7 +1003,7 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
         e1 = pool_event(st);
         CK(cudaEventRecord(e0, s));
     }
-    foe_status rl = launch_prior(st->model, st->kind, a1, st->B, s);
+    foe_status rl = launch_prior(st->model, st->kind, a1, st->B, s, -1, !timed);
     if (rl != FOE_OK) return rl;
     if (timed) {
         CK(cudaEventRecord(e1, s));
@@ -982,7 +1011,7 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
         st->k1_launches += 1;
     }
     const foe::K3Args a3 = state_k3_args(st);
-    foe::k_decide<<<st->B, kThreads, 0, s>>>(a3);
+    CK(launch_pdl(foe::k_decide, dim3(st->B), dim3(kThreads), 0, s, a3));
     count_launch(1);
     CKL("k_decide");
     st->total_launches += 3;

@@ -111,6 +111,13 @@ __device__ __forceinline__ float rcp_approx(float x) {
     return y;
 }
 
+// Programmatic dependent launch (graph trial rounds K2 -> K8 -> K3): a kernel launched with the
+// programmatic-serialization attribute may start while its predecessor drains; pdl_wait() blocks
+// until the predecessor grid has completed and its memory is visible (a no-op for a normal launch),
+// pdl_trigger() lets the successor be scheduled once every CTA has triggered or exited.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ int wrap_idx(int i, int n) {
     int r = i % n;
     return r < 0 ? r + n : r;
@@ -944,7 +951,9 @@ __device__ __forceinline__ void inertial_prox_blk(const K2Args& a, const int bx,
 template <int PXT>
 __global__ void __launch_bounds__(kThreads, FOE_K2_CTAS)
 k_inertial_prox(const K2Args a) {  // (4 CTAs/SM: <= 64 registers; 3 -> 4 gave 253 -> 222 us, 5 spills)
+    pdl_wait();   // programmatic launch after K3: its control blocks must be complete
     inertial_prox_blk<PXT>(a, blockIdx.x, blockIdx.y);
+    pdl_trigger();
 }
 
 // ---------------------------------------------------------------------------------
@@ -1025,7 +1034,11 @@ __device__ __forceinline__ void decide_img(const K3Args& a, const int b) {
     c.active = (c.status == ST_OK && !c.done && c.n < c.target) ? 1 : 0;
 }
 
-__global__ void __launch_bounds__(kThreads) k_decide(const K3Args a) { decide_img(a, blockIdx.x); }
+__global__ void __launch_bounds__(kThreads) k_decide(const K3Args a) {
+    pdl_wait();
+    decide_img(a, blockIdx.x);
+    pdl_trigger();
+}
 
 // ---------------------------------------------------------------------------------
 // Setup / helper kernels

@@ -197,10 +197,22 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
 
     const K1Args& args = ta.k;
     const int b = blockIdx.y;
+    const int t = threadIdx.x, warp = __shfl_sync(0xffffffffu, t >> 5, 0);
+    // independent of the predecessor (programmatic launch after K2): the B images' bulk copy
+    if (t == 0) {
+        tc::mbar_init(&mbar_bimg, 1);
+        tc::mbar_fence_init();
+        tc::bulk_g2s(smb + G::SM_B, ta.bimg, (uint32_t)G::B_BYTES, &mbar_bimg);
+    }
+    pdl_wait();
     int wslot = 0, gslot = 0;
     if (args.ctl != nullptr) {
         const ImgCtl& c = args.ctl[b];
-        if (!c.active) return;
+        if (!c.active) {   // nothing to do; the bulk copy must land before the CTA's smem goes
+            __syncthreads();
+            tc::mbar_wait(&mbar_bimg, 0);
+            return;
+        }
         wslot = args.which_cur ? c.cur : c.cand;
         gslot = args.which_cur ? c.gcur : c.gcand;
     }
@@ -208,7 +220,6 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
     const size_t HW = (size_t)H * W;
     const int tile = args.tile_off + blockIdx.x;
     const double* w = args.w + (size_t)wslot * args.w_slot_stride + (size_t)b * HW;
-    const int t = threadIdx.x, warp = __shfl_sync(0xffffffffu, t >> 5, 0);
     const int wg = warp >> 2;                                   // warp group (0, 1)
     const int l = (warp & 3) * 32 + (t & 31);                   // TMEM lane = response pixel
     // tile geometry: a full tile (band ty, columns x0 ..), or a packed tile whose lane strips (of
@@ -236,9 +247,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
     if (t == 0) {
         tc::mbar_init(&mbar_f, 1);
         tc::mbar_init(&mbar_b, 1);
-        tc::mbar_init(&mbar_bimg, 1);
         tc::mbar_fence_init();
-        tc::bulk_g2s(smb + G::SM_B, ta.bimg, (uint32_t)G::B_BYTES, &mbar_bimg);
     }
     const int yc = min(y0 + R / 2, H - 1), xc = min(x0 + (packed ? args.tc_rem : G::OW) / 2, W - 1);
     const bool udom = args.udom != 0;
@@ -434,6 +443,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
     // (a7) per-CTA energy partial (fixed order)
     const double e = block_sum_d(e_acc, red);
     if (t == 0) args.epart[(size_t)b * args.ntiles * args.groups + tile] = e;
+    pdl_trigger();
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc<G::TCOLS>(tb);
