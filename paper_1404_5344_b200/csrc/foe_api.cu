@@ -1305,6 +1305,12 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     // when the launch still has >= 4 blocks per SM; slab members keep kPxt2 (whole K2 blocks per
     // 64-row band for W % 32 == 0)
     if (!t_slab_member && (long long)B * H * W >= 4LL * md->nsm * kThreads * 16) st->pxt2 = 16;
+#ifndef FOE_K2_PXT_SMALL
+#define FOE_K2_PXT_SMALL 4
+#endif
+    // a launch of fewer than ~4 blocks per SM at 8 px/thread (one 512^2 image: 128 blocks) is
+    // fp64-latency bound: more, smaller blocks
+    if (!t_slab_member && (long long)B * H * W < 4LL * md->nsm * kThreads * kPxt2) st->pxt2 = FOE_K2_PXT_SMALL;
     if (t_slab_member && t_force_pxt > 0) st->pxt2 = t_force_pxt;
     if (want_persist && pl.kind == FOE_STENCIL_FFMA) {
         // K2 items: one pixel per thread while the grid can hold them all, else four
