@@ -1,25 +1,29 @@
 #!/bin/bash
-# Round-end evidence: smoke, full GPU tests, bench lines (c4 default, c5, c1-c3 persistent,
-# reference arm), the ncu launch list of the default bench command and full captures of the
-# dominant kernels (K8, K2) and of the persistent small-image kernel.
+# Round-end evidence: smoke, bench lines (c4 default, c5 weak + strong, c1-c3, reference arm, the
+# Fig. 2 protocol), the ncu launch list of the default bench command and full captures of the
+# dominant kernels (K8, K2, the HVP of the Lipschitz setup, the persistent small-image kernel).
 TAG=${1:-final}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 NCU=/usr/local/cuda/bin/ncu
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/rc.txt
-timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/rc.txt
 timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/rc.txt
-timeout 900 python bench.py --config c5 --steps 2 --warmup 3 > $OUT/bench_c5.json 2> $OUT/bench_c5.err; echo "bench c5 rc=$?" >> $OUT/rc.txt
+for sc in weak strong; do
+  timeout 900 python bench.py --config c5 --scaling $sc --steps 2 --warmup 3 > $OUT/bench_c5_$sc.json 2> $OUT/bench_c5_$sc.err; echo "bench c5 $sc rc=$?" >> $OUT/rc.txt
+done
 for c in c1 c2 c3; do
   timeout 300 python bench.py --config $c --steps 5 --warmup 3 > $OUT/bench_$c.json 2> $OUT/bench_$c.err; echo "bench $c rc=$?" >> $OUT/rc.txt
 done
 timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "bench ref rc=$?" >> $OUT/rc.txt
+timeout 300 python bench.py --protocol fig2 > $OUT/fig2.json 2> $OUT/fig2.err; echo "fig2 rc=$?" >> $OUT/rc.txt
 timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
   python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > $OUT/ncu_launch.log 2>&1; echo "ncu-launch rc=$?" >> $OUT/rc.txt
-timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_prior_grad_tc -s 5 -c 1 \
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_prior_grad_th -s 5 -c 1 \
   -o $OUT/k8 python bench.py --steps 1 --warmup 3 --iters 5 --no-e2e --no-cpu-baseline > $OUT/ncu_k8.log 2>&1; echo "ncu-k8 rc=$?" >> $OUT/rc.txt
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_inertial_prox -s 2 -c 1 \
   -o $OUT/k2 python bench.py --steps 1 --warmup 3 --iters 5 --no-e2e --no-cpu-baseline > $OUT/ncu_k2.log 2>&1; echo "ncu-k2 rc=$?" >> $OUT/rc.txt
+timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_hvp_th -s 3 -c 1 \
+  -o $OUT/hvp python bench.py --steps 1 --warmup 3 --iters 5 --no-e2e --no-cpu-baseline > $OUT/ncu_hvp.log 2>&1; echo "ncu-hvp rc=$?" >> $OUT/rc.txt
 timeout 900 $NCU --set full --clock-control none --import-source on -k regex:k_ipiano_persistent -c 1 \
   -o $OUT/kp python bench.py --config c2 --steps 1 --warmup 1 --iters 20 --no-e2e --no-cpu-baseline > $OUT/ncu_kp.log 2>&1; echo "ncu-persistent rc=$?" >> $OUT/rc.txt
 cat $OUT/rc.txt

@@ -29,6 +29,12 @@ KEYS = [
     "dram__throughput.avg.pct_of_peak_sustained_elapsed", "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
     "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic", "launch__grid_size",
     "launch__occupancy_limit_registers", "sm__maximum_warps_per_active_cycle_pct",
+    # tensor pipe (K8: tcgen05 kind::f16) -- the one pipe the tensor-core stencil is built on
+    "sm__ops_path_tensor_op_utchmma_src_fp16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active",
+    "smsp__pcsamp_warps_issue_stalled_barrier", "smsp__pcsamp_warps_issue_stalled_wait",
+    "smsp__pcsamp_warps_issue_stalled_math_pipe_throttle", "smsp__pcsamp_warps_issue_stalled_short_scoreboard",
 ]
 
 

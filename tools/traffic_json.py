@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Write profiles/r01_traffic.json from ncu --set full captures (run here on gpurun's files):
+"""Write profiles/r02_traffic.json from ncu --set full captures (run here on gpurun's files):
 dram__bytes_read.sum + dram__bytes_write.sum per launch of the captured kernel, which bench.py
 reports as roofline.traffic for the matching config.
 
@@ -28,7 +28,7 @@ def dram_bytes(rep):
 
 def main():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    path = os.path.join(root, "profiles", "r01_traffic.json")
+    path = os.path.join(root, "profiles", "r02_traffic.json")
     data = json.load(open(path)) if os.path.exists(path) else {}
     for arg in sys.argv[1:]:
         key, rest = arg.split("=", 1)
