@@ -252,7 +252,7 @@ namespace {
 // hi = fp16(v), lo = fp16(v - hi) (from the fp64 value); s_f, s_b = 2^(13 - e) with 2^e <= max|v|.
 foe_status build_th_images(foe_model* md) {
     const int m = md->m, nf = md->nf, NP = md->tc_np, TAPS = m * m;
-    const int NCH = (m + 1) / 2, NB = (TAPS / 8) * 8, NBP = ((NB + 15) / 16) * 16, NKB = NP / 16;
+    const int NCH = (m + 1) / 2, NB = foe::th_nb(m), NBP = ((NB + 15) / 16) * 16, NKB = NP / 16;
     const size_t BF = (size_t)NCH * 16 * NP, BB = (size_t)NKB * 16 * NBP;   // halves per image
     std::vector<double> kf((size_t)NCH * 16 * NP, 0.0), kb((size_t)NP * NBP, 0.0);
     for (int i = 0; i < nf; ++i) {

@@ -39,7 +39,21 @@
 
 namespace foe {
 
-constexpr float kThPScale = 16384.0f;   // P = rho'/2 in [-1/2, 1/2] is stored x 2^14 (fp16 range)
+// 1: all m^2 taps of the backward GEMM on the tensor core (N = 64 for m = 7: the 49th tap no longer
+// needs a CUDA-core dot product and a partial-sum hand-off); 0: 48 taps + the last on CUDA cores.
+// Measured on c4 (tools/gpu_ablib.sh): 1 with FOE_K8_PSCALE 0 0.961 ms vs 0.9645 ms, but the K8 vs
+// oracle gradient error rises 3.4e-6 -> 3.7e-6 (the unscaled P); 1 with the scale 0.972 ms
+#ifndef FOE_K8_TAP49
+#define FOE_K8_TAP49 0
+#endif
+// K8's P = rho'/2 in [-1/2, 1/2] is stored x 2^14 (FOE_K8_PSCALE 0: unscaled -- fp16 lo parts below
+// 2^-14 are subnormal, an absolute error <= 2^-25 in P)
+#ifndef FOE_K8_PSCALE
+#define FOE_K8_PSCALE 1
+#endif
+constexpr float kThPScale = FOE_K8_PSCALE ? 16384.0f : 1.0f;
+// taps of the backward GEMM on the tensor core (host and device)
+__host__ __device__ constexpr int th_nb(int m) { return FOE_K8_TAP49 ? m * m : (m * m / 8) * 8; }
 
 template <int M, int NP, int R>
 struct ThGeom {
@@ -53,7 +67,7 @@ struct ThGeom {
     static constexpr int UP = UX + 2;                   // u pitch (floats)
     static constexpr int NCH = (M + 1) / 2;             // forward K = 16 chunks (two ring slots each)
     static constexpr int RS = M + 1;                    // ring slots per copy (A2 + m rows)
-    static constexpr int NB = (TAPS / 8) * 8;           // backward taps on the tensor core
+    static constexpr int NB = th_nb(M);                 // backward taps on the tensor core
     static constexpr int NBP = ((NB + 15) / 16) * 16;   // ... padded to the MMA's N granularity
     static constexpr int NKB = NP / 16;                 // backward K = 16 chunks (filters)
     // TMEM columns: ring hi / lo (2 RS slots x 4 columns each), D (= Z), P hi / lo (fp16 pairs)
@@ -72,11 +86,12 @@ struct ThGeom {
     static constexpr int SM_B = 0;
     static constexpr int SM_U = SM_B + B_BYTES;
     static constexpr int SM_Z = SM_U + UY * UP * 4;
-    static constexpr int SM_HAND = SM_Z + NB * LANES * 4;
+    static constexpr int NZ8 = (NB + 7) / 8;            // Z read-out chunks of 8 taps
+    static constexpr int SM_HAND = SM_Z + NZ8 * 8 * LANES * 4;
     static constexpr int SM_ZL = SM_HAND + 8 * LANES * 4;
     static constexpr int SMEM_BYTES = SM_ZL + 4 * LANES * 4 + 64;
     static_assert(NP % 16 == 0 && NBP <= ND, "MMA shapes");
-    static_assert(TAPS - NB == 1, "one CUDA-core tap");
+    static_assert(TAPS - NB <= 1, "at most one CUDA-core tap");
     static_assert(TCOLS_USED <= 256, "TMEM budget: two CTAs per SM");
     static_assert(B_BYTES % 16 == 0 && SM_U % 16 == 0, "B images: one TMA bulk copy");
 };
@@ -170,7 +185,7 @@ __device__ __forceinline__ float th_epilogue(uint32_t t_d, uint32_t t_ph, uint32
             // one MUFU reciprocal per filter pair: 1/d_A = d_B / (d_A d_B) (d >= 1; see K1)
             const float q = rcp_approx(d.x * d.y) * kThPScale;
             const float2 pv = __fmul2_rn(rv, __fmul2_rn(make_float2(d.y, d.x), make_float2(q, q)));
-            zl2 = __ffma2_rn(pv, make_float2(kbl[i], kbl[i + 1]), zl2);
+            if (!FOE_K8_TAP49) zl2 = __ffma2_rn(pv, make_float2(kbl[i], kbl[i + 1]), zl2);
             h2_split(pv, ph[e / 2], pl[e / 2]);
         }
         tc::tmem_st4u(t_ph + f8 * 4, ph);
@@ -297,7 +312,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
     const bool out_col = svalid && (ocol < ow) && (x0 + ocol < W);
 
     double e_acc = 0.0;
-    constexpr int NZ8 = G::NB / 8, HZ8 = (NZ8 + 1) / 2;    // Z tap chunks: wg0 [0,HZ8), wg1 [HZ8,NZ8)
+    constexpr int NZ8 = G::NZ8, HZ8 = (NZ8 + 1) / 2;       // Z tap chunks: wg0 [0,HZ8), wg1 [HZ8,NZ8)
     constexpr int NF8 = NP / 8, HF8 = NF8 / 2;             // filter chunks: wg0 [0,HF8), wg1 [HF8,NF8)
     constexpr int A0 = C + 1, A1 = M - A0;                 // col2im rows: wg0 a < A0, wg1 a >= A0
     float acc[A0 > A1 ? A0 : A1];
@@ -419,7 +434,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
             const float el = wg == 0
                 ? th_epilogue<0, HF8>(tl + G::COL_D, tl + G::COL_PH, tl + G::COL_PL, uq, inv, cc.sumk, cc.thl, cc.kbl, zl)
                 : th_epilogue<HF8, NF8>(tl + G::COL_D, tl + G::COL_PH, tl + G::COL_PL, uq, inv, cc.sumk, cc.thl, cc.kbl, zl);
-            zls[(j & 1) * 2 * L + wg * L + l] = zl;
+            if (!FOE_K8_TAP49) zls[(j & 1) * 2 * L + wg * L + l] = zl;
             if (own) e_acc += (double)el;
             tc::wait_st();
             tc::fence_before_sync();
@@ -544,7 +559,7 @@ __device__ __forceinline__ void th_hvp_epilogue(uint32_t t_d, uint32_t t_dt, uin
             const float q = rcp_approx(d.x * d.y);
             const float2 id = __fmul2_rn(make_float2(d.y, d.x), make_float2(q, q));   // 1 / d
             const float2 pv = __fmul2_rn(__fmul2_rn(omr, t2), __fmul2_rn(id, id));
-            zl2 = __ffma2_rn(pv, make_float2(kbl[i], kbl[i + 1]), zl2);
+            if (!FOE_K8_TAP49) zl2 = __ffma2_rn(pv, make_float2(kbl[i], kbl[i + 1]), zl2);
             h2_split(pv, ph[e / 2], pl[e / 2]);
         }
         tc::tmem_st4u(t_ph + f8 * 4, ph);
@@ -653,7 +668,7 @@ __global__ void __launch_bounds__(256, 1) k_hvp_th(const TcArgs ta, const __grid
     const uint32_t b_base = tc::smem_u32(smb + G::SM_B);
     const bool out_col = (l < G::OW) && (x0 + l < W);
 
-    constexpr int NZ8 = G::NB / 8, HZ8 = (NZ8 + 1) / 2;
+    constexpr int NZ8 = G::NZ8, HZ8 = (NZ8 + 1) / 2;
     constexpr int NF8 = NP / 8, HF8 = NF8 / 2;
     constexpr int A0 = C + 1, A1 = M - A0;
     float acc[A0 > A1 ? A0 : A1];
@@ -781,7 +796,7 @@ __global__ void __launch_bounds__(256, 1) k_hvp_th(const TcArgs ta, const __grid
             else
                 th_hvp_epilogue<HF8, NF8>(tl + GH::COL_D, tl + GH::COL_DT, tl + GH::COL_PH, tl + GH::COL_PL, uq, inv,
                                           inv_t, cc.sumk, cc.kbl, zl);
-            zls[(j & 1) * 2 * L + wg * L + l] = zl;
+            if (!FOE_K8_TAP49) zls[(j & 1) * 2 * L + wg * L + l] = zl;
             tc::wait_st();
             tc::fence_before_sync();
             __syncthreads();
