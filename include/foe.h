@@ -175,8 +175,9 @@ typedef struct {
  *                          only (FOE_ERR_UNSUPPORTED with FOE_STENCIL_TENSOR); for images that
  *                          cannot fill the GPU, where launches and their gaps dominate a round.
  *   FOE_SOLVER_AUTO        persistent when the state resolves to the FFMA stencil and
- *                          B*H*W < 2^18 (configs c1, c2), else the graph (c3: the tensor-core
- *                          stencil in 8-row tiles).
+ *                          B*H*W < 2^16 (config c1; < 2^18 for banks without a tensor-core
+ *                          stencil), else the graph (c2, c3: the tensor-core stencil in 4- and
+ *                          8-row tiles).
  * ipiano_profile(st, 1) (per-launch K1 timing) always uses the graph driver. */
 #define FOE_SOLVER_AUTO 0
 #define FOE_SOLVER_GRAPH 1

@@ -144,8 +144,11 @@ cudaError_t tc_set_attr() {
     e = cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              th_smem<M, NP, 16>());
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                th_smem<M, NP, 8>());
+    e = cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             th_smem<M, NP, 8>());
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                th_smem<M, NP, 4>());
 }
 // the banks K8 has an instantiation for: (m, padded N_f)
 int tc_np(int m, int nf) {
@@ -545,7 +548,7 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
     int bestR = kTcR;
     if (pack_ok) {
         double best = 1e30;
-        for (int R : {64, 32, 16, 8}) {
+        for (int R : {64, 32, 16, 8, 4}) {
             Plan q;
             tiling(R, q);
             const double waves = std::ceil((double)q.ntiles * B / (2.0 * md->nsm));
@@ -606,16 +609,20 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
             CK(launch_pdl(foe::k_prior_grad_th<7, 48, 64>, grid, dim3(T), th_smem<7, 48, 64>(), s, ta, *md->th_const));
         else if (R == 8 && md->tc_np == 48)
             CK(launch_pdl(foe::k_prior_grad_th<7, 48, 8>, grid, dim3(T), th_smem<7, 48, 8>(), s, ta, *md->th_const));
+        else if (R == 4 && md->tc_np == 48)
+            CK(launch_pdl(foe::k_prior_grad_th<7, 48, 4>, grid, dim3(T), th_smem<7, 48, 4>(), s, ta, *md->th_const));
         else pdl = false;
         if (pdl) return FOE_OK;
     }
     if (md->tc_np == 48) {
-        if (R == 8) foe::k_prior_grad_th<7, 48, 8><<<grid, T, th_smem<7, 48, 8>(), s>>>(ta, *md->th_const);
+        if (R == 4) foe::k_prior_grad_th<7, 48, 4><<<grid, T, th_smem<7, 48, 4>(), s>>>(ta, *md->th_const);
+        else if (R == 8) foe::k_prior_grad_th<7, 48, 8><<<grid, T, th_smem<7, 48, 8>(), s>>>(ta, *md->th_const);
         else if (R == 16) foe::k_prior_grad_th<7, 48, 16><<<grid, T, th_smem<7, 48, 16>(), s>>>(ta, *md->th_const);
         else if (R == 32) foe::k_prior_grad_th<7, 48, 32><<<grid, T, th_smem<7, 48, 32>(), s>>>(ta, *md->th_const);
         else foe::k_prior_grad_th<7, 48, 64><<<grid, T, th_smem<7, 48, 64>(), s>>>(ta, *md->th_const);
     } else {
-        if (R == 8) foe::k_prior_grad_th<5, 32, 8><<<grid, T, th_smem<5, 32, 8>(), s>>>(ta, *md->th_const);
+        if (R == 4) foe::k_prior_grad_th<5, 32, 4><<<grid, T, th_smem<5, 32, 4>(), s>>>(ta, *md->th_const);
+        else if (R == 8) foe::k_prior_grad_th<5, 32, 8><<<grid, T, th_smem<5, 32, 8>(), s>>>(ta, *md->th_const);
         else if (R == 16) foe::k_prior_grad_th<5, 32, 16><<<grid, T, th_smem<5, 32, 16>(), s>>>(ta, *md->th_const);
         else if (R == 32) foe::k_prior_grad_th<5, 32, 32><<<grid, T, th_smem<5, 32, 32>(), s>>>(ta, *md->th_const);
         else foe::k_prior_grad_th<5, 32, 64><<<grid, T, th_smem<5, 32, 64>(), s>>>(ta, *md->th_const);
@@ -1288,7 +1295,8 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     // trial-loop driver (f4): persistent for problems that cannot fill the GPU
     const long long npx = (long long)B * H * W;
     const bool want_persist = cfg.solver == FOE_SOLVER_PERSISTENT ||
-                              (cfg.solver == FOE_SOLVER_AUTO && cfg.stencil != FOE_STENCIL_TENSOR && npx < (1LL << 18));
+                              (cfg.solver == FOE_SOLVER_AUTO && cfg.stencil != FOE_STENCIL_TENSOR &&
+                               (npx < (1LL << 16) || (md->tc_np == 0 && npx <= (1LL << 18))));
     const int pref = want_persist ? FOE_STENCIL_FFMA : cfg.stencil;
     const Plan pl = plan_stencil(md, B, H, W, H, pref, cfg.filter_groups, !t_slab_member);
     st->kind = pl.kind;

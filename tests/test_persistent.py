@@ -77,11 +77,11 @@ def test_persistent_matches_graph(name, iters):
     b = _run(md, d, L0, iters, P.FOE_SOLVER_PERSISTENT)
     assert a[0] == P.FOE_SOLVER_GRAPH and b[0] == P.FOE_SOLVER_PERSISTENT
     _same_trajectory(a, b)
-    # AUTO resolves to the persistent FFMA driver for images below 2^18 pixels (c1, c2), and to
-    # the graph driver with the tensor-core stencil in small tiles from there (c3: 512^2)
+    # AUTO resolves to the persistent FFMA driver for images below 2^16 pixels (c1), and to the
+    # graph driver with the tensor-core stencil in short tiles from there (c2: 4-row, c3: 8-row)
     c = P.ipiano_config_default(max_iters=1)
     st = P.ipiano_state_create(md, _cuda(d["f"], torch.float32), d["lambdas"], L0, c)
-    if name == "c3":
+    if name in ("c2", "c3"):
         assert P.ipiano_state_solver(st) == P.FOE_SOLVER_GRAPH
         assert P.ipiano_state_stencil(st) == P.FOE_STENCIL_TENSOR
     else:
