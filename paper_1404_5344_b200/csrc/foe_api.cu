@@ -974,6 +974,7 @@ foe::K2Args state_k2_args(const ipiano_state* st) {
     a2.nblk = st->nblk2;
     a2.HW = st->HW;
     a2.idiv = st->model->term == FOE_DATA_IDIV;
+    a2.pairs = FOE_K2_PAIRS && st->HW % 4 == 0;
     return a2;
 }
 
@@ -1747,6 +1748,7 @@ foe_status slab_k2(ipiano_slabs* g, int j) {
     a2.halo_sys_fence = g->p2p && g->comm && g->comm->nranks > 1;
     a2.halo_px = (size_t)foe::kHalo * g->W;
     a2.idiv = st->model->term == FOE_DATA_IDIV;
+    a2.pairs = FOE_K2_PAIRS && st->HW % 4 == 0;
     if (st->pxt2 == 16) foe::k_inertial_prox<16><<<dim3(st->nblk2, 1), kThreads, 0, g->s>>>(a2);
     else foe::k_inertial_prox<kPxt2><<<dim3(st->nblk2, 1), kThreads, 0, g->s>>>(a2);
     count_launch(1);

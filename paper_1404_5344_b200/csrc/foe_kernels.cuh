@@ -29,8 +29,14 @@ constexpr int kThreads = 256;
 #ifndef FOE_K2_UNROLL
 #define FOE_K2_UNROLL 2   // K2 pixels in flight per thread
 #endif
+#ifndef FOE_K2_ETAB
+#define FOE_K2_ETAB 1     // K2 fast path: table-driven fp64 exponential (k2_etab in shared memory)
+#endif
+#ifndef FOE_K2_PAIRS
+#define FOE_K2_PAIRS 1    // K2 by pixel pairs (inertial_prox_pairs) when HW % 4 == 0
+#endif
 #ifndef FOE_K2_CTAS
-#define FOE_K2_CTAS 4     // K2 CTAs per SM (64 registers)
+#define FOE_K2_CTAS 3     // K2 CTAs per SM (80 registers; pairs: 223 us at 4 CTAs (spills) vs 163 at 3)
 #endif
 constexpr int kK2Unroll = FOE_K2_UNROLL;
 constexpr int kTile = 64;  // output tile side of K1
@@ -718,6 +724,31 @@ __device__ __forceinline__ void exp2a_pm(double a, double& ep, double& em) {
     em = (c - sh) * __hiloint2double((1023 - ni) << 20, 0);
 }
 
+// Table-driven e^{2a} and e^{-2a} for the prox's fast path (|2a| <= 700): 2a = (64 m + j) ln2/64 + r,
+// |r| <= ln2/128; e^{+-2a} = 2^{+-m} 2^{+-j/64} e^{+-r}, the cosh/sinh parts of r to r^6 / r^5
+// (remainder < 4e-17 relative).  tab = k2_etab(): [0, 64) = 2^{j/64}, [64, 128) = 2^{-j/64}, in
+// shared memory (filled by k2_etab_init); 2 table reads instead of ten more fp64 FMAs.
+__device__ __forceinline__ double* k2_etab() {
+    __shared__ double t[128];
+    return t;
+}
+__device__ __forceinline__ void k2_etab_init() {
+    double* t = k2_etab();
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) t[i] = exp2((i < 64 ? i : 64 - i) * (1.0 / 64.0));
+}
+__device__ __forceinline__ void exp2a_pm_tab(double a, double& ep, double& em) {
+    const double x = 2.0 * a;
+    const double kd = rint(x * 92.33248261689366);                                 // x 64 / ln 2
+    const double r = fma(-kd, 3.623510646634843e-19, fma(-kd, 1.0830424696249145e-02, x));   // x - kd ln2/64
+    const int k = (int)kd, j = k & 63, m = k >> 6;
+    const double r2 = r * r;
+    const double c = fma(r2, fma(r2, fma(r2, 1.0 / 720.0, 1.0 / 24.0), 0.5), 1.0);
+    const double s = r * fma(r2, fma(r2, 1.0 / 120.0, 1.0 / 6.0), 1.0);
+    const double* t = k2_etab();
+    ep = (c + s) * (t[j] * __hiloint2double((m + 1023) << 20, 0));
+    em = (c - s) * (t[64 + j] * __hiloint2double((1023 - m) << 20, 0));
+}
+
 // 1/b to full fp64 precision: MUFU reciprocal seed + two Newton steps (b finite, nonzero)
 __device__ __forceinline__ double rcp_f64(double b) {
     double y;
@@ -748,7 +779,12 @@ __device__ __forceinline__ float ex2_approx(float x) {
 // (large steps, overflow) the safeguarded fp64 Newton/bisection iteration on the bracket
 // [min(0, log f - what) - 1, max(0, log f - what) + 1] runs to |phi| <= tol
 // (SPEC.md:251).  Returns the Newton updates, or -1 past the cap; em_out = e^{-2z}, ep_out = e^{2z}.
-__device__ __forceinline__ int prox_newton(double what, double ft, double tau, double l1,
+// fp32 copies of the per-image prox constants tau l1, tau l2 (hoisted out of the pixel loop: an
+// fp64 <-> fp32 conversion is a slow instruction on sm_100, and K2 was stalled on them)
+struct ProxF {
+    float tl1, tl2;
+};
+__device__ __forceinline__ int prox_newton(double what, double ft, float ff, const ProxF& pf, double tau, double l1,
                                            double l2, double tol, int cap, double& z_out,
                                            double& em_out, double& ep_out) {
     const double f2 = ft * ft;
@@ -756,7 +792,7 @@ __device__ __forceinline__ int prox_newton(double what, double ft, double tau, d
     // Newton step from there -- quadratic convergence takes the fp32 error to ~1e-14, accepted by
     // the same error bound as below; one fp64 exponential pair (at z0 = what + d32) instead of two
     if (fabs(what) <= 40.0) {
-        const float tl1f2 = (float)(tau * l1 * f2), tl2 = (float)(tau * l2), c0f = (float)(tau * (l1 - l2 * f2));
+        const float f2f = ff * ff, tl1f2 = pf.tl1 * f2f, tl2 = pf.tl2, c0f = fmaf(-pf.tl2, f2f, pf.tl1);
         const float wf = (float)what;
         const float Af = tl1f2 * ex2_approx(-2.8853900817779268f * wf), Bf = tl2 * ex2_approx(2.8853900817779268f * wf);
         float d = -(c0f - Af + Bf) * rcp_approx(1.0f + 2.0f * (Af + Bf));
@@ -768,7 +804,11 @@ __device__ __forceinline__ int prox_newton(double what, double ft, double tau, d
         }
         const double z0 = what + (double)d;
         double Ep0, Em0;
-        exp2a_pm(z0, Ep0, Em0);                    // e^{2 z0}, e^{-2 z0}
+#if FOE_K2_ETAB
+        exp2a_pm_tab(z0, Ep0, Em0);                // e^{2 z0}, e^{-2 z0}
+#else
+        exp2a_pm(z0, Ep0, Em0);
+#endif
         const double am = tau * l1 * f2 * Em0, bp = tau * l2 * Ep0;
         const double phi = (double)d + tau * (l1 - l2 * f2) - am + bp;
         const double dphi = 1.0 + 2.0 * (am + bp);
@@ -846,6 +886,7 @@ struct K2Args {
     double* halo_up;
     double* halo_dn;
     int halo_sys_fence;    // peer-GPU destination: make the stores visible system-wide
+    int pairs;             // HW % 4 == 0: pixel pairs by 16-/8-byte vector loads (inertial_prox_pairs)
     size_t halo_px;        // kHalo * W
     int idiv;              // model (6) in u: closed-form prox of (lam/2)(u^2 - 2 f^2 log u), lam = lam1
 };
@@ -853,15 +894,16 @@ struct K2Args {
 // Test partials of one trial (a10): <g, D>, ||D||^2, G(w+), ||w||^2, max |w+| (or the domain
 // flag of model (6)), max Newton iterations, prox failures.
 struct K2Acc {
-    double gd = 0, dd = 0, Gp = 0, ww = 0, wmax = 0, nit = 0, fail = 0;
+    double gd = 0, dd = 0, Gp = 0, ww = 0, wmax = 0;
+    int nit = 0, fail = 0;
 };
 
 // One pixel of K2 (a8-a10): inertial point, prox, and its contribution to the test partials.
-// Shared by k_inertial_prox and the fused K8 trial kernel; the inertial point is written with
-// explicit roundings so that both compile to the same arithmetic (bitwise-equal w+).
-__device__ __forceinline__ double k2_pixel(double wv, double wpv, double gv, double f, double alpha, double beta,
-                                           double l1, double l2, const SolverParams& sp, int idiv, K2Acc& acc,
-                                           bool own = true) {
+// Shared by k_inertial_prox and the persistent driver's phase A; the inertial point is written
+// with explicit roundings so that both compile to the same arithmetic (bitwise-equal w+).
+__device__ __forceinline__ double k2_pixel(double wv, double wpv, double gv, double f, float ff, double alpha,
+                                           double beta, double l1, double l2, const ProxF& pf,
+                                           const SolverParams& sp, int idiv, K2Acc& acc) {
     const double what = __fma_rn(beta, __dsub_rn(wv, wpv), __fma_rn(-alpha, gv, wv));
     double z, em, ep;
     int it;
@@ -871,9 +913,8 @@ __device__ __forceinline__ double k2_pixel(double wv, double wpv, double gv, dou
         z = (what + sqrt(fma(what, what, 4.0 * (1.0 + tl) * tl * f * f))) / (2.0 * (1.0 + tl));
         em = 0.0; ep = 0.0; it = 0;
     } else {
-        it = prox_newton(what, f, alpha, l1, l2, sp.newton_tol, sp.newton_cap, z, em, ep);
+        it = prox_newton(what, f, ff, pf, alpha, l1, l2, sp.newton_tol, sp.newton_cap, z, em, ep);
     }
-    if (!own) return z;   // a fused K8 tile's halo pixel: its owning tile counts it
     const double d = z - wv;
     acc.gd += gv * d;
     acc.dd += d * d;
@@ -886,7 +927,7 @@ __device__ __forceinline__ double k2_pixel(double wv, double wpv, double gv, dou
         acc.wmax = fmax(acc.wmax, fabs(z));
     }
     acc.ww += wv * wv;
-    if (it < 0) acc.fail += 1.0; else acc.nit = fmax(acc.nit, (double)it);
+    if (it < 0) ++acc.fail; else acc.nit = max(acc.nit, it);
     if (!(z == z)) acc.wmax = INFINITY;
     return z;
 }
@@ -894,7 +935,7 @@ __device__ __forceinline__ double k2_pixel(double wv, double wpv, double gv, dou
 // fixed-order CTA reduction of the 7 test partials (sums; slots 4 and 5 max) -> out[0..7]
 // (out[7] = 0); every thread of the CTA calls it
 __device__ __forceinline__ void k2_block_partials(const K2Acc& acc, double* out) {
-    double v[7] = {acc.gd, acc.dd, acc.Gp, acc.ww, acc.wmax, acc.nit, acc.fail};
+    double v[7] = {acc.gd, acc.dd, acc.Gp, acc.ww, acc.wmax, (double)acc.nit, (double)acc.fail};
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
@@ -924,6 +965,7 @@ __device__ __forceinline__ void inertial_prox_blk(const K2Args& a, const int bx,
     if (!c.active) return;
     const double alpha = a.sp.safety * 2.0 * (1.0 - a.sp.beta) / c.L;
     const double beta = a.sp.beta, l1 = c.lam1, l2 = c.lam2;
+    const ProxF pf{(float)(alpha * l1), (float)(alpha * l2)};
     const double* w = a.w + (size_t)c.cur * a.w_slot_stride + (size_t)b * a.HW;
     const double* wp = a.w + (size_t)c.prev * a.w_slot_stride + (size_t)b * a.HW;
     double* wn = a.w + (size_t)c.cand * a.w_slot_stride + (size_t)b * a.HW;
@@ -937,7 +979,8 @@ __device__ __forceinline__ void inertial_prox_blk(const K2Args& a, const int bx,
         if (p >= a.HW) break;
         float gs = g[p];
         for (int q = 1; q < a.groups; ++q) gs += g[(size_t)q * a.g_group_stride + p];
-        const double z = k2_pixel(w[p], wp[p], (double)gs, (double)ft[p], alpha, beta, l1, l2, a.sp, a.idiv, acc);
+        const float fv = ft[p];
+        const double z = k2_pixel(w[p], wp[p], (double)gs, (double)fv, fv, alpha, beta, l1, l2, pf, a.sp, a.idiv, acc);
         wn[p] = z;
         if (a.halo_up != nullptr) {
             if (p < a.halo_px) a.halo_up[p] = z;
@@ -948,11 +991,111 @@ __device__ __forceinline__ void inertial_prox_blk(const K2Args& a, const int bx,
     k2_block_partials(acc, a.ppart + ((size_t)b * a.nblk + bx) * kNumPart);
 }
 
+// Pixel block bx of image b by pixel PAIRS (HW % 4 == 0, so every pair is 16-/8-byte aligned): one
+// vector load per array per pair, 32-bit pair indices, the next pair's loads issued before the
+// current pair's arithmetic; the per-image constants come from shared memory (im).  Same per-pixel
+// arithmetic as inertial_prox_blk (k2_pixel), so w+ is bitwise the same.
+struct K2Img {
+    double alpha, beta, l1, l2;
+    ProxF pf;
+};
+template <int PXT>
+__device__ __forceinline__ void inertial_prox_pairs(const K2Args& a, const K2Img& im, const int bx, const int b) {
+    const ImgCtl& c = a.ctl[b];
+    const size_t base = (size_t)bx * (kThreads * PXT), o = (size_t)b * a.HW + base;
+    const double2* w2 = reinterpret_cast<const double2*>(a.w + (size_t)c.cur * a.w_slot_stride + o);
+    const double2* wp2 = reinterpret_cast<const double2*>(a.w + (size_t)c.prev * a.w_slot_stride + o);
+    double2* wn2 = reinterpret_cast<double2*>(a.w + (size_t)c.cand * a.w_slot_stride + o);
+    const float2* g2 = reinterpret_cast<const float2*>(a.g + (size_t)c.gcur * a.g_slot_stride + o);
+    const float2* f2p = reinterpret_cast<const float2*>(a.ft + o);
+    const int n2 = (int)(min((size_t)(kThreads * PXT), a.HW - base) >> 1);
+    const int gq = (int)(a.g_group_stride >> 1);
+    K2Acc acc;
+    int q = threadIdx.x;
+    if (q < n2) {
+        double2 wv = w2[q], wpv = wp2[q];
+        float2 gs = g2[q], fv = f2p[q];
+        for (int k = 1; k < a.groups; ++k) { const float2 t = g2[k * gq + q]; gs.x += t.x; gs.y += t.y; }
+#pragma unroll 1
+        for (int k = 0; k < PXT / 2; ++k) {
+            const int qn = q + kThreads;
+            const bool more = k + 1 < PXT / 2 && qn < n2;
+            double2 wv1 = make_double2(0.0, 0.0), wpv1 = wv1;
+            float2 gs1 = make_float2(0.f, 0.f), fv1 = make_float2(1.f, 1.f);
+            if (more) {
+                wv1 = w2[qn]; wpv1 = wp2[qn]; gs1 = g2[qn]; fv1 = f2p[qn];
+                for (int kk = 1; kk < a.groups; ++kk) { const float2 t = g2[kk * gq + qn]; gs1.x += t.x; gs1.y += t.y; }
+            }
+            double2 z;
+            z.x = k2_pixel(wv.x, wpv.x, (double)gs.x, (double)fv.x, fv.x, im.alpha, im.beta, im.l1, im.l2, im.pf, a.sp, a.idiv, acc);
+            z.y = k2_pixel(wv.y, wpv.y, (double)gs.y, (double)fv.y, fv.y, im.alpha, im.beta, im.l1, im.l2, im.pf, a.sp, a.idiv, acc);
+            wn2[q] = z;
+            if (a.halo_up != nullptr) {
+                const size_t p = base + 2 * (size_t)q;
+                if (p < a.halo_px) { a.halo_up[p] = z.x; a.halo_up[p + 1] = z.y; }
+                else if (p >= a.HW - a.halo_px) {
+                    a.halo_dn[p - (a.HW - a.halo_px)] = z.x; a.halo_dn[p + 1 - (a.HW - a.halo_px)] = z.y;
+                }
+            }
+            if (!more) break;
+            q = qn; wv = wv1; wpv = wpv1; gs = gs1; fv = fv1;
+        }
+    }
+    if (a.halo_sys_fence) __threadfence_system();
+    k2_block_partials(acc, a.ppart + ((size_t)b * a.nblk + bx) * kNumPart);
+}
+
+// L2 prefetch of bytes [p, p + n) by one bulk request (the 16-B aligned interior; a hint: the
+// loads that follow read the same addresses)
+__device__ __forceinline__ void l2_prefetch_range(const void* p, size_t n) {
+    const uintptr_t s = ((uintptr_t)p + 15) & ~(uintptr_t)15, e = ((uintptr_t)p + n) & ~(uintptr_t)15;
+    if (e > s)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(s), "r"((uint32_t)(e - s)) : "memory");
+}
+
+#ifndef FOE_K2_L2PF
+#define FOE_K2_L2PF 1
+#endif
 template <int PXT>
 __global__ void __launch_bounds__(kThreads, FOE_K2_CTAS)
-k_inertial_prox(const K2Args a) {  // (4 CTAs/SM: <= 64 registers; 3 -> 4 gave 253 -> 222 us, 5 spills)
+k_inertial_prox(const K2Args a) {
+#if FOE_K2_ETAB
+    k2_etab_init();
+    __syncthreads();
+#endif
     pdl_wait();   // programmatic launch after K3: its control blocks must be complete
-    inertial_prox_blk<PXT>(a, blockIdx.x, blockIdx.y);
+#if FOE_K2_L2PF
+    // K2 is latency-bound on its loads (long-scoreboard stalls at the first use of g and f~): one
+    // thread asks L2 for the block's whole range of w, w-, g, f~ up front, so that the per-pixel
+    // loads after the first unrolled pair hit L2 (~250 cycles) instead of HBM
+    if (threadIdx.x == 0) {
+        const ImgCtl& c = a.ctl[blockIdx.y];
+        const size_t base = (size_t)blockIdx.x * (kThreads * PXT);
+        if (c.active && base < a.HW) {
+            const size_t n = min((size_t)(kThreads * PXT), a.HW - base), o = (size_t)blockIdx.y * a.HW + base;
+            l2_prefetch_range(a.w + (size_t)c.cur * a.w_slot_stride + o, n * 8);
+            l2_prefetch_range(a.w + (size_t)c.prev * a.w_slot_stride + o, n * 8);
+            for (int q = 0; q < a.groups; ++q)
+                l2_prefetch_range(a.g + (size_t)c.gcur * a.g_slot_stride + (size_t)q * a.g_group_stride + o, n * 4);
+            l2_prefetch_range(a.ft + o, n * 4);
+        }
+    }
+#endif
+    if (PXT % 2 == 0 && a.pairs) {
+        __shared__ K2Img im;
+        const ImgCtl& c = a.ctl[blockIdx.y];
+        if (c.active) {
+            if (threadIdx.x == 0) {
+                im.alpha = a.sp.safety * 2.0 * (1.0 - a.sp.beta) / c.L;
+                im.beta = a.sp.beta; im.l1 = c.lam1; im.l2 = c.lam2;
+                im.pf = ProxF{(float)(im.alpha * c.lam1), (float)(im.alpha * c.lam2)};
+            }
+            __syncthreads();
+            inertial_prox_pairs<PXT>(a, im, blockIdx.x, blockIdx.y);
+        }
+    } else {
+        inertial_prox_blk<PXT>(a, blockIdx.x, blockIdx.y);
+    }
     pdl_trigger();
 }
 

@@ -81,6 +81,9 @@ k_ipiano_persistent(const PersistArgs pa, const __grid_constant__ TapParams2 tp)
         long long* dst = reinterpret_cast<long long*>(my);
         for (int i = threadIdx.x; i < words; i += kThreads) dst[i] = src[i];
     }
+#if FOE_K2_ETAB
+    k2_etab_init();   // the prox's exponential table (phase A)
+#endif
     __syncthreads();
     unsigned int gen = 0;
     int round = 0;
