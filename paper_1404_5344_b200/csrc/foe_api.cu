@@ -1000,6 +1000,7 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
         if (st->pxt2 == 1) CK(launch_pdl(foe::k_inertial_prox<1>, g2, tb, 0, s, a2));
         else if (st->pxt2 == 4) CK(launch_pdl(foe::k_inertial_prox<4>, g2, tb, 0, s, a2));
         else if (st->pxt2 == 16) CK(launch_pdl(foe::k_inertial_prox<16>, g2, tb, 0, s, a2));
+        else if (st->pxt2 == 32) CK(launch_pdl(foe::k_inertial_prox<32>, g2, tb, 0, s, a2));
         else CK(launch_pdl(foe::k_inertial_prox<kPxt2>, g2, tb, 0, s, a2));
         count_launch(1);
         CKL("k_inertial_prox");
@@ -1313,7 +1314,11 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     // 16 pixels per thread halve the per-pixel share of K2's block reduction (c4: 223 -> 213 us)
     // when the launch still has >= 4 blocks per SM; slab members keep kPxt2 (whole K2 blocks per
     // 64-row band for W % 32 == 0)
+#ifndef FOE_K2_PXT_LARGE
+#define FOE_K2_PXT_LARGE 16
+#endif
     if (!t_slab_member && (long long)B * H * W >= 4LL * md->nsm * kThreads * 16) st->pxt2 = 16;
+    if (!t_slab_member && (long long)B * H * W >= 4LL * md->nsm * kThreads * FOE_K2_PXT_LARGE) st->pxt2 = FOE_K2_PXT_LARGE;
 #ifndef FOE_K2_PXT_SMALL
 #define FOE_K2_PXT_SMALL 4
 #endif

@@ -35,6 +35,9 @@ constexpr int kThreads = 256;
 #ifndef FOE_K2_PAIRS
 #define FOE_K2_PAIRS 1    // K2 by pixel pairs (inertial_prox_pairs) when HW % 4 == 0
 #endif
+#ifndef FOE_K2_LOCKSTEP
+#define FOE_K2_LOCKSTEP 0 // K2 pairs: both fast-path proxes as one block (k2_pair; measured 153 vs 152 us: off)
+#endif
 #ifndef FOE_K2_CTAS
 #define FOE_K2_CTAS 3     // K2 CTAs per SM (80 registers; pairs: 223 us at 4 CTAs (spills) vs 163 at 3)
 #endif
@@ -784,43 +787,46 @@ __device__ __forceinline__ float ex2_approx(float x) {
 struct ProxF {
     float tl1, tl2;
 };
-__device__ __forceinline__ int prox_newton(double what, double ft, float ff, const ProxF& pf, double tau, double l1,
-                                           double l2, double tol, int cap, double& z_out,
-                                           double& em_out, double& ep_out) {
-    const double f2 = ft * ft;
-    // Fast path: three Newton steps on d in fp32 (MUFU exponentials, ~1e-7 relative), then ONE fp64
-    // Newton step from there -- quadratic convergence takes the fp32 error to ~1e-14, accepted by
-    // the same error bound as below; one fp64 exponential pair (at z0 = what + d32) instead of two
-    if (fabs(what) <= 40.0) {
-        const float f2f = ff * ff, tl1f2 = pf.tl1 * f2f, tl2 = pf.tl2, c0f = fmaf(-pf.tl2, f2f, pf.tl1);
-        const float wf = (float)what;
-        const float Af = tl1f2 * ex2_approx(-2.8853900817779268f * wf), Bf = tl2 * ex2_approx(2.8853900817779268f * wf);
-        float d = -(c0f - Af + Bf) * rcp_approx(1.0f + 2.0f * (Af + Bf));
+// The fast path: one fp32 Newton step from d = 0 and FOE_K2_F32_STEPS more (MUFU exponentials,
+// ~1e-7 relative), then ONE fp64 Newton step from there -- quadratic convergence takes the fp32
+// error to ~1e-14, accepted by the error bound above; one fp64 exponential pair (at
+// z0 = what + d32) instead of two.  Branch-free (|what| > 40 is computed at what = 0 and
+// rejected), so that the two pixels of a pair interleave.  Returns true when accepted.
+__device__ __forceinline__ bool prox_fast(double what, double f2, float ff, const ProxF& pf, double tau, double l1,
+                                          double l2, double tol, double& z_out, double& em_out, double& ep_out) {
+    const bool inr = fabs(what) <= 40.0;
+    const double wc = inr ? what : 0.0;
+    const float f2f = ff * ff, tl1f2 = pf.tl1 * f2f, tl2 = pf.tl2, c0f = fmaf(-pf.tl2, f2f, pf.tl1);
+    const float wf = (float)wc;
+    const float Af = tl1f2 * ex2_approx(-2.8853900817779268f * wf), Bf = tl2 * ex2_approx(2.8853900817779268f * wf);
+    float d = -(c0f - Af + Bf) * rcp_approx(1.0f + 2.0f * (Af + Bf));
 #pragma unroll
-        for (int k = 0; k < FOE_K2_F32_STEPS; ++k) {
-            const float p = ex2_approx(2.8853900817779268f * d), q = rcp_approx(p);
-            const float am = Af * q, bp = Bf * p;
-            d -= (d + c0f - am + bp) * rcp_approx(1.0f + 2.0f * (am + bp));
-        }
-        const double z0 = what + (double)d;
-        double Ep0, Em0;
-#if FOE_K2_ETAB
-        exp2a_pm_tab(z0, Ep0, Em0);                // e^{2 z0}, e^{-2 z0}
-#else
-        exp2a_pm(z0, Ep0, Em0);
-#endif
-        const double am = tau * l1 * f2 * Em0, bp = tau * l2 * Ep0;
-        const double phi = (double)d + tau * (l1 - l2 * f2) - am + bp;
-        const double dphi = 1.0 + 2.0 * (am + bp);
-        const double st = phi * rcp_f64(dphi);
-        if (isfinite(st) && (dphi - 1.0) * st * st <= 0.25 * tol && fabs(st) <= 1e-6) {
-            const double e = -2.0 * st;                                  // e^{+-e}, |e| <= 2e-6
-            z_out = z0 - st;
-            ep_out = Ep0 * fma(0.5 * e, e, 1.0 + e);
-            em_out = Em0 * fma(0.5 * e, e, 1.0 - e);
-            return 4;
-        }
+    for (int k = 0; k < FOE_K2_F32_STEPS; ++k) {
+        const float p = ex2_approx(2.8853900817779268f * d), q = rcp_approx(p);
+        const float am = Af * q, bp = Bf * p;
+        d -= (d + c0f - am + bp) * rcp_approx(1.0f + 2.0f * (am + bp));
     }
+    const double z0 = wc + (double)d;
+    double Ep0, Em0;
+#if FOE_K2_ETAB
+    exp2a_pm_tab(z0, Ep0, Em0);                // e^{2 z0}, e^{-2 z0}
+#else
+    exp2a_pm(z0, Ep0, Em0);
+#endif
+    const double am = tau * l1 * f2 * Em0, bp = tau * l2 * Ep0;
+    const double phi = (double)d + tau * (l1 - l2 * f2) - am + bp;
+    const double dphi = 1.0 + 2.0 * (am + bp);
+    const double st = phi * rcp_f64(dphi);
+    const double e = -2.0 * st;                                  // e^{+-e}, |e| <= 2e-6 when accepted
+    z_out = z0 - st;
+    ep_out = Ep0 * fma(0.5 * e, e, 1.0 + e);
+    em_out = Em0 * fma(0.5 * e, e, 1.0 - e);
+    return inr & isfinite(st) & ((dphi - 1.0) * st * st <= 0.25 * tol) & (fabs(st) <= 1e-6);
+}
+
+// The safeguarded part of the prox (when the fast path rejects)
+__device__ __forceinline__ int prox_slow(double what, double ft, double f2, double tau, double l1, double l2,
+                                         double tol, int cap, double& z_out, double& em_out, double& ep_out) {
     double Em, Ep;
     if (fabs(what) <= 340.0) {
         exp2a_pm(what, Ep, Em);                    // e^{2 what}, e^{-2 what}
@@ -868,6 +874,14 @@ __device__ __forceinline__ int prox_newton(double what, double ft, float ff, con
     return -1;
 }
 
+__device__ __forceinline__ int prox_newton(double what, double ft, float ff, const ProxF& pf, double tau, double l1,
+                                           double l2, double tol, int cap, double& z_out,
+                                           double& em_out, double& ep_out) {
+    const double f2 = ft * ft;
+    if (prox_fast(what, f2, ff, pf, tau, l1, l2, tol, z_out, em_out, ep_out)) return 4;
+    return prox_slow(what, ft, f2, tau, l1, l2, tol, cap, z_out, em_out, ep_out);
+}
+
 struct K2Args {
     double* w;            // [3][B][HW]
     size_t w_slot_stride;
@@ -898,6 +912,24 @@ struct K2Acc {
     int nit = 0, fail = 0;
 };
 
+// a pixel's contribution to the test partials (a10)
+__device__ __forceinline__ void k2_acc(K2Acc& acc, double wv, double gv, double f2, double z, double em, double ep,
+                                       int it, double l1, double l2, int idiv) {
+    const double d = z - wv;
+    acc.gd += gv * d;
+    acc.dd += d * d;
+    if (idiv) {
+        acc.Gp += 0.5 * l1 * (z * z - 2.0 * f2 * log(z));                 // Eq.(5), PAPER.md:144
+        acc.wmax = fmax(acc.wmax, z > 0.0 ? 0.0 : INFINITY);              // the iterate must stay > 0
+    } else {
+        acc.Gp += 0.5 * l1 * (2.0 * z + f2 * em) + 0.5 * l2 * (ep - 2.0 * f2 * z);
+        acc.wmax = fmax(acc.wmax, fabs(z));
+    }
+    acc.ww += wv * wv;
+    if (it < 0) ++acc.fail; else acc.nit = max(acc.nit, it);
+    if (!(z == z)) acc.wmax = INFINITY;
+}
+
 // One pixel of K2 (a8-a10): inertial point, prox, and its contribution to the test partials.
 // Shared by k_inertial_prox and the persistent driver's phase A; the inertial point is written
 // with explicit roundings so that both compile to the same arithmetic (bitwise-equal w+).
@@ -915,21 +947,30 @@ __device__ __forceinline__ double k2_pixel(double wv, double wpv, double gv, dou
     } else {
         it = prox_newton(what, f, ff, pf, alpha, l1, l2, sp.newton_tol, sp.newton_cap, z, em, ep);
     }
-    const double d = z - wv;
-    acc.gd += gv * d;
-    acc.dd += d * d;
-    const double f2 = f * f;
-    if (idiv) {
-        acc.Gp += 0.5 * l1 * (z * z - 2.0 * f2 * log(z));                 // Eq.(5), PAPER.md:144
-        acc.wmax = fmax(acc.wmax, z > 0.0 ? 0.0 : INFINITY);              // the iterate must stay > 0
-    } else {
-        acc.Gp += 0.5 * l1 * (2.0 * z + f2 * em) + 0.5 * l2 * (ep - 2.0 * f2 * z);
-        acc.wmax = fmax(acc.wmax, fabs(z));
-    }
-    acc.ww += wv * wv;
-    if (it < 0) ++acc.fail; else acc.nit = max(acc.nit, it);
-    if (!(z == z)) acc.wmax = INFINITY;
+    k2_acc(acc, wv, gv, f * f, z, em, ep, it, l1, l2, idiv);
     return z;
+}
+
+// Lock-step pair of pixels of model (10)/(8) (inertial_prox_pairs): both inertial points, both
+// fast-path proxes as one straight-line block (the scheduler interleaves the two dependency
+// chains), the safeguarded prox only for a rejected pixel, then the partials in pixel order --
+// per pixel the same arithmetic as k2_pixel.
+__device__ __forceinline__ double2 k2_pair(const double2 wv, const double2 wpv, const float2 gs, const float2 fv,
+                                           double alpha, double beta, double l1, double l2, const ProxF& pf,
+                                           const SolverParams& sp, K2Acc& acc) {
+    const double gx = (double)gs.x, gy = (double)gs.y, fx = (double)fv.x, fy = (double)fv.y;
+    const double wx = __fma_rn(beta, __dsub_rn(wv.x, wpv.x), __fma_rn(-alpha, gx, wv.x));
+    const double wy = __fma_rn(beta, __dsub_rn(wv.y, wpv.y), __fma_rn(-alpha, gy, wv.y));
+    const double f2x = fx * fx, f2y = fy * fy;
+    double zx, emx, epx, zy, emy, epy;
+    const bool okx = prox_fast(wx, f2x, fv.x, pf, alpha, l1, l2, sp.newton_tol, zx, emx, epx);
+    const bool oky = prox_fast(wy, f2y, fv.y, pf, alpha, l1, l2, sp.newton_tol, zy, emy, epy);
+    int itx = 4, ity = 4;
+    if (!okx) itx = prox_slow(wx, fx, f2x, alpha, l1, l2, sp.newton_tol, sp.newton_cap, zx, emx, epx);
+    if (!oky) ity = prox_slow(wy, fy, f2y, alpha, l1, l2, sp.newton_tol, sp.newton_cap, zy, emy, epy);
+    k2_acc(acc, wv.x, gx, f2x, zx, emx, epx, itx, l1, l2, 0);
+    k2_acc(acc, wv.y, gy, f2y, zy, emy, epy, ity, l1, l2, 0);
+    return make_double2(zx, zy);
 }
 
 // fixed-order CTA reduction of the 7 test partials (sums; slots 4 and 5 max) -> out[0..7]
@@ -1027,8 +1068,12 @@ __device__ __forceinline__ void inertial_prox_pairs(const K2Args& a, const K2Img
                 for (int kk = 1; kk < a.groups; ++kk) { const float2 t = g2[kk * gq + qn]; gs1.x += t.x; gs1.y += t.y; }
             }
             double2 z;
-            z.x = k2_pixel(wv.x, wpv.x, (double)gs.x, (double)fv.x, fv.x, im.alpha, im.beta, im.l1, im.l2, im.pf, a.sp, a.idiv, acc);
-            z.y = k2_pixel(wv.y, wpv.y, (double)gs.y, (double)fv.y, fv.y, im.alpha, im.beta, im.l1, im.l2, im.pf, a.sp, a.idiv, acc);
+            if (a.idiv || !FOE_K2_LOCKSTEP) {
+                z.x = k2_pixel(wv.x, wpv.x, (double)gs.x, (double)fv.x, fv.x, im.alpha, im.beta, im.l1, im.l2, im.pf, a.sp, a.idiv, acc);
+                z.y = k2_pixel(wv.y, wpv.y, (double)gs.y, (double)fv.y, fv.y, im.alpha, im.beta, im.l1, im.l2, im.pf, a.sp, a.idiv, acc);
+            } else {
+                z = k2_pair(wv, wpv, gs, fv, im.alpha, im.beta, im.l1, im.l2, im.pf, a.sp, acc);
+            }
             wn2[q] = z;
             if (a.halo_up != nullptr) {
                 const size_t p = base + 2 * (size_t)q;
