@@ -393,6 +393,7 @@ def main():
     if profile_in_timed:
         P.ipiano_profile(st, True)
         P.ipiano_profile_read(st)  # reset counters
+        P.ipiano_profile_read_k2(st)
     sampler = ClockSampler(smi_index(local)) if rank == 0 else None
     if sampler:
         sampler.start()
@@ -414,18 +415,22 @@ def main():
     D.barrier()
     clocks = sampler.stop() if sampler else None
     cnt = P.ipiano_get_counters(st)
+    k2_ms, k2_launches = 0.0, 0
     if persistent:
         k1_ms, k1_launches = sum(a.elapsed_time(b) for a, b in solve_ms), len(solve_ms)
         kernel_timing = "the cooperative launch of each timed step, CUDA events on the launching stream"
     elif profile_in_timed:
         k1_ms, k1_launches, _ = P.ipiano_profile_read(st)
+        k2_ms, k2_launches = P.ipiano_profile_read_k2(st)
         kernel_timing = "every launch in the timed region, CUDA events on the library's stream"
     else:
         P.ipiano_profile(st, True)
         P.ipiano_profile_read(st)
+        P.ipiano_profile_read_k2(st)
         step()
         torch.cuda.synchronize()
         k1_ms, k1_launches, _ = P.ipiano_profile_read(st)
+        k2_ms, k2_launches = P.ipiano_profile_read_k2(st)
         k1_ms *= args.steps           # per-launch time x the timed region's launches (same trials)
         k1_launches *= args.steps
         P.ipiano_profile(st, False)
@@ -446,6 +451,15 @@ def main():
                               persistent=persistent)
     roofline["kernel_timing"] = kernel_timing
     fp32_peak = roofline["fp32_peak"]
+    # K2 (inertial step + prox + partials), the second kernel of a round: HBM-bound at 32 B/px
+    # algorithmic (read w, w- 8+8, g 4, f~ 4; write w+ 8), timed by the same events
+    k2 = None
+    if not persistent and k2_launches:
+        k2_us = 1e3 * k2_ms / k2_launches
+        k2_gbs = 32.0 * B * H * W / (k2_us * 1e-6) / 1e9
+        hbm = measured_peaks()[0].get("hbm_gbs")
+        k2 = {"us_per_launch": k2_us, "launches_profiled": k2_launches, "achieved_gbs": k2_gbs,
+              "bytes_per_px": 32, "peak_gbs": hbm, "frac": (k2_gbs / hbm) if hbm else None}
 
     # ---- e2e: the public C-ABI call with host buffers (H2D of f and D2H of u inside)
     e2e = None
@@ -509,7 +523,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "dtype_detail": DTYPE_DETAIL[P.ipiano_state_stencil(st)],
             "data": "synthetic", "config": config_block(cfg, ws, B, H * W, args),
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "roofline": roofline, "k2": k2, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "trials_per_iter": trials_per_step / (B * cfg.iters),
             "run_fp32_frac": (flops_per_eval_px * H * W * trials_per_step * args.steps * ws / (total_ms / 1e3) / 1e12)
                              / fp32_peak / ws,

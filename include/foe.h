@@ -246,6 +246,9 @@ foe_status ipiano_get_trace(const ipiano_state* st, void* host_trace, size_t byt
 foe_status ipiano_profile(ipiano_state* st, int enable);
 foe_status ipiano_profile_read(ipiano_state* st, double* k1_ms, long long* k1_launches,
                                long long* total_launches);
+/* The same for K2 (k_inertial_prox: inertial step + prox + test partials) of the graph driver
+ * (events before K2 and before the prior kernel of each profiled round); resets its counters. */
+foe_status ipiano_profile_read_k2(ipiano_state* st, double* k2_ms, long long* k2_launches);
 
 /* The stencil this state resolved to (FOE_STENCIL_FFMA or FOE_STENCIL_TENSOR). */
 int ipiano_state_stencil(const ipiano_state* st);

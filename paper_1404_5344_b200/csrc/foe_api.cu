@@ -239,9 +239,9 @@ struct ipiano_state {
     int graph_rounds = 0;
     bool profile = false;
     std::vector<cudaEvent_t> ev_pool;
-    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_live;
-    double k1_ms = 0.0;
-    long long k1_launches = 0, total_launches = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_live, ev_live_k2;
+    double k1_ms = 0.0, k2_ms = 0.0;
+    long long k1_launches = 0, total_launches = 0, k2_launches = 0;
 };
 
 namespace {
@@ -994,6 +994,11 @@ foe::K3Args state_k3_args(const ipiano_state* st) {
 // One trial round for every active image: K2 -> K1 (candidate) -> K3, as programmatic dependent
 // launches (each kernel's launch and independent prologue overlap its predecessor's drain).
 foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
+    cudaEvent_t k0 = nullptr;
+    if (timed) {
+        k0 = pool_event(st);
+        CK(cudaEventRecord(k0, s));
+    }
     {
         const foe::K2Args a2 = state_k2_args(st);
         const dim3 g2(st->nblk2, st->B), tb(kThreads);
@@ -1011,6 +1016,8 @@ foe_status launch_round(ipiano_state* st, cudaStream_t s, bool timed) {
         e0 = pool_event(st);
         e1 = pool_event(st);
         CK(cudaEventRecord(e0, s));
+        st->ev_live_k2.emplace_back(k0, e0);
+        st->k2_launches += 1;
     }
     foe_status rl = launch_prior(st->model, st->kind, a1, st->B, s, -1, !timed);
     if (rl != FOE_OK) return rl;
@@ -1140,6 +1147,12 @@ foe_status sync_ctl(ipiano_state* st) {
         st->ev_pool.push_back(pr.second);
     }
     st->ev_live.clear();
+    for (auto& pr : st->ev_live_k2) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) st->k2_ms += ms;
+        st->ev_pool.push_back(pr.first);   // (pr.second is also an ev_live start event)
+    }
+    st->ev_live_k2.clear();
     return FOE_OK;
 }
 
@@ -1225,6 +1238,7 @@ void ipiano_state_destroy(ipiano_state* st) {
     if (st->hctl) cudaFreeHost(st->hctl);
     for (auto e : st->ev_pool) cudaEventDestroy(e);
     for (auto& pr : st->ev_live) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+    for (auto& pr : st->ev_live_k2) cudaEventDestroy(pr.first);
     if (st->sync_ev) cudaEventDestroy(st->sync_ev);
     if (st->s) cudaStreamDestroy(st->s);
     delete st;
@@ -1528,6 +1542,18 @@ foe_status ipiano_profile_read(ipiano_state* st, double* k1_ms, long long* k1_la
     st->k1_ms = 0.0;
     st->k1_launches = 0;
     st->total_launches = 0;
+    return FOE_OK;
+}
+
+foe_status ipiano_profile_read_k2(ipiano_state* st, double* k2_ms, long long* k2_launches) {
+    if (!st) return fail(FOE_ERR_INVALID_ARGUMENT, "state is NULL");
+    CK(cudaSetDevice(st->model->dev));
+    foe_status r = sync_ctl(st);
+    if (r != FOE_OK) return r;
+    if (k2_ms) *k2_ms = st->k2_ms;
+    if (k2_launches) *k2_launches = st->k2_launches;
+    st->k2_ms = 0.0;
+    st->k2_launches = 0;
     return FOE_OK;
 }
 

@@ -727,7 +727,7 @@ __device__ __forceinline__ void exp2a_pm(double a, double& ep, double& em) {
     em = (c - sh) * __hiloint2double((1023 - ni) << 20, 0);
 }
 
-// Table-driven e^{2a} and e^{-2a} for the prox's fast path (|2a| <= 700): 2a = (64 m + j) ln2/64 + r,
+// Table-driven e^{2a} and e^{-2a} for the prox's fast path (|2a| <= 160): 2a = (64 m + j) ln2/64 + r,
 // |r| <= ln2/128; e^{+-2a} = 2^{+-m} 2^{+-j/64} e^{+-r}, the cosh/sinh parts of r to r^6 / r^5
 // (remainder < 4e-17 relative).  tab = k2_etab(): [0, 64) = 2^{j/64}, [64, 128) = 2^{-j/64}, in
 // shared memory (filled by k2_etab_init); 2 table reads instead of ten more fp64 FMAs.
@@ -735,9 +735,44 @@ __device__ __forceinline__ double* k2_etab() {
     __shared__ double t[128];
     return t;
 }
+// 2^{j/64} (j = 0..63), then 2^{-j/64}: correctly rounded (60-digit decimal evaluation)
+__device__ const double kK2Etab[128] = {
+    1.0, 1.0108892860517005, 1.0218971486541166, 1.0330248790212284,
+    1.0442737824274138, 1.0556451783605572, 1.0671404006768237, 1.0787607977571199,
+    1.0905077326652577, 1.102382583307841, 1.1143867425958924, 1.1265216186082418,
+    1.1387886347566916, 1.1511892299529827, 1.1637248587775775, 1.1763969916502812,
+    1.189207115002721, 1.202156731452703, 1.215247359980469, 1.22848053610687,
+    1.241857812073484, 1.255380757024691, 1.2690509571917332, 1.2828700160787783,
+    1.2968395546510096, 1.3109612115247644, 1.3252366431597413, 1.339667524053303,
+    1.3542555469368927, 1.3690024229745905, 1.383909881963832, 1.3989796725383112,
+    1.4142135623730951, 1.42961333839197, 1.4451808069770467, 1.460917794180647,
+    1.4768261459394993, 1.4929077282912648, 1.5091644275934228, 1.5255981507445384,
+    1.5422108254079407, 1.559004400237837, 1.5759808451078865, 1.593142151342267,
+    1.6104903319492543, 1.6280274218573478, 1.645755478153965, 1.6636765803267364,
+    1.681792830507429, 1.7001063537185235, 1.718619298122478, 1.7373338352737062,
+    1.7562521603732995, 1.7753764925265212, 1.7947090750031072, 1.8142521755003989,
+    1.8340080864093424, 1.8539791250833855, 1.8741676341103, 1.8945759815869656,
+    1.9152065613971474, 1.9360617934922943, 1.9571441241754002, 1.978456026387951,
+    1.0, 0.9892280131939755, 0.9785720620877001, 0.9680308967461472,
+    0.9576032806985737, 0.9472879907934828, 0.93708381705515, 0.9269895625416927,
+    0.9170040432046712, 0.9071260877501994, 0.8973545375015536, 0.8876882462632606,
+    0.8781260801866497, 0.8686669176368531, 0.859309649061239, 0.8500531768592617,
+    0.8408964152537145, 0.8318382901633682, 0.8228777390769825, 0.8140137109286739,
+    0.8052451659746271, 0.7965710756711335, 0.7879904225539432, 0.7795022001189185,
+    0.7711054127039704, 0.7627990753722692, 0.7545822137967114, 0.7464538641456324,
+    0.7384130729697497, 0.7304588970903235, 0.7225904034885233, 0.714806669195985,
+    0.7071067811865476, 0.6994898362691556, 0.691954940981916, 0.6845012114872953,
+    0.6771277734684463, 0.6698337620266515, 0.6626183215798707, 0.6554806057623822,
+    0.6484197773255048, 0.6414350080393891, 0.6345254785958666, 0.6276903785123455,
+    0.620928906036742, 0.614240268053435, 0.6076236799902345, 0.6010783657263515,
+    0.5946035575013605, 0.5881984958251406, 0.5818624293887887, 0.5755946149764913,
+    0.5693943173783458, 0.5632608093041209, 0.5571933712979462, 0.5511912916539204,
+    0.5452538663326288, 0.5393803988785599, 0.5335702003384118, 0.5278225891802786,
+    0.5221368912137069, 0.5165124395106142, 0.5109485743270583, 0.5054446430258502,
+};
 __device__ __forceinline__ void k2_etab_init() {
     double* t = k2_etab();
-    for (int i = threadIdx.x; i < 128; i += blockDim.x) t[i] = exp2((i < 64 ? i : 64 - i) * (1.0 / 64.0));
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) t[i] = kK2Etab[i];
 }
 __device__ __forceinline__ void exp2a_pm_tab(double a, double& ep, double& em) {
     const double x = 2.0 * a;
@@ -748,8 +783,9 @@ __device__ __forceinline__ void exp2a_pm_tab(double a, double& ep, double& em) {
     const double c = fma(r2, fma(r2, fma(r2, 1.0 / 720.0, 1.0 / 24.0), 0.5), 1.0);
     const double s = r * fma(r2, fma(r2, 1.0 / 120.0, 1.0 / 6.0), 1.0);
     const double* t = k2_etab();
-    ep = (c + s) * (t[j] * __hiloint2double((m + 1023) << 20, 0));
-    em = (c - s) * (t[64 + j] * __hiloint2double((1023 - m) << 20, 0));
+    const double tp = t[j], tm = t[64 + j];                 // 2^{+-m} by the exponent field (|m| <= 127)
+    ep = (c + s) * __hiloint2double(__double2hiint(tp) + (m << 20), __double2loint(tp));
+    em = (c - s) * __hiloint2double(__double2hiint(tm) - (m << 20), __double2loint(tm));
 }
 
 // 1/b to full fp64 precision: MUFU reciprocal seed + two Newton steps (b finite, nonzero)
@@ -821,7 +857,8 @@ __device__ __forceinline__ bool prox_fast(double what, double f2, float ff, cons
     z_out = z0 - st;
     ep_out = Ep0 * fma(0.5 * e, e, 1.0 + e);
     em_out = Em0 * fma(0.5 * e, e, 1.0 - e);
-    return inr & isfinite(st) & ((dphi - 1.0) * st * st <= 0.25 * tol) & (fabs(st) <= 1e-6);
+    // (|z0| <= 80 keeps 2 z0 inside the table exponential's range, |2a| <= 160)
+    return inr & (fabs(z0) <= 80.0) & isfinite(st) & ((dphi - 1.0) * st * st <= 0.25 * tol) & (fabs(st) <= 1e-6);
 }
 
 // The safeguarded part of the prox (when the fast path rejects)
@@ -908,11 +945,14 @@ struct K2Args {
 // Test partials of one trial (a10): <g, D>, ||D||^2, G(w+), ||w||^2, max |w+| (or the domain
 // flag of model (6)), max Newton iterations, prox failures.
 struct K2Acc {
-    double gd = 0, dd = 0, Gp = 0, ww = 0, wmax = 0;
+    double gd = 0, dd = 0, Gp = 0, ww = 0;
+    unsigned long long wbits = 0;   // max |w+| as the bits of a non-negative double (NaN > inf)
     int nit = 0, fail = 0;
 };
 
 // a pixel's contribution to the test partials (a10)
+// (G(w+) of Eq. (10): (l1/2)(2z + f^2 e^{-2z}) + (l2/2)(e^{2z} - 2 f^2 z) = l1 z + (l1/2) f^2 e^{-2z}
+//  + (l2/2) e^{2z} - l2 f^2 z; max |w+| by the bits of |z|, NaN above inf)
 __device__ __forceinline__ void k2_acc(K2Acc& acc, double wv, double gv, double f2, double z, double em, double ep,
                                        int it, double l1, double l2, int idiv) {
     const double d = z - wv;
@@ -920,14 +960,17 @@ __device__ __forceinline__ void k2_acc(K2Acc& acc, double wv, double gv, double 
     acc.dd += d * d;
     if (idiv) {
         acc.Gp += 0.5 * l1 * (z * z - 2.0 * f2 * log(z));                 // Eq.(5)
-        acc.wmax = fmax(acc.wmax, z > 0.0 ? 0.0 : INFINITY);              // the iterate must stay > 0
+        const unsigned long long b = z > 0.0 ? 0ull : 0x7ff0000000000000ull;   // the iterate must stay > 0
+        acc.wbits = max(acc.wbits, b);
     } else {
-        acc.Gp += 0.5 * l1 * (2.0 * z + f2 * em) + 0.5 * l2 * (ep - 2.0 * f2 * z);
-        acc.wmax = fmax(acc.wmax, fabs(z));
+        double g = fma(0.5 * l1, f2 * em, acc.Gp);
+        g = fma(0.5 * l2, ep, g);
+        g = fma(l1, z, g);
+        acc.Gp = fma(-l2, f2 * z, g);
+        acc.wbits = max(acc.wbits, (unsigned long long)__double_as_longlong(z) & 0x7fffffffffffffffull);
     }
     acc.ww += wv * wv;
     if (it < 0) ++acc.fail; else acc.nit = max(acc.nit, it);
-    if (!(z == z)) acc.wmax = INFINITY;
 }
 
 // One pixel of K2 (a8-a10): inertial point, prox, and its contribution to the test partials.
@@ -976,7 +1019,8 @@ __device__ __forceinline__ double2 k2_pair(const double2 wv, const double2 wpv, 
 // fixed-order CTA reduction of the 7 test partials (sums; slots 4 and 5 max) -> out[0..7]
 // (out[7] = 0); every thread of the CTA calls it
 __device__ __forceinline__ void k2_block_partials(const K2Acc& acc, double* out) {
-    double v[7] = {acc.gd, acc.dd, acc.Gp, acc.ww, acc.wmax, (double)acc.nit, (double)acc.fail};
+    const double wmax = acc.wbits > 0x7ff0000000000000ull ? INFINITY : __longlong_as_double((long long)acc.wbits);
+    double v[7] = {acc.gd, acc.dd, acc.Gp, acc.ww, wmax, (double)acc.nit, (double)acc.fail};
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
@@ -1099,7 +1143,7 @@ __device__ __forceinline__ void l2_prefetch_range(const void* p, size_t n) {
 }
 
 #ifndef FOE_K2_L2PF
-#define FOE_K2_L2PF 1
+#define FOE_K2_L2PF 0   // measured with the pair path: 158.7 us with, 153.9 without
 #endif
 template <int PXT>
 __global__ void __launch_bounds__(kThreads, FOE_K2_CTAS)

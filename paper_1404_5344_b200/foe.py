@@ -29,7 +29,7 @@ EXPORTED = (
     "foe_last_error", "foe_status_string", "foe_version", "foe_kernel_launches", "foe_model_create", "foe_model_destroy",
     "foe_energy_grad", "foe_hvp", "foe_estimate_lipschitz", "ipiano_config_default",
     "ipiano_state_create", "ipiano_state_reset", "ipiano_step", "ipiano_solve", "ipiano_get_iterate",
-    "ipiano_get_counters", "ipiano_get_trace", "ipiano_profile", "ipiano_profile_read",
+    "ipiano_get_counters", "ipiano_get_trace", "ipiano_profile", "ipiano_profile_read", "ipiano_profile_read_k2",
     "ipiano_state_destroy", "ipiano_state_stencil", "ipiano_state_solver", "ipiano_run",
     "foe_model_set_stencil", "foe_slab_exchange_plan", "foe_comm_unique_id", "foe_comm_create", "foe_comm_destroy", "ipiano_slabs_create", "ipiano_slabs_reset",
     "ipiano_slabs_solve", "ipiano_slabs_advance", "ipiano_slabs_get_iterate", "ipiano_slabs_member", "ipiano_slabs_destroy",
@@ -93,6 +93,7 @@ def lib():
     L.ipiano_get_trace.argtypes = [_vp, _vp, C.c_size_t]
     L.ipiano_profile.argtypes = [_vp, C.c_int]
     L.ipiano_profile_read.argtypes = [_vp, _dp, _llp, _llp]
+    L.ipiano_profile_read_k2.argtypes = [_vp, _dp, _llp]
     L.ipiano_state_stencil.argtypes = [_vp]
     L.ipiano_state_stencil.restype = C.c_int
     L.ipiano_state_solver.argtypes = [_vp]
@@ -401,6 +402,13 @@ def ipiano_profile_read(state: State):
     ms = C.c_double(); n = C.c_longlong(); tot = C.c_longlong()
     _check(lib().ipiano_profile_read(state.handle, C.byref(ms), C.byref(n), C.byref(tot)))
     return ms.value, n.value, tot.value
+
+
+def ipiano_profile_read_k2(state: State):
+    """(ms, launches) of K2 in the profiled rounds since the last call (graph driver)."""
+    ms = C.c_double(); n = C.c_longlong()
+    _check(lib().ipiano_profile_read_k2(state.handle, C.byref(ms), C.byref(n)))
+    return ms.value, n.value
 
 
 def ipiano_state_stencil(state: State) -> int:
