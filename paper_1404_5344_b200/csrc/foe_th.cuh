@@ -108,12 +108,30 @@ struct ThConst {
     float kabs;     // max_i sum_t |k_i[t]| (bounds |K t| for the HVP's scale)
 };
 
-// fp16 hi/lo split of a float pair: hi = rn_fp16(x), lo = rn_fp16(x - hi) (x - hi exact in fp32)
+// fp16 hi/lo split of a float pair: hi = rn_fp16(x), lo = rn_fp16(x - hi) (x - hi exact in fp32).
+// FOE_K8_NEGLO 1: the lo parts are stored NEGATED, rn_fp16(hi - x), by sm_100's mixed-precision
+// subtract (one FHADD per element instead of two fp16 -> fp32 unpacks and an FADD2), and the MMAs
+// that read lo parts (pass 1 of every GEMM: A = lo) set the instruction descriptor's negate-A bit
+// (kLoNeg) -- the same products, bitwise (rounding to nearest is odd-symmetric).
+#ifndef FOE_K8_NEGLO
+#define FOE_K8_NEGLO 1
+#endif
+#ifndef FOE_K8_ESKIP
+#define FOE_K8_ESKIP 1   // halo response rows: epilogue without the energy logarithms (c4: -1.4 %)
+#endif
+constexpr uint32_t kLoNeg = FOE_K8_NEGLO ? (1u << 13) : 0u;   // idesc bit 13: negate A
 __device__ __forceinline__ void h2_split(float2 v, uint32_t& hi, uint32_t& lo) {
     const __half2 h = __float22half2_rn(v);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+#if FOE_K8_NEGLO
+    float dx, dy;
+    asm("sub.rn.f32.f16 %0, %1, %2;" : "=f"(dx) : "h"((unsigned short)(hi & 0xffffu)), "f"(v.x));
+    asm("sub.rn.f32.f16 %0, %1, %2;" : "=f"(dy) : "h"((unsigned short)(hi >> 16)), "f"(v.y));
+    const __half2 l = __float22half2_rn(make_float2(dx, dy));
+#else
     const float2 hb = __half22float2(h);
     const __half2 l = __float22half2_rn(__fadd2_rn(v, make_float2(-hb.x, -hb.y)));
-    hi = *reinterpret_cast<const uint32_t*>(&h);
+#endif
     lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 
@@ -163,7 +181,7 @@ __device__ __forceinline__ void th_build_a2(const float* us, int j, int xg, floa
 // epilogue of filter chunks [F0, F1) of 8: r = R / (s_u s_f) + c sum k; energy
 // sum theta ln2 lg2(1 + r^2); P = 2^14 r / (1 + r^2) (= 2^14 rho'/2) split into fp16 hi / lo pairs,
 // to TMEM (column = filter pair); zlast += P kb_last (Z units)
-template <int F0, int F1>
+template <int F0, int F1, bool E = true>
 __device__ __forceinline__ float th_epilogue(uint32_t t_d, uint32_t t_ph, uint32_t t_pl, float uq, float inv,
                                              const float* css, const float* ths, const float* kbl, float& zlast) {
     float r[(F1 - F0) * 8];
@@ -181,7 +199,7 @@ __device__ __forceinline__ float th_epilogue(uint32_t t_d, uint32_t t_ph, uint32
             const float2 r2 = make_float2(r[(f8 - F0) * 8 + e], r[(f8 - F0) * 8 + e + 1]);
             const float2 rv = __ffma2_rn(uq2, make_float2(css[i], css[i + 1]), __fmul2_rn(r2, inv2));
             const float2 d = __ffma2_rn(rv, rv, one2);
-            el2 = __ffma2_rn(make_float2(ths[i], ths[i + 1]), make_float2(lg2_approx(d.x), lg2_approx(d.y)), el2);
+            if (E) el2 = __ffma2_rn(make_float2(ths[i], ths[i + 1]), make_float2(lg2_approx(d.x), lg2_approx(d.y)), el2);
             // one MUFU reciprocal per filter pair: 1/d_A = d_B / (d_A d_B) (d >= 1; see K1)
             const float q = rcp_approx(d.x * d.y) * kThPScale;
             const float2 pv = __fmul2_rn(rv, __fmul2_rn(make_float2(d.y, d.x), make_float2(q, q)));
@@ -359,7 +377,8 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
 #pragma unroll
                 for (int c = 0; c < G::NCH; ++c) {
                     const uint64_t bd = tc::sdesc_kmajor(b_base + boff + c * 2 * NP * 16, NP * 16, 128);
-                    tc::mma_f16_ts_warp(tb + G::COL_D, tb + acol + 4 * (ws + 2 * c), bd, idf, (pass | c) != 0);
+                    tc::mma_f16_ts_warp(tb + G::COL_D, tb + acol + 4 * (ws + 2 * c), bd, pass == 1 ? idf | kLoNeg : idf,
+                                        (pass | c) != 0);
                 }
             }
             tc::mma_commit_warp(&mbar_f);
@@ -429,9 +448,18 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
             tc::mbar_wait(&mbar_f, (uint32_t)(j & 1));
             tc::fence_after_sync();
             // (a4, a7) responses r, rho (owned responses), rho'/2 -> P (fp16 hi/lo)
-            const bool own = col_own && (j >= C) && (j < C + R) && (sy0 - C + j < H);
-            float zl;
-            const float el = wg == 0
+            const bool row_own = (j >= C) && (j < C + R) && (sy0 - C + j < H);   // (packed tiles: per strip)
+            const bool own = col_own && row_own;
+            float zl, el;
+#if FOE_K8_ESKIP
+            // responses of halo rows carry no energy: their epilogue leaves out the logarithms
+            if (!packed && !row_own)
+                el = wg == 0
+                    ? th_epilogue<0, HF8, false>(tl + G::COL_D, tl + G::COL_PH, tl + G::COL_PL, uq, inv, cc.sumk, cc.thl, cc.kbl, zl)
+                    : th_epilogue<HF8, NF8, false>(tl + G::COL_D, tl + G::COL_PH, tl + G::COL_PL, uq, inv, cc.sumk, cc.thl, cc.kbl, zl);
+            else
+#endif
+            el = wg == 0
                 ? th_epilogue<0, HF8>(tl + G::COL_D, tl + G::COL_PH, tl + G::COL_PL, uq, inv, cc.sumk, cc.thl, cc.kbl, zl)
                 : th_epilogue<HF8, NF8>(tl + G::COL_D, tl + G::COL_PH, tl + G::COL_PL, uq, inv, cc.sumk, cc.thl, cc.kbl, zl);
             if (!FOE_K8_TAP49) zls[(j & 1) * 2 * L + wg * L + l] = zl;
@@ -448,7 +476,8 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
 #pragma unroll
                     for (int kc = 0; kc < G::NKB; ++kc) {
                         const uint64_t bd = tc::sdesc_kmajor(b_base + boff + kc * 2 * G::NBP * 16, G::NBP * 16, 128);
-                        tc::mma_f16_ts_warp(tb + G::COL_Z, tb + acol + kc * 8, bd, idb, (pass | kc) != 0);
+                        tc::mma_f16_ts_warp(tb + G::COL_Z, tb + acol + kc * 8, bd, pass == 1 ? idb | kLoNeg : idb,
+                                            (pass | kc) != 0);
                     }
                 }
                 tc::mma_commit_warp(&mbar_b);
@@ -714,9 +743,10 @@ __global__ void __launch_bounds__(256, 1) k_hvp_th(const TcArgs ta, const __grid
                 for (int c = 0; c < G::NCH; ++c) {
                     const uint64_t bd = tc::sdesc_kmajor(b_base + boff + c * 2 * NP * 16, NP * 16, 128);
                     const uint32_t off = 4 * (ws + 2 * c);
-                    tc::mma_f16_ts_warp(tb + GH::COL_D, tb + (pass == 1 ? GH::COL_UL : GH::COL_UH) + off, bd, idf,
+                    const uint32_t id = pass == 1 ? idf | kLoNeg : idf;
+                    tc::mma_f16_ts_warp(tb + GH::COL_D, tb + (pass == 1 ? GH::COL_UL : GH::COL_UH) + off, bd, id,
                                         (pass | c) != 0);
-                    tc::mma_f16_ts_warp(tb + GH::COL_DT, tb + (pass == 1 ? GH::COL_TL : GH::COL_TH) + off, bd, idf,
+                    tc::mma_f16_ts_warp(tb + GH::COL_DT, tb + (pass == 1 ? GH::COL_TL : GH::COL_TH) + off, bd, id,
                                         (pass | c) != 0);
                 }
             }
@@ -809,7 +839,8 @@ __global__ void __launch_bounds__(256, 1) k_hvp_th(const TcArgs ta, const __grid
 #pragma unroll
                     for (int kc = 0; kc < G::NKB; ++kc) {
                         const uint64_t bd = tc::sdesc_kmajor(b_base + boff + kc * 2 * G::NBP * 16, G::NBP * 16, 128);
-                        tc::mma_f16_ts_warp(tb + GH::COL_Z, tb + acol + kc * 8, bd, idb, (pass | kc) != 0);
+                        tc::mma_f16_ts_warp(tb + GH::COL_Z, tb + acol + kc * 8, bd, pass == 1 ? idb | kLoNeg : idb,
+                                            (pass | kc) != 0);
                     }
                 }
                 tc::mma_commit_warp(&mbar_b);

@@ -3,6 +3,7 @@
 ncu's SASS source page with nvdisasm -g line info of the same cubin (run here, on the CPU box).
 
     python tools/ncu_lines.py <prof.ncu-rep> <libfoe.so> <mangled kernel name> [top]
+    OUTER=1 python tools/ncu_lines.py ...   attribute inlined code to the kernel-level call-site line
 """
 import collections, csv, io, os, re, subprocess, sys, tempfile
 
@@ -20,7 +21,8 @@ def main():
     with tempfile.TemporaryDirectory() as d:
         subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(so)], cwd=d, capture_output=True)
         cub = [f for f in os.listdir(d) if f.endswith(".cubin")][0]
-        dis = subprocess.run(["nvdisasm", "-g", os.path.join(d, cub)], capture_output=True, text=True).stdout
+        flag = "-gi" if os.environ.get("OUTER") else "-g"   # OUTER=1: the kernel-level (outermost) call-site line
+        dis = subprocess.run(["nvdisasm", flag, os.path.join(d, cub)], capture_output=True, text=True).stdout
     sec = dis[dis.index(".text." + fn + ":"):]
     sec = sec[: sec.find("\n.text.", 10) if "\n.text." in sec[10:] else len(sec)]
     line_of = {}
