@@ -270,7 +270,8 @@ foe_status build_th_images(foe_model* md) {
             }
             kf[(size_t)k * NP + i] = v;
         }
-        for (int t = 0; t < NB; ++t) kb[(size_t)i * NBP + t] = (double)md->tp->bwd[(size_t)i * TAPS + t];
+        for (int t = 0; t < NB; ++t)   // column = the tap's Z column (foe::th_zcol: col2im read order)
+            kb[(size_t)i * NBP + foe::th_zcol(m, t / m, t % m)] = (double)md->tp->bwd[(size_t)i * TAPS + t];
     }
     auto scale_of = [](const std::vector<double>& v) {
         double mx = 0.0;

@@ -116,15 +116,4 @@ __device__ __forceinline__ void tc_stage_u_packed(float* us, const double* w, in
     }
 }
 
-// Z chunks [C0, C1) of 8 taps -> zs[tap][lane]
-template <int L, int C0, int C1>
-__device__ __forceinline__ void tc_z_to_smem(uint32_t t_z, float* zs, int l) {
-    float z[(C1 - C0) * 8];
-#pragma unroll
-    for (int c8 = C0; c8 < C1; ++c8) tc::tmem_ld8(t_z + c8 * 8, *reinterpret_cast<float(*)[8]>(z + (c8 - C0) * 8));
-    tc::wait_ld();
-#pragma unroll
-    for (int k = 0; k < (C1 - C0) * 8; ++k) zs[(C0 * 8 + k) * L + l] = z[k];
-}
-
 }  // namespace foe

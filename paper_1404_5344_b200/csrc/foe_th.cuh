@@ -54,6 +54,33 @@ namespace foe {
 constexpr float kThPScale = FOE_K8_PSCALE ? 16384.0f : 1.0f;
 // taps of the backward GEMM on the tensor core (host and device)
 __host__ __device__ constexpr int th_nb(int m) { return FOE_K8_TAP49 ? m * m : (m * m / 8) * 8; }
+// Z column (backward GEMM N index, = the Kb image's column) of tap (a, b): grouped by the col2im's
+// kernel rows so that its reads are 8-byte pairs -- warp group 0's rows a < C + 1 as pairs
+// (a, a + 1) then a single row, warp group 1's rows as pairs then singles; inside a pair group
+// column = base + 2 b + (a - a0), inside a single row base + b.  The last tap (m-1, m-1) comes last
+// (column m^2 - 1 >= NB: on CUDA cores unless FOE_K8_TAP49).
+__host__ __device__ constexpr int th_zcol(int m, int a, int b) {
+    const int C = (m - 1) / 2, A0 = C + 1, A1 = m - A0, NPR = (A1 - 1) / 2;
+    int n = 0;
+    for (int a0 = 0; a0 + 1 < A0; a0 += 2) {
+        if (a == a0 || a == a0 + 1) return n + 2 * b + (a - a0);
+        n += 2 * m;
+    }
+    if (A0 % 2 == 1) {
+        if (a == A0 - 1) return n + b;
+        n += m;
+    }
+    for (int q = 0; q < NPR; ++q) {
+        const int a0 = A0 + 2 * q;
+        if (a == a0 || a == a0 + 1) return n + 2 * b + (a - a0);
+        n += 2 * m;
+    }
+    for (int a1 = A0 + 2 * NPR; a1 < m; ++a1) {
+        if (a == a1) return n + b;
+        n += m;
+    }
+    return -1;
+}
 
 template <int M, int NP, int R>
 struct ThGeom {
@@ -81,19 +108,22 @@ struct ThGeom {
     static constexpr int BF_BYTES = NCH * 16 * NP * 2;
     static constexpr int BB_BYTES = NKB * 16 * NBP * 2;
     static constexpr int B_BYTES = 2 * BF_BYTES + 2 * BB_BYTES;
-    // shared memory (bytes): B images | u tile | Z transpose [NB][LANES] | col2im hand-off ring
+    // shared memory (bytes): B images | u tile | Z [LANES + 8][ZP] | col2im hand-off ring
     // [8][LANES] | last-tap partials [2 rows][2 groups][LANES] | tile max per warp
     static constexpr int SM_B = 0;
     static constexpr int SM_U = SM_B + B_BYTES;
     static constexpr int SM_Z = SM_U + UY * UP * 4;
     static constexpr int NZ8 = (NB + 7) / 8;            // Z read-out chunks of 8 taps
-    static constexpr int SM_HAND = SM_Z + NZ8 * 8 * LANES * 4;
+    static constexpr int ZP = NB + 2;                   // Z pitch (floats): zs[lane][column], ZP/2 odd
+    static constexpr int SM_HAND = SM_Z + (LANES + 8) * ZP * 4;   // (+8 lanes: reads at l + b past 127)
     static constexpr int SM_ZL = SM_HAND + 8 * LANES * 4;
     static constexpr int SMEM_BYTES = SM_ZL + 4 * LANES * 4 + 64;
     static_assert(NP % 16 == 0 && NBP <= ND, "MMA shapes");
     static_assert(TAPS - NB <= 1, "at most one CUDA-core tap");
     static_assert(TCOLS_USED <= 256, "TMEM budget: two CTAs per SM");
     static_assert(B_BYTES % 16 == 0 && SM_U % 16 == 0, "B images: one TMA bulk copy");
+    static_assert(NB % 8 == 0 && (ZP / 2) % 2 == 1 && SM_HAND % 16 == 0, "Z layout: conflict-free 8-byte accesses");
+    static_assert(th_zcol(M, M - 1, M - 1) == TAPS - 1, "Z columns: the last tap last");
 };
 
 // Per-filter epilogue constants of K8, in the kernel-parameter constant bank (FFMA operands
@@ -211,6 +241,80 @@ __device__ __forceinline__ float th_epilogue(uint32_t t_d, uint32_t t_ph, uint32
     }
     zlast = zl2.x + zl2.y;
     return el2.x + el2.y;
+}
+
+// This thread's Z columns [8 C0, 8 C1) (its lane) -> zs[l][.] by 8-byte stores
+template <int ZP, int C0, int C1>
+__device__ __forceinline__ void th_z_to_smem(uint32_t t_z, float* zs, int l) {
+    float z[(C1 - C0) * 8];
+#pragma unroll
+    for (int c8 = C0; c8 < C1; ++c8) tc::tmem_ld8(t_z + c8 * 8, *reinterpret_cast<float(*)[8]>(z + (c8 - C0) * 8));
+    tc::wait_ld();
+    float2* row = reinterpret_cast<float2*>(zs + l * ZP + C0 * 8);
+#pragma unroll
+    for (int k = 0; k < (C1 - C0) * 4; ++k) row[k] = make_float2(z[2 * k], z[2 * k + 1]);
+}
+
+// (a5) col2im of Z row jz: Z row jz feeds output rows o = jz - a at column l,
+//   s[o][l] += sum_b Z[(jz, l + b), (a, b)];
+// warp group 0 sums kernel rows a < A0 = C + 1 (acc[k]: row jz - k; its share of row jz - C goes to
+// the hand-off ring), warp group 1 rows a >= A0 plus the CUDA-core last tap from zl (acc[k]: row
+// jz - A0 - k).  Returns (warp group 1) the complete sum of output row o = jz - 2C (o >= 0 only).
+template <int M, int NB, int ZP>
+__device__ __forceinline__ float th_col2im(const float* zs, const float* zl, float* hand, int l, int jz, int wg,
+                                           float* acc) {
+    constexpr int C = (M - 1) / 2, A0 = C + 1, A1 = M - A0, L = 128;
+    const float* zr = zs + l * ZP;
+    if (wg == 0) {
+#pragma unroll
+        for (int a = 0; a + 1 < A0; a += 2) {
+            float2 sa = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int bb = 0; bb < M; ++bb)
+                sa = __fadd2_rn(sa, *reinterpret_cast<const float2*>(zr + bb * ZP + th_zcol(M, a, bb)));
+            acc[a] += sa.x;
+            acc[a + 1] += sa.y;
+        }
+        if constexpr (A0 % 2 == 1) {
+            float sa = 0.f;
+#pragma unroll
+            for (int bb = 0; bb < M; ++bb) sa += zr[bb * ZP + th_zcol(M, A0 - 1, bb)];
+            acc[A0 - 1] += sa;
+        }
+        const int o = jz - (A0 - 1);                    // wg0's share of row o is complete
+        if (o >= 0) hand[(o & 7) * L + l] = acc[A0 - 1];
+#pragma unroll
+        for (int k = A0 - 1; k > 0; --k) acc[k] = acc[k - 1];
+        acc[0] = 0.f;
+        return 0.f;
+    } else {
+        constexpr int NPR = (A1 - 1) / 2;
+#pragma unroll
+        for (int q = 0; q < NPR; ++q) {
+            const int a = A0 + 2 * q;
+            float2 sa = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int bb = 0; bb < M; ++bb)
+                sa = __fadd2_rn(sa, *reinterpret_cast<const float2*>(zr + bb * ZP + th_zcol(M, a, bb)));
+            acc[2 * q] += sa.x;
+            acc[2 * q + 1] += sa.y;
+        }
+#pragma unroll
+        for (int k = 2 * NPR; k < A1; ++k) {
+            const int a = A0 + k;
+            float sa = 0.f;
+#pragma unroll
+            for (int bb = 0; bb < M; ++bb)
+                sa += th_zcol(M, a, bb) < NB ? zr[bb * ZP + th_zcol(M, a, bb)] : zl[l + bb] + zl[L + l + bb];
+            acc[k] += sa;
+        }
+        const int o = jz - 2 * C;
+        const float s_tot = o >= 0 ? acc[A1 - 1] + hand[(o & 7) * L + l] : 0.f;
+#pragma unroll
+        for (int k = A1 - 1; k > 0; --k) acc[k] = acc[k - 1];
+        acc[0] = 0.f;
+        return s_tot;
+    }
 }
 
 template <int M, int NP, int R>
@@ -361,8 +465,8 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
         if (j > 0) {
             tc::mbar_wait(&mbar_b, (uint32_t)((j - 1) & 1));
             tc::fence_after_sync();
-            if (wg == 0) tc_z_to_smem<L, 0, HZ8>(tl + G::COL_Z, zs, l);
-            else tc_z_to_smem<L, HZ8, NZ8>(tl + G::COL_Z, zs, l);
+            if (wg == 0) th_z_to_smem<G::ZP, 0, HZ8>(tl + G::COL_Z, zs, l);
+            else th_z_to_smem<G::ZP, HZ8, NZ8>(tl + G::COL_Z, zs, l);
         }
         tc::wait_st();
         tc::fence_before_sync();
@@ -384,64 +488,13 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
             tc::mma_commit_warp(&mbar_f);
         }
         if (j > 0) {
-            // col2im of row jz = j - 1: Z row jz feeds output rows o = jz - a at column ox = l:
-            //   s[o][ox] += sum_b Z[(jz, ox + b), (a, b)];  acc[k] holds row jz - (a0 + k)
             const int jz = j - 1;
-            if (wg == 0) {
-#pragma unroll
-                for (int a = 0; a + 1 < A0; a += 2) {
-                    float2 sa = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int bb = 0; bb < M; ++bb)
-                        sa = __fadd2_rn(sa, make_float2(zs[(a * M + bb) * L + l + bb], zs[((a + 1) * M + bb) * L + l + bb]));
-                    acc[a] += sa.x;
-                    acc[a + 1] += sa.y;
-                }
-                if constexpr (A0 % 2 == 1) {
-                    float sa = 0.f;
-#pragma unroll
-                    for (int bb = 0; bb < M; ++bb) sa += zs[((A0 - 1) * M + bb) * L + l + bb];
-                    acc[A0 - 1] += sa;
-                }
-                const int o = jz - (A0 - 1);                    // wg0's share of row o is complete
-                if (o >= 0) hand[(o & 7) * L + l] = acc[A0 - 1];
-#pragma unroll
-                for (int k = A0 - 1; k > 0; --k) acc[k] = acc[k - 1];
-                acc[0] = 0.f;
-            } else {
-                const float* zl = zls + (jz & 1) * 2 * L;
-                constexpr int NPR = (A1 - 1) / 2;
-#pragma unroll
-                for (int q = 0; q < NPR; ++q) {
-                    const int a = A0 + 2 * q;
-                    float2 sa = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int bb = 0; bb < M; ++bb)
-                        sa = __fadd2_rn(sa, make_float2(zs[(a * M + bb) * L + l + bb], zs[((a + 1) * M + bb) * L + l + bb]));
-                    acc[2 * q] += sa.x;
-                    acc[2 * q + 1] += sa.y;
-                }
-#pragma unroll
-                for (int k = 2 * NPR; k < A1; ++k) {
-                    const int a = A0 + k;
-                    float sa = 0.f;
-#pragma unroll
-                    for (int bb = 0; bb < M; ++bb) {
-                        const int tap = a * M + bb;
-                        sa += tap < G::NB ? zs[tap * L + l + bb] : zl[l + bb] + zl[L + l + bb];
-                    }
-                    acc[k] += sa;
-                }
-                // (a6) row o = jz - 2C is complete: g = u (.) s, s = (Z-unit sum) / (s_b 2^14)
-                const int o = jz - 2 * C;
-                if (o >= 0 && o < R && out_col && sy0 + o < H) {
-                    const float s_tot = acc[A1 - 1] + hand[(o & 7) * L + l];
-                    const float u = udom ? 1.0f : us[(o + 2 * C) * G::UP + l + 2 * C] + cst;   // W = diag(e^w)
-                    gout[(size_t)(sy0 + o) * W + x0 + ocol] = (u * cc.inv_z) * s_tot;
-                }
-#pragma unroll
-                for (int k = A1 - 1; k > 0; --k) acc[k] = acc[k - 1];
-                acc[0] = 0.f;
+            const float s_tot = th_col2im<M, G::NB, G::ZP>(zs, zls + (jz & 1) * 2 * L, hand, l, jz, wg, acc);
+            // (a6) row o = jz - 2C is complete: g = u (.) s, s = (Z-unit sum) / (s_b 2^14)
+            const int o = jz - 2 * C;
+            if (wg == 1 && o >= 0 && o < R && out_col && sy0 + o < H) {
+                const float u = udom ? 1.0f : us[(o + 2 * C) * G::UP + l + 2 * C] + cst;   // W = diag(e^w)
+                gout[(size_t)(sy0 + o) * W + x0 + ocol] = (u * cc.inv_z) * s_tot;
             }
         }
         if (j < G::RR) {
@@ -728,8 +781,8 @@ __global__ void __launch_bounds__(256, 1) k_hvp_th(const TcArgs ta, const __grid
         if (j > 0) {
             tc::mbar_wait(&mbar_b, (uint32_t)((j - 1) & 1));
             tc::fence_after_sync();
-            if (wg == 0) tc_z_to_smem<L, 0, HZ8>(tl + GH::COL_Z, zs, l);
-            else tc_z_to_smem<L, HZ8, NZ8>(tl + GH::COL_Z, zs, l);
+            if (wg == 0) th_z_to_smem<G::ZP, 0, HZ8>(tl + GH::COL_Z, zs, l);
+            else th_z_to_smem<G::ZP, HZ8, NZ8>(tl + GH::COL_Z, zs, l);
         }
         tc::wait_st();
         tc::fence_before_sync();
@@ -754,66 +807,18 @@ __global__ void __launch_bounds__(256, 1) k_hvp_th(const TcArgs ta, const __grid
         }
         if (j > 0) {
             const int jz = j - 1;
-            if (wg == 0) {
-#pragma unroll
-                for (int a = 0; a + 1 < A0; a += 2) {
-                    float2 sa = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int bb = 0; bb < M; ++bb)
-                        sa = __fadd2_rn(sa, make_float2(zs[(a * M + bb) * L + l + bb], zs[((a + 1) * M + bb) * L + l + bb]));
-                    acc[a] += sa.x;
-                    acc[a + 1] += sa.y;
+            const float s_sum = th_col2im<M, G::NB, G::ZP>(zs, zls + (jz & 1) * 2 * L, hand, l, jz, wg, acc);
+            const int o = jz - 2 * C;
+            if (wg == 1 && o >= 0 && o < R && out_col && y0 + o < H) {
+                const float s_tot = s_sum * inv_zt;
+                const size_t gi = (size_t)(y0 + o) * W + x0 + l;
+                float val;
+                if (udom) val = s_tot;
+                else {
+                    const float u = us[(o + 2 * C) * G::UP + l + 2 * C] + cst;
+                    val = (float)(vv[gi] * (double)args.gw[(size_t)b * HW + gi] + (double)(u * s_tot));
                 }
-                if constexpr (A0 % 2 == 1) {
-                    float sa = 0.f;
-#pragma unroll
-                    for (int bb = 0; bb < M; ++bb) sa += zs[((A0 - 1) * M + bb) * L + l + bb];
-                    acc[A0 - 1] += sa;
-                }
-                const int o = jz - (A0 - 1);
-                if (o >= 0) hand[(o & 7) * L + l] = acc[A0 - 1];
-#pragma unroll
-                for (int k = A0 - 1; k > 0; --k) acc[k] = acc[k - 1];
-                acc[0] = 0.f;
-            } else {
-                const float* zl = zls + (jz & 1) * 2 * L;
-                constexpr int NPR = (A1 - 1) / 2;
-#pragma unroll
-                for (int q = 0; q < NPR; ++q) {
-                    const int a = A0 + 2 * q;
-                    float2 sa = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int bb = 0; bb < M; ++bb)
-                        sa = __fadd2_rn(sa, make_float2(zs[(a * M + bb) * L + l + bb], zs[((a + 1) * M + bb) * L + l + bb]));
-                    acc[2 * q] += sa.x;
-                    acc[2 * q + 1] += sa.y;
-                }
-#pragma unroll
-                for (int k = 2 * NPR; k < A1; ++k) {
-                    const int a = A0 + k;
-                    float sa = 0.f;
-#pragma unroll
-                    for (int bb = 0; bb < M; ++bb) {
-                        const int tap = a * M + bb;
-                        sa += tap < G::NB ? zs[tap * L + l + bb] : zl[l + bb] + zl[L + l + bb];
-                    }
-                    acc[k] += sa;
-                }
-                const int o = jz - 2 * C;
-                if (o >= 0 && o < R && out_col && y0 + o < H) {
-                    const float s_tot = (acc[A1 - 1] + hand[(o & 7) * L + l]) * inv_zt;
-                    const size_t gi = (size_t)(y0 + o) * W + x0 + l;
-                    float val;
-                    if (udom) val = s_tot;
-                    else {
-                        const float u = us[(o + 2 * C) * G::UP + l + 2 * C] + cst;
-                        val = (float)(vv[gi] * (double)args.gw[(size_t)b * HW + gi] + (double)(u * s_tot));
-                    }
-                    gout[gi] = val;
-                }
-#pragma unroll
-                for (int k = A1 - 1; k > 0; --k) acc[k] = acc[k - 1];
-                acc[0] = 0.f;
+                gout[gi] = val;
             }
         }
         if (j < G::RR) {
