@@ -163,6 +163,8 @@ typedef struct {
                                 per tile (partial gradients summed in fixed order)                    */
     int stencil;             /* prior energy+gradient kernel: FOE_STENCIL_AUTO / _FFMA / _TENSOR     */
     int solver;              /* trial-loop driver: FOE_SOLVER_AUTO / _GRAPH / _PERSISTENT (below)    */
+    int tile_rows;           /* tensor-core stencil output rows per tile: 0 = automatic (fewest waves
+                                x rows), else one of 4, 8, 16, 32, 64; batch path only (slabs: 64) */
 } ipiano_config;
 
 /* Trial-loop drivers.  Both run the same K2 -> K1 -> K3 round per trial

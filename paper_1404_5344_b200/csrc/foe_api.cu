@@ -522,7 +522,7 @@ struct Plan {
     int ncp = kNCP, nchunks = 0;  // K1: filter pairs per chunk, chunks
 };
 Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref, int req_groups,
-                  bool allow_pack = true) {
+                  bool allow_pack = true, int req_rows = 0) {
     Plan p;
     const int ow = 128 - (md->m - 1);
     const bool pack_ok = allow_pack && H_grid == H;
@@ -547,7 +547,9 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
     // fewest (waves of 2 CTAs per SM) x (response rows + ~8 rows of prologue) -- c3 (512^2): R = 8,
     // 278 CTAs instead of 35.  Row slabs keep R = 64 (their bands).
     int bestR = kTcR;
-    if (pack_ok) {
+    if (pack_ok && req_rows > 0) {
+        bestR = req_rows;
+    } else if (pack_ok) {
         double best = 1e30;
         for (int R : {64, 32, 16, 8, 4}) {
             Plan q;
@@ -905,6 +907,7 @@ void ipiano_config_default(ipiano_config* c) {
     c->filter_groups = 0;
     c->stencil = FOE_STENCIL_AUTO;
     c->solver = FOE_SOLVER_AUTO;
+    c->tile_rows = 0;
 }
 
 }  // extern "C"
@@ -1309,13 +1312,18 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
         delete st;
         return fail(FOE_ERR_UNSUPPORTED, "the persistent solver runs the FFMA stencil only");
     }
+    if (cfg.tile_rows != 0 && cfg.tile_rows != 4 && cfg.tile_rows != 8 && cfg.tile_rows != 16 && cfg.tile_rows != 32 &&
+        cfg.tile_rows != 64) {
+        delete st;
+        return fail(FOE_ERR_INVALID_ARGUMENT, "tile_rows %d is not 0, 4, 8, 16, 32 or 64", cfg.tile_rows);
+    }
     // trial-loop driver (f4): persistent for problems that cannot fill the GPU
     const long long npx = (long long)B * H * W;
     const bool want_persist = cfg.solver == FOE_SOLVER_PERSISTENT ||
                               (cfg.solver == FOE_SOLVER_AUTO && cfg.stencil != FOE_STENCIL_TENSOR &&
                                (npx < (1LL << 16) || (md->tc_np == 0 && npx <= (1LL << 18))));
     const int pref = want_persist ? FOE_STENCIL_FFMA : cfg.stencil;
-    const Plan pl = plan_stencil(md, B, H, W, H, pref, cfg.filter_groups, !t_slab_member);
+    const Plan pl = plan_stencil(md, B, H, W, H, pref, cfg.filter_groups, !t_slab_member, cfg.tile_rows);
     st->kind = pl.kind;
     st->tiles_x = pl.tiles_x;
     st->tc_rem = pl.tc_rem;

@@ -51,7 +51,7 @@ class IPianoConfig(C.Structure):
         ("shrink", C.c_double), ("max_iters", C.c_int), ("max_backtracks", C.c_int),
         ("newton_max_iters", C.c_int), ("newton_tol", C.c_double), ("rel_change_tol", C.c_double),
         ("w_guard", C.c_double), ("record_trace", C.c_int), ("filter_groups", C.c_int),
-        ("stencil", C.c_int), ("solver", C.c_int),
+        ("stencil", C.c_int), ("solver", C.c_int), ("tile_rows", C.c_int),
     ]
 
 

@@ -166,3 +166,41 @@ def test_tc_slabs_bitwise_g_invariant():
         np.testing.assert_array_equal(tr, outs[0][1])
     ref = oracle.ipiano_run(f, k, th, 160.0, 0.004, oracle.make_cfg(2.0 ** 18, 15))
     assert rel_l2(np.exp(outs[0][0]), ref["u"]) <= 1e-4
+
+
+@pytest.mark.parametrize("rows", [8, 32])
+@pytest.mark.parametrize("B,H,W", [(2, 300, 260), (1, 520, 512)])
+def test_tc_tile_rows_P3(rows, B, H, W):
+    """K8 with forced tile heights (ipiano_config.tile_rows) against the oracle on batch shapes: a
+    last band shorter than the tile, ragged and packed remainder columns (W = 512: the 24 remainder
+    columns of several bands share one tile), every image of a batch.  P3 bars (final image rel L2
+    <= 1e-4, |dPSNR| <= 0.01 dB, identical L_n / trials, H trace to 1e-6) over 30 iterations."""
+    cfg, d, L0 = _setup("c4", B=B, H=H, W=W, iters=30)
+    md = P.foe_model_create(d["filters"], d["theta"], lam=tuple(d["lambdas"][0]))
+    c = P.ipiano_config_default(max_iters=cfg.iters, stencil=TENSOR, tile_rows=rows)
+    st = P.ipiano_state_create(md, _cuda(d["f"], torch.float32), d["lambdas"], L0, c)
+    P.ipiano_solve(st)
+    _, u = P.ipiano_get_iterate(st)
+    u = u.cpu().numpy()
+    tr = P.ipiano_get_trace(st)
+    cnt = P.ipiano_get_counters(st)
+    for b in range(B):
+        assert cnt["status"][b] == 0 and cnt["iters"][b] == cfg.iters
+        l1, l2 = d["lambdas"][b]
+        ref = oracle.ipiano_run(d["f"][b], d["filters"], d["theta"], l1, l2, oracle.make_cfg(L0[b], cfg.iters))
+        assert ref["status"] == 0
+        assert rel_l2(u[b], ref["u"]) <= 1e-4, (b, rel_l2(u[b], ref["u"]))
+        clean = d["clean"][b]
+        assert abs(oracle.psnr(u[b], clean) - oracle.psnr(ref["u"], clean)) <= 0.01
+        np.testing.assert_array_equal(tr[b, 1:, 3], ref["trace"][1:, 3])
+        np.testing.assert_array_equal(tr[b, 1:, 4], ref["trace"][1:, 4])
+        np.testing.assert_allclose(tr[b, :, 2], ref["trace"][:, 2], rtol=1e-6)
+
+
+def test_tc_tile_rows_invalid():
+    k, th = S.random_filter_bank(48, 7, 5)
+    md = P.foe_model_create(k, th, lam=(310.0, 0.008))
+    f = _cuda(np.full((1, 64, 64), 50.0), torch.float32)
+    with pytest.raises(P.FoeError) as e:
+        P.ipiano_state_create(md, f, None, np.array([1.0]), P.ipiano_config_default(tile_rows=48))
+    assert e.value.status == 1
