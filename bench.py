@@ -57,6 +57,7 @@ def parse_args():
     ap.add_argument("--solver", choices=["auto", "graph", "persistent"], default="auto",
                     help="trial-loop driver (auto: persistent for single small images, SURVEY 8(f) f4)")
     ap.add_argument("--filter-groups", type=int, default=0, help="K1 filter groups per tile (0: automatic)")
+    ap.add_argument("--tile-rows", type=int, default=0, help="K8 output rows per tile (0: automatic)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-p2p", action="store_true", help="c5: ghost rows over ncclSend/Recv instead of K2 peer stores")
     ap.add_argument("--protocol", choices=["none", "fig2"], default="none",
@@ -353,7 +354,7 @@ def main():
     solver = {"auto": P.FOE_SOLVER_AUTO, "graph": P.FOE_SOLVER_GRAPH, "persistent": P.FOE_SOLVER_PERSISTENT}[args.solver]
     stencil = {"auto": P.FOE_STENCIL_AUTO, "ffma": P.FOE_STENCIL_FFMA, "tensor": P.FOE_STENCIL_TENSOR}[args.stencil]
     cfgc = P.ipiano_config_default(max_iters=cfg.iters, record_trace=0, solver=solver, stencil=stencil,
-                                   filter_groups=args.filter_groups)
+                                   filter_groups=args.filter_groups, tile_rows=args.tile_rows)
     st = P.ipiano_state_create(md, f_dev, d["lambdas"], L0, cfgc)
     u_dev = torch.empty((B, H, W), dtype=torch.float32, device=dev)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2

@@ -128,27 +128,30 @@ void k1_dispatch(int m, bool hvp, const K1Args& a, const TapParams& tp, const fo
 // path when the launch fills the GPU), or 32 / 16 for single images that cannot fill 148 SMs with
 // 64-row tiles (plan_stencil)
 constexpr int kTcR = 64;
+// 1: the batch path's K8 tiles compute their own rows' responses only (no row halos; the partial
+// sums of the rows near band edges meet in K2); 0: tiles with row halos (A/B knob)
+#ifndef FOE_K8_NH
+#define FOE_K8_NH 1
+#endif
 template <int M, int NP, int R>
 constexpr int th_smem() { return foe::ThGeom<M, NP, R>::SMEM_BYTES; }
+template <int M, int NP, int R, bool NH>
+cudaError_t th_attr() {
+    return cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, R, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                th_smem<M, NP, R>());
+}
 template <int M, int NP>
 cudaError_t tc_set_attr() {
-    cudaError_t e = cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         th_smem<M, NP, 64>());
+    cudaError_t e = cudaFuncSetAttribute(foe::k_hvp_th<M, NP, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         foe::ThHGeom<M, NP, 64>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             th_smem<M, NP, 32>());
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(foe::k_hvp_th<M, NP, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             foe::ThHGeom<M, NP, 64>::SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             th_smem<M, NP, 16>());
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             th_smem<M, NP, 8>());
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                th_smem<M, NP, 4>());
+    const cudaError_t es[] = {th_attr<M, NP, 64, false>(), th_attr<M, NP, 32, false>(), th_attr<M, NP, 16, false>(),
+                              th_attr<M, NP, 8, false>(),  th_attr<M, NP, 4, false>(),  th_attr<M, NP, 64, true>(),
+                              th_attr<M, NP, 32, true>(),  th_attr<M, NP, 16, true>(),  th_attr<M, NP, 8, true>(),
+                              th_attr<M, NP, 4, true>()};
+    for (cudaError_t x : es)
+        if (x != cudaSuccess) return x;
+    return cudaSuccess;
 }
 // the banks K8 has an instantiation for: (m, padded N_f)
 int tc_np(int m, int nf) {
@@ -226,6 +229,8 @@ struct ipiano_state {
     unsigned long long* phase_ns = nullptr;  // FOE_PERSIST_PHASES=1: CTA 0's phase timestamps
     double* w = nullptr;      // [3][B][HW]
     float* g = nullptr;       // [2][groups][B][HW]
+    float* gedge = nullptr;   // K8 without row halos: [2][B][H / tc_rows][2C][W] band-boundary shares
+    unsigned int* tcnt = nullptr;   // ... and their arrival counters [B][H / tc_rows][tiles_x + 1]
     float* ft = nullptr;      // [B][HW]
     double* epart = nullptr;  // [B][ntiles*groups]
     double* ppart = nullptr;  // [2][B][nblk2][8] (buffer 1: the persistent driver's odd rounds)
@@ -589,6 +594,25 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
     return p;
 }
 
+// K8 launch of tile height R (4 .. 64), with or without row halos (NH), as a programmatic
+// dependent launch (the graph trial rounds) or a plain one
+template <int M, int NP, bool NH, int RR>
+cudaError_t launch_th_r(dim3 grid, cudaStream_t s, const foe::TcArgs& ta, const foe::ThConst& cc, bool pdl) {
+    if (pdl) return launch_pdl(foe::k_prior_grad_th<M, NP, RR, NH>, grid, dim3(256), th_smem<M, NP, RR>(), s, ta, cc);
+    foe::k_prior_grad_th<M, NP, RR, NH><<<grid, 256, th_smem<M, NP, RR>(), s>>>(ta, cc);
+    return cudaGetLastError();
+}
+template <int M, int NP, bool NH>
+cudaError_t launch_th(int R, dim3 grid, cudaStream_t s, const foe::TcArgs& ta, const foe::ThConst& cc, bool pdl) {
+    switch (R) {
+        case 4: return launch_th_r<M, NP, NH, 4>(grid, s, ta, cc, pdl);
+        case 8: return launch_th_r<M, NP, NH, 8>(grid, s, ta, cc, pdl);
+        case 16: return launch_th_r<M, NP, NH, 16>(grid, s, ta, cc, pdl);
+        case 32: return launch_th_r<M, NP, NH, 32>(grid, s, ta, cc, pdl);
+        default: return launch_th_r<M, NP, NH, 64>(grid, s, ta, cc, pdl);
+    }
+}
+
 // Launch the prior energy+gradient evaluation `a` (tiling fields taken from the plan).
 foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStream_t s, int ntiles_grid = -1,
                         bool pdl = false) {
@@ -605,31 +629,14 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
     count_launch(1);
     const dim3 grid(ntiles_grid >= 0 ? ntiles_grid : a.ntiles - a.tile_off, B);
     if (grid.x == 0) return FOE_OK;
-    constexpr int T = 256;
     const int R = a.tc_rows;
-    if (pdl) {   // the batch path's 64-row tiles (graph trial rounds)
-        if (R == 64 && md->tc_np == 48)
-            CK(launch_pdl(foe::k_prior_grad_th<7, 48, 64>, grid, dim3(T), th_smem<7, 48, 64>(), s, ta, *md->th_const));
-        else if (R == 8 && md->tc_np == 48)
-            CK(launch_pdl(foe::k_prior_grad_th<7, 48, 8>, grid, dim3(T), th_smem<7, 48, 8>(), s, ta, *md->th_const));
-        else if (R == 4 && md->tc_np == 48)
-            CK(launch_pdl(foe::k_prior_grad_th<7, 48, 4>, grid, dim3(T), th_smem<7, 48, 4>(), s, ta, *md->th_const));
-        else pdl = false;
-        if (pdl) return FOE_OK;
-    }
-    if (md->tc_np == 48) {
-        if (R == 4) foe::k_prior_grad_th<7, 48, 4><<<grid, T, th_smem<7, 48, 4>(), s>>>(ta, *md->th_const);
-        else if (R == 8) foe::k_prior_grad_th<7, 48, 8><<<grid, T, th_smem<7, 48, 8>(), s>>>(ta, *md->th_const);
-        else if (R == 16) foe::k_prior_grad_th<7, 48, 16><<<grid, T, th_smem<7, 48, 16>(), s>>>(ta, *md->th_const);
-        else if (R == 32) foe::k_prior_grad_th<7, 48, 32><<<grid, T, th_smem<7, 48, 32>(), s>>>(ta, *md->th_const);
-        else foe::k_prior_grad_th<7, 48, 64><<<grid, T, th_smem<7, 48, 64>(), s>>>(ta, *md->th_const);
-    } else {
-        if (R == 4) foe::k_prior_grad_th<5, 32, 4><<<grid, T, th_smem<5, 32, 4>(), s>>>(ta, *md->th_const);
-        else if (R == 8) foe::k_prior_grad_th<5, 32, 8><<<grid, T, th_smem<5, 32, 8>(), s>>>(ta, *md->th_const);
-        else if (R == 16) foe::k_prior_grad_th<5, 32, 16><<<grid, T, th_smem<5, 32, 16>(), s>>>(ta, *md->th_const);
-        else if (R == 32) foe::k_prior_grad_th<5, 32, 32><<<grid, T, th_smem<5, 32, 32>(), s>>>(ta, *md->th_const);
-        else foe::k_prior_grad_th<5, 32, 64><<<grid, T, th_smem<5, 32, 64>(), s>>>(ta, *md->th_const);
-    }
+    const bool nh = a.gedge != nullptr;
+    cudaError_t e;
+    if (md->tc_np == 48) e = nh ? launch_th<7, 48, true>(R, grid, s, ta, *md->th_const, pdl)
+                                : launch_th<7, 48, false>(R, grid, s, ta, *md->th_const, pdl);
+    else e = nh ? launch_th<5, 32, true>(R, grid, s, ta, *md->th_const, pdl)
+                : launch_th<5, 32, false>(R, grid, s, ta, *md->th_const, pdl);
+    CK(e);
     CKL("k_prior_grad_th");
     return FOE_OK;
 }
@@ -949,6 +956,9 @@ K1Args state_k1_args(const ipiano_state* st, int which_cur) {
     a.tc_rem = st->tc_rem;
     a.tc_spt = st->tc_spt;
     a.tc_rows = st->tc_rows;
+    a.gedge = st->gedge;
+    a.gedge_slot_stride = st->gedge ? (size_t)st->B * (st->H / st->tc_rows) * (st->model->m - 1) * st->W : 0;
+    a.tcnt = st->tcnt;
     return a;
 }
 
@@ -1225,7 +1235,7 @@ void ipiano_state_destroy(ipiano_state* st) {
     cudaSetDevice(st->model->dev);
     if (st->s) cudaStreamSynchronize(st->s);
     if (st->graph) cudaGraphExecDestroy(st->graph);
-    cudaFree(st->w); cudaFree(st->g); cudaFree(st->ft); cudaFree(st->epart); cudaFree(st->ppart);
+    cudaFree(st->w); cudaFree(st->g); cudaFree(st->gedge); cudaFree(st->tcnt); cudaFree(st->ft); cudaFree(st->epart); cudaFree(st->ppart);
     if (st->phase_ns) {   // FOE_PERSIST_PHASES diagnostics: mean phase durations of the last launch
         std::vector<unsigned long long> h(4 * foe::kPhaseRounds, 0);
         cudaMemcpy(h.data(), st->phase_ns, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
@@ -1377,6 +1387,15 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     const size_t n = (size_t)B * st->HW;
     CKS(cudaMalloc((void**)&st->w, sizeof(double) * 3 * n));
     CKS(cudaMalloc((void**)&st->g, sizeof(float) * 2 * st->groups * n));
+    // K8 without row halos (foe_th.cuh): the batch path's tensor-core stencil when the bands tile H
+    // and are at least 2C rows tall (a row near a band edge then takes contributions from two bands)
+    if (FOE_K8_NH && st->kind == FOE_STENCIL_TENSOR && !t_slab_member && H % st->tc_rows == 0 &&
+        st->tc_rows >= md->m - 1) {
+        CKS(cudaMalloc((void**)&st->gedge, sizeof(float) * 2 * (size_t)B * (H / st->tc_rows) * (md->m - 1) * W));
+        const size_t nc = (size_t)B * (H / st->tc_rows) * (st->tiles_x + 1);
+        CKS(cudaMalloc((void**)&st->tcnt, sizeof(unsigned int) * nc));
+        CKS(cudaMemset(st->tcnt, 0, sizeof(unsigned int) * nc));
+    }
     CKS(cudaMalloc((void**)&st->ft, sizeof(float) * n));
     CKS(cudaMalloc((void**)&st->epart, sizeof(double) * B * st->ntiles * st->groups));
     CKS(cudaMalloc((void**)&st->ppart, sizeof(double) * 2 * B * st->nblk2 * foe::kNumPart));

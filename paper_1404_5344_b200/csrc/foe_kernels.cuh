@@ -103,6 +103,14 @@ struct K1Args {
     // two boundary bands after it): tile = tile_off + blockIdx.x; energy partials by tile index
     int tile_off;
     int ncp;                // K1 v2: filter pairs per shared-memory chunk (1 or 2; 0 = 2)
+    // K8 without row halos (foe_th.cuh, NH): a tile computes the responses of its own R rows only;
+    // an output row within C of a band start takes contributions from two bands -- the band below
+    // writes its share into g, the band above its share into gedge [slots][B][nb][2C][W] (boundary
+    // t = the lower band, row k = y + C - t R) -- and the second of the two tiles to finish adds
+    // them (a per-boundary arrival counter in tcnt [B][nb][tiles_x + 1], left at 0)
+    float* gedge;
+    size_t gedge_slot_stride;
+    unsigned int* tcnt;
     // HVP only
     const double* v;        // [B][H][W]
     const float* gw;        // [B][H][W] gradient at w

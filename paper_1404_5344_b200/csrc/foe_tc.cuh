@@ -51,7 +51,8 @@ __device__ __forceinline__ float tc_stage_val(double x, bool udom, float cst, do
 // are the same for every row), rows wrap or come from the slab's ghost rows
 template <int UY, int UX, int UP, int NWARPS>
 __device__ __forceinline__ void tc_stage_u(float* us, const double* w, const double* halo, int H, int W, int y0,
-                                           int x0, int c2, bool udom, float cst, double wc, int warp, int lane) {
+                                           int x0, int c2, bool udom, float cst, double wc, int warp, int lane,
+                                           int uy_lo = 0, int uy_hi = UY) {
     constexpr int NX = (UX + 31) / 32;
     const double ec = udom ? 0.0 : exp(wc);
     int gx[NX];
@@ -59,7 +60,7 @@ __device__ __forceinline__ void tc_stage_u(float* us, const double* w, const dou
     for (int k = 0; k < NX; ++k) gx[k] = wrap_idx(x0 - c2 + lane + 32 * k, W);
     // FOE_STAGE_ROWS rows per warp in flight (all their loads issued before any exponential)
     constexpr int NRB = FOE_STAGE_ROWS;
-    for (int uy0 = warp * NRB; uy0 < UY; uy0 += NWARPS * NRB) {
+    for (int uy0 = uy_lo + warp * NRB; uy0 < uy_hi; uy0 += NWARPS * NRB) {
         double v[NRB][NX];
 #pragma unroll
         for (int r = 0; r < NRB; ++r) {
@@ -71,12 +72,12 @@ __device__ __forceinline__ void tc_stage_u(float* us, const double* w, const dou
             else if (y >= H) src = halo + (size_t)(kHalo + y - H) * W;
             else src = w + (size_t)y * W;
 #pragma unroll
-            for (int k = 0; k < NX; ++k) v[r][k] = (uy < UY && lane + 32 * k < UX) ? src[gx[k]] : wc;
+            for (int k = 0; k < NX; ++k) v[r][k] = (uy < uy_hi && lane + 32 * k < UX) ? src[gx[k]] : wc;
         }
 #pragma unroll
         for (int r = 0; r < NRB; ++r) {
             const int uy = uy0 + r;
-            if (uy >= UY) break;
+            if (uy >= uy_hi) break;
 #pragma unroll
             for (int k = 0; k < NX; ++k) {
                 const int ux = lane + 32 * k;
@@ -92,7 +93,7 @@ __device__ __forceinline__ void tc_stage_u(float* us, const double* w, const dou
 template <int UY, int UX, int UP, int NWARPS>
 __device__ __forceinline__ void tc_stage_u_packed(float* us, const double* w, int H, int W, int R, int x0r, int c2,
                                                   int SP, int spt, int band0, int nbands, bool udom, float cst,
-                                                  double wc, int warp, int lane) {
+                                                  double wc, int warp, int lane, int uy_lo = 0, int uy_hi = UY) {
     constexpr int NX = (UX + 31) / 32;
     const double ec = udom ? 0.0 : exp(wc);
     int gx[NX], yb[NX];
@@ -104,7 +105,7 @@ __device__ __forceinline__ void tc_stage_u_packed(float* us, const double* w, in
         gx[k] = wrap_idx(x0r - c2 + (ux - st * SP), W);
         yb[k] = band * R - c2;
     }
-    for (int uy = warp; uy < UY; uy += NWARPS) {
+    for (int uy = uy_lo + warp; uy < uy_hi; uy += NWARPS) {
         double v[NX];
 #pragma unroll
         for (int k = 0; k < NX; ++k) v[k] = ok[k] ? w[(size_t)wrap_idx(yb[k] + uy, H) * W + gx[k]] : wc;

@@ -260,11 +260,30 @@ __device__ __forceinline__ void th_z_to_smem(uint32_t t_z, float* zs, int l) {
 // warp group 0 sums kernel rows a < A0 = C + 1 (acc[k]: row jz - k; its share of row jz - C goes to
 // the hand-off ring), warp group 1 rows a >= A0 plus the CUDA-core last tap from zl (acc[k]: row
 // jz - A0 - k).  Returns (warp group 1) the complete sum of output row o = jz - 2C (o >= 0 only).
-template <int M, int NB, int ZP>
+// NH (tiles without row halos, K1Args::gedge): output rows o >= -C are emitted (the wg0 share of
+// a row o < 0 is zero: its kernel rows a <= C would need Z rows below the first, C); Z0: a drain
+// step with no Z row (the accumulators only roll on).
+template <int M, int NB, int ZP, bool Z0 = false>
 __device__ __forceinline__ float th_col2im(const float* zs, const float* zl, float* hand, int l, int jz, int wg,
-                                           float* acc) {
+                                           float* acc, bool nh = false) {
     constexpr int C = (M - 1) / 2, A0 = C + 1, A1 = M - A0, L = 128;
     const float* zr = zs + l * ZP;
+    if (Z0) {
+        if (wg == 0) {
+            const int o = jz - (A0 - 1);
+            if (o >= 0) hand[(o & 7) * L + l] = acc[A0 - 1];
+#pragma unroll
+            for (int k = A0 - 1; k > 0; --k) acc[k] = acc[k - 1];
+            acc[0] = 0.f;
+            return 0.f;
+        }
+        const int o = jz - 2 * C;
+        const float s_tot = acc[A1 - 1] + (o >= 0 ? hand[(o & 7) * L + l] : 0.f);
+#pragma unroll
+        for (int k = A1 - 1; k > 0; --k) acc[k] = acc[k - 1];
+        acc[0] = 0.f;
+        return s_tot;
+    }
     if (wg == 0) {
 #pragma unroll
         for (int a = 0; a + 1 < A0; a += 2) {
@@ -309,7 +328,7 @@ __device__ __forceinline__ float th_col2im(const float* zs, const float* zl, flo
             acc[k] += sa;
         }
         const int o = jz - 2 * C;
-        const float s_tot = o >= 0 ? acc[A1 - 1] + hand[(o & 7) * L + l] : 0.f;
+        const float s_tot = o >= 0 ? acc[A1 - 1] + hand[(o & 7) * L + l] : (nh ? acc[A1 - 1] : 0.f);
 #pragma unroll
         for (int k = A1 - 1; k > 0; --k) acc[k] = acc[k - 1];
         acc[0] = 0.f;
@@ -317,7 +336,7 @@ __device__ __forceinline__ float th_col2im(const float* zs, const float* zl, flo
     }
 }
 
-template <int M, int NP, int R>
+template <int M, int NP, int R, bool NH = false>
 __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const __grid_constant__ ThConst cc) {
     using G = ThGeom<M, NP, R>;
     constexpr int C = G::C, L = G::LANES, RS = G::RS;
@@ -390,15 +409,21 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
     const bool udom = args.udom != 0;
     const double wc = w[(size_t)yc * W + xc];
     const float cst = (float)(udom ? wc : exp(wc));
-    if (!packed) tc_stage_u<G::UY, G::UX, G::UP, 8>(us, w, args.halo, H, W, y0, x0, 2 * C, udom, cst, wc, warp, t & 31);
+    // NH (no row halos, args.gedge): response rows [C, C + R) only (output rows 0 .. R-1), u rows
+    // [C, R + 3C) staged; else response rows [0, R + 2C), u rows [0, R + 4C)
+    constexpr bool nh = NH;
+    const int j0 = nh ? C : 0, jre = nh ? C + R : G::RR;
+    const int uy_lo = nh ? C : 0, uy_hi = nh ? G::UY - C : G::UY;
+    if (!packed)
+        tc_stage_u<G::UY, G::UX, G::UP, 8>(us, w, args.halo, H, W, y0, x0, 2 * C, udom, cst, wc, warp, t & 31, uy_lo, uy_hi);
     else tc_stage_u_packed<G::UY, G::UX, G::UP, 8>(us, w, H, W, R, x0, 2 * C, SP, args.tc_spt, y0 / R, nbands, udom,
-                                                   cst, wc, warp, t & 31);
+                                                   cst, wc, warp, t & 31, uy_lo, uy_hi);
     tc::fence_before_sync();
     __syncthreads();
     // tile scale s_u = 2^(13 - e), 2^e <= 2 max|u - cst| < 2^(e+1): every U and A2 entry (a
     // difference of two staged values) has magnitude < 2^14 (fp16 max 65504)
     float m = 0.f;
-    for (int y = warp; y < G::UY; y += 8)
+    for (int y = uy_lo + warp; y < uy_hi; y += 8)
         for (int x = t & 31; x < G::UX; x += 32) m = fmaxf(m, fabsf(us[y * G::UP + x]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
@@ -419,7 +444,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
     const int xg = l + C;                                       // u column of the pixel's window centre
     // ring rows 0 .. m-2 (row j + m - 1 is built in iteration j)
 #pragma unroll 1
-    for (int y = 0; y < M - 1; ++y) {
+    for (int y = j0; y < j0 + M - 1; ++y) {
         if (wg == 0) th_build_row<M, G::UP, RS, 0>(us, y, l, xg, su, t_rh, t_rl, y % RS);
         else th_build_row<M, G::UP, RS, 1>(us, y, l, xg, su, t_rh, t_rl, y % RS);
     }
@@ -441,6 +466,30 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
 #pragma unroll
     for (int k = 0; k < (A0 > A1 ? A0 : A1); ++k) acc[k] = 0.f;
     float* gout = args.g + (size_t)gslot * args.g_slot_stride + (size_t)b * HW;
+    // (a6) g = u (.) s of output row o: with row halos rows [0, R) of the band; NH rows [-C, R + C)
+    // (rows within C of a band edge are partial sums): [-C, R - C) into g (row o < 0 wraps to the
+    // bottom of the image), [R - C, R + C) into gedge at the next band's boundary
+    const int nbh = nh ? H / R : 1;
+    float* gedge = nh ? args.gedge + (size_t)gslot * args.gedge_slot_stride + (size_t)b * nbh * (2 * C) * W : nullptr;
+    auto emit = [&](int o, float s_tot) {
+        if (!out_col) return;
+        if (!nh) {
+            if (o < 0 || o >= R || sy0 + o >= H) return;
+        } else if (o < -C || o >= R + C) {
+            return;
+        }
+        const float u = udom ? 1.0f : us[(o + 2 * C) * G::UP + l + 2 * C] + cst;   // W = diag(e^w)
+        const float v = (u * cc.inv_z) * s_tot;    // s = (Z-unit sum) / (s_b 2^14)
+        if (nh && o >= R - C) {
+            int tb = sy0 / R + 1;
+            if (tb >= nbh) tb -= nbh;
+            gedge[((size_t)tb * (2 * C) + (o - R + C)) * W + x0 + ocol] = v;
+        } else {
+            int y = sy0 + o;
+            if (y < 0) y += H;
+            gout[(size_t)y * W + x0 + ocol] = v;
+        }
+    };
 
     // Software pipeline over response rows (iteration j):
     //   ring row j+m-1, A2_j | wait MMAb(j-1), Z(j-1) -> smem | sync | issue MMAf(j) |
@@ -448,10 +497,10 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
     // MMAb(j) runs under the next iteration's ring build and Z wait.  The ring slots written in
     // iteration j (u row j-2's and u row j-1's) were last read by MMAf(j-1), complete by then.
 #pragma unroll 1
-    for (int j = 0; j <= G::RR; ++j) {
+    for (int j = j0; j <= jre; ++j) {
         float uq = 0.f;
         const int ws = (j + RS - 1) % RS;                       // slot of A2_j (= u row j-1's)
-        if (j < G::RR) {
+        if (j < jre) {
             const int yn = j + M - 1;
             if (wg == 0) {
                 th_build_row<M, G::UP, RS, 0>(us, yn, l, xg, su, t_rh, t_rl, yn % RS);
@@ -462,8 +511,8 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
             }
             uq = us[(j + C) * G::UP + xg] + cst;                // u_q (window centre): the DC restore value
         }
-        if (j > 0) {
-            tc::mbar_wait(&mbar_b, (uint32_t)((j - 1) & 1));
+        if (j > j0) {
+            tc::mbar_wait(&mbar_b, (uint32_t)((j - 1 - j0) & 1));
             tc::fence_after_sync();
             if (wg == 0) th_z_to_smem<G::ZP, 0, HZ8>(tl + G::COL_Z, zs, l);
             else th_z_to_smem<G::ZP, HZ8, NZ8>(tl + G::COL_Z, zs, l);
@@ -471,7 +520,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
         tc::wait_st();
         tc::fence_before_sync();
         __syncthreads();
-        if (warp == 0 && j < G::RR) {
+        if (warp == 0 && j < jre) {
             tc::fence_after_sync();
             // the small cross terms first, then hi.hi: the fp32 accumulator loses less of them
 #pragma unroll
@@ -487,18 +536,13 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
             }
             tc::mma_commit_warp(&mbar_f);
         }
-        if (j > 0) {
+        if (j > j0) {
             const int jz = j - 1;
-            const float s_tot = th_col2im<M, G::NB, G::ZP>(zs, zls + (jz & 1) * 2 * L, hand, l, jz, wg, acc);
-            // (a6) row o = jz - 2C is complete: g = u (.) s, s = (Z-unit sum) / (s_b 2^14)
-            const int o = jz - 2 * C;
-            if (wg == 1 && o >= 0 && o < R && out_col && sy0 + o < H) {
-                const float u = udom ? 1.0f : us[(o + 2 * C) * G::UP + l + 2 * C] + cst;   // W = diag(e^w)
-                gout[(size_t)(sy0 + o) * W + x0 + ocol] = (u * cc.inv_z) * s_tot;
-            }
+            const float s_tot = th_col2im<M, G::NB, G::ZP>(zs, zls + (jz & 1) * 2 * L, hand, l, jz, wg, acc, nh);
+            if (wg == 1) emit(jz - 2 * C, s_tot);   // row o = jz - 2C is complete (NH: or partial)
         }
-        if (j < G::RR) {
-            tc::mbar_wait(&mbar_f, (uint32_t)(j & 1));
+        if (j < jre) {
+            tc::mbar_wait(&mbar_f, (uint32_t)((j - j0) & 1));
             tc::fence_after_sync();
             // (a4, a7) responses r, rho (owned responses), rho'/2 -> P (fp16 hi/lo)
             const bool row_own = (j >= C) && (j < C + R) && (sy0 - C + j < H);   // (packed tiles: per strip)
@@ -534,6 +578,53 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
                     }
                 }
                 tc::mma_commit_warp(&mbar_b);
+            }
+        }
+    }
+    if constexpr (NH) {
+        // drain: the last 2C output rows (partial: the band below adds its share) from the rolling
+        // sums, no Z rows left -- wg0's hand-offs of rows [jre - C, jre) first, then wg1's rows
+        if (wg == 0)
+            for (int jz = jre; jz < jre + C; ++jz) th_col2im<M, G::NB, G::ZP, true>(zs, zls, hand, l, jz, 0, acc, true);
+        __syncthreads();
+        if (wg == 1)
+            for (int jz = jre; jz < jre + 2 * C; ++jz)
+                emit(jz - 2 * C, th_col2im<M, G::NB, G::ZP, true>(zs, zls, hand, l, jz, 1, acc, true));
+        // the two band boundaries of the tile (per strip of a packed tile): the second of the two
+        // tiles sharing a boundary to arrive adds the shares, g = g + gedge on its 2C rows (a
+        // two-term sum: the same bits whichever tile adds it)
+        __shared__ int fold[16];
+        const int nst = packed ? args.tc_spt : 1;
+        const int xt = packed ? ta.tiles_x : tile % ta.tiles_x;
+        __threadfence();
+        __syncthreads();
+        if (t < 2 * nst) {
+            const int band = y0 / R + (t >> 1);
+            int tb = band + (t & 1);
+            if (tb >= nbh) tb -= nbh;
+            int second = 0;
+            if (band < nbands) {
+                unsigned int* cnt = args.tcnt + ((size_t)b * nbh + tb) * (ta.tiles_x + 1) + xt;
+                if (atomicAdd(cnt, 1u) == 1u) {
+                    *cnt = 0u;   // both arrived: ready for the next launch
+                    second = 1;
+                }
+                __threadfence();
+            }
+            fold[t] = second ? tb : -1;
+        }
+        __syncthreads();
+        const int xa = packed ? x0 : x0, ncol = packed ? args.tc_rem : min(G::OW, W - x0);
+        for (int f = 0; f < 2 * nst; ++f) {
+            const int tb = fold[f];
+            if (tb < 0) continue;
+            const float* ge = gedge + (size_t)tb * (2 * C) * W;
+            for (int i = t; i < 2 * C * ncol; i += 256) {
+                const int k = i / ncol, x = xa + (i - k * ncol);
+                int y = tb * R - C + k;
+                if (y < 0) y += H;
+                float* gp = gout + (size_t)y * W + x;
+                *gp = __ldcg(gp) + __ldcg(ge + (size_t)k * W + x);
             }
         }
     }
