@@ -133,11 +133,15 @@ constexpr int kTcR = 64;
 #ifndef FOE_K8_NH
 #define FOE_K8_NH 1
 #endif
+// 1: ... and without column halos when 128-column tiles tile W (A/B knob)
+#ifndef FOE_K8_NHC
+#define FOE_K8_NHC 1
+#endif
 template <int M, int NP, int R>
 constexpr int th_smem() { return foe::ThGeom<M, NP, R>::SMEM_BYTES; }
-template <int M, int NP, int R, bool NH>
+template <int M, int NP, int R, int MODE>
 cudaError_t th_attr() {
-    return cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, R, NH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(foe::k_prior_grad_th<M, NP, R, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 th_smem<M, NP, R>());
 }
 template <int M, int NP>
@@ -145,10 +149,11 @@ cudaError_t tc_set_attr() {
     cudaError_t e = cudaFuncSetAttribute(foe::k_hvp_th<M, NP, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          foe::ThHGeom<M, NP, 64>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    const cudaError_t es[] = {th_attr<M, NP, 64, false>(), th_attr<M, NP, 32, false>(), th_attr<M, NP, 16, false>(),
-                              th_attr<M, NP, 8, false>(),  th_attr<M, NP, 4, false>(),  th_attr<M, NP, 64, true>(),
-                              th_attr<M, NP, 32, true>(),  th_attr<M, NP, 16, true>(),  th_attr<M, NP, 8, true>(),
-                              th_attr<M, NP, 4, true>()};
+    const cudaError_t es[] = {th_attr<M, NP, 64, 0>(), th_attr<M, NP, 32, 0>(), th_attr<M, NP, 16, 0>(),
+                              th_attr<M, NP, 8, 0>(),  th_attr<M, NP, 4, 0>(),  th_attr<M, NP, 64, 1>(),
+                              th_attr<M, NP, 32, 1>(), th_attr<M, NP, 16, 1>(), th_attr<M, NP, 8, 1>(),
+                              th_attr<M, NP, 4, 1>(),  th_attr<M, NP, 64, 2>(), th_attr<M, NP, 32, 2>(),
+                              th_attr<M, NP, 16, 2>(), th_attr<M, NP, 8, 2>(),  th_attr<M, NP, 4, 2>()};
     for (cudaError_t x : es)
         if (x != cudaSuccess) return x;
     return cudaSuccess;
@@ -230,7 +235,10 @@ struct ipiano_state {
     double* w = nullptr;      // [3][B][HW]
     float* g = nullptr;       // [2][groups][B][HW]
     float* gedge = nullptr;   // K8 without row halos: [2][B][H / tc_rows][2C][W] band-boundary shares
-    unsigned int* tcnt = nullptr;   // ... and their arrival counters [B][H / tc_rows][tiles_x + 1]
+    unsigned int* tcnt = nullptr;   // ... and their arrival counters [3][B][H / tc_rows][tiles_x + 1]
+    float* gright = nullptr;        // K8 without column halos: [2][B][W / 128][H][2C]
+    float* gcorner = nullptr;       // ... [2][B][H / tc_rows][W / 128][2C][2C]
+    int tc_mode = 0;                // K8: 0 halos, 1 no row halos, 2 no row / column halos
     float* ft = nullptr;      // [B][HW]
     double* epart = nullptr;  // [B][ntiles*groups]
     double* ppart = nullptr;  // [2][B][nblk2][8] (buffer 1: the persistent driver's odd rounds)
@@ -524,10 +532,11 @@ struct Plan {
     int tiles_x = 0, ntiles = 0, groups = 1;
     int tc_rem = 0, tc_spt = 0;   // K8 column packing (K1Args::tc_rem / tc_spt)
     int tc_rows = 64;             // K8 output rows per tile (v7: chosen per problem)
+    int tc_mode = 0;              // K8: 0 halos, 1 no row halos, 2 no row / column halos (foe_th.cuh)
     int ncp = kNCP, nchunks = 0;  // K1: filter pairs per chunk, chunks
 };
 Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref, int req_groups,
-                  bool allow_pack = true, int req_rows = 0) {
+                  bool allow_pack = true, int req_rows = 0, bool allow_nh = false) {
     Plan p;
     const int ow = 128 - (md->m - 1);
     const bool pack_ok = allow_pack && H_grid == H;
@@ -535,6 +544,18 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
     // columns of several bands share one packed tile (not for row slabs, whose energy partials are
     // per 64-row band)
     auto tiling = [&](int R, Plan& q) {
+        // the batch path's tiles without row halos (bands of R that tile H, R >= 2C), and without
+        // column halos when 128-column tiles tile W (foe_th.cuh MODE 1 / 2)
+        q.tc_mode = FOE_K8_NH && allow_nh && pack_ok && H % R == 0 && R >= md->m - 1 ? 1 : 0;
+        if (q.tc_mode == 1 && FOE_K8_NHC && W % 128 == 0) {
+            q.tc_mode = 2;
+            q.tiles_x = W / 128;
+            q.ntiles = (H / R) * q.tiles_x;
+            q.tc_rem = 0;
+            q.tc_spt = 0;
+            q.tc_rows = R;
+            return;
+        }
         int nfull = W / ow, rem = W - nfull * ow, spt = 0;
         if (rem > 0 && pack_ok) {
             spt = 128 / ((rem + 2 * (md->m - 1) + 7) & ~7);   // strips of a multiple of 8 lanes
@@ -596,21 +617,28 @@ Plan plan_stencil(const foe_model* md, int B, int H, int W, int H_grid, int pref
 
 // K8 launch of tile height R (4 .. 64), with or without row halos (NH), as a programmatic
 // dependent launch (the graph trial rounds) or a plain one
-template <int M, int NP, bool NH, int RR>
+template <int M, int NP, int MODE, int RR>
 cudaError_t launch_th_r(dim3 grid, cudaStream_t s, const foe::TcArgs& ta, const foe::ThConst& cc, bool pdl) {
-    if (pdl) return launch_pdl(foe::k_prior_grad_th<M, NP, RR, NH>, grid, dim3(256), th_smem<M, NP, RR>(), s, ta, cc);
-    foe::k_prior_grad_th<M, NP, RR, NH><<<grid, 256, th_smem<M, NP, RR>(), s>>>(ta, cc);
+    if (pdl) return launch_pdl(foe::k_prior_grad_th<M, NP, RR, MODE>, grid, dim3(256), th_smem<M, NP, RR>(), s, ta, cc);
+    foe::k_prior_grad_th<M, NP, RR, MODE><<<grid, 256, th_smem<M, NP, RR>(), s>>>(ta, cc);
     return cudaGetLastError();
 }
-template <int M, int NP, bool NH>
+template <int M, int NP, int MODE>
 cudaError_t launch_th(int R, dim3 grid, cudaStream_t s, const foe::TcArgs& ta, const foe::ThConst& cc, bool pdl) {
     switch (R) {
-        case 4: return launch_th_r<M, NP, NH, 4>(grid, s, ta, cc, pdl);
-        case 8: return launch_th_r<M, NP, NH, 8>(grid, s, ta, cc, pdl);
-        case 16: return launch_th_r<M, NP, NH, 16>(grid, s, ta, cc, pdl);
-        case 32: return launch_th_r<M, NP, NH, 32>(grid, s, ta, cc, pdl);
-        default: return launch_th_r<M, NP, NH, 64>(grid, s, ta, cc, pdl);
+        case 4: return launch_th_r<M, NP, MODE, 4>(grid, s, ta, cc, pdl);
+        case 8: return launch_th_r<M, NP, MODE, 8>(grid, s, ta, cc, pdl);
+        case 16: return launch_th_r<M, NP, MODE, 16>(grid, s, ta, cc, pdl);
+        case 32: return launch_th_r<M, NP, MODE, 32>(grid, s, ta, cc, pdl);
+        default: return launch_th_r<M, NP, MODE, 64>(grid, s, ta, cc, pdl);
     }
+}
+template <int M, int NP>
+cudaError_t launch_th_mode(int mode, int R, dim3 grid, cudaStream_t s, const foe::TcArgs& ta, const foe::ThConst& cc,
+                           bool pdl) {
+    if (mode == 2) return launch_th<M, NP, 2>(R, grid, s, ta, cc, pdl);
+    if (mode == 1) return launch_th<M, NP, 1>(R, grid, s, ta, cc, pdl);
+    return launch_th<M, NP, 0>(R, grid, s, ta, cc, pdl);
 }
 
 // Launch the prior energy+gradient evaluation `a` (tiling fields taken from the plan).
@@ -630,12 +658,9 @@ foe_status launch_prior(const foe_model* md, int kind, K1Args a, int B, cudaStre
     const dim3 grid(ntiles_grid >= 0 ? ntiles_grid : a.ntiles - a.tile_off, B);
     if (grid.x == 0) return FOE_OK;
     const int R = a.tc_rows;
-    const bool nh = a.gedge != nullptr;
-    cudaError_t e;
-    if (md->tc_np == 48) e = nh ? launch_th<7, 48, true>(R, grid, s, ta, *md->th_const, pdl)
-                                : launch_th<7, 48, false>(R, grid, s, ta, *md->th_const, pdl);
-    else e = nh ? launch_th<5, 32, true>(R, grid, s, ta, *md->th_const, pdl)
-                : launch_th<5, 32, false>(R, grid, s, ta, *md->th_const, pdl);
+    const int mode = a.gedge == nullptr ? 0 : (a.gright == nullptr ? 1 : 2);
+    const cudaError_t e = md->tc_np == 48 ? launch_th_mode<7, 48>(mode, R, grid, s, ta, *md->th_const, pdl)
+                                          : launch_th_mode<5, 32>(mode, R, grid, s, ta, *md->th_const, pdl);
     CK(e);
     CKL("k_prior_grad_th");
     return FOE_OK;
@@ -959,6 +984,11 @@ K1Args state_k1_args(const ipiano_state* st, int which_cur) {
     a.gedge = st->gedge;
     a.gedge_slot_stride = st->gedge ? (size_t)st->B * (st->H / st->tc_rows) * (st->model->m - 1) * st->W : 0;
     a.tcnt = st->tcnt;
+    a.gright = st->gright;
+    a.gcorner = st->gcorner;
+    a.gright_slot_stride = st->gright ? (size_t)st->B * st->tiles_x * st->H * (st->model->m - 1) : 0;
+    a.gcorner_slot_stride =
+        st->gcorner ? (size_t)st->B * (st->H / st->tc_rows) * st->tiles_x * (st->model->m - 1) * (st->model->m - 1) : 0;
     return a;
 }
 
@@ -1235,7 +1265,7 @@ void ipiano_state_destroy(ipiano_state* st) {
     cudaSetDevice(st->model->dev);
     if (st->s) cudaStreamSynchronize(st->s);
     if (st->graph) cudaGraphExecDestroy(st->graph);
-    cudaFree(st->w); cudaFree(st->g); cudaFree(st->gedge); cudaFree(st->tcnt); cudaFree(st->ft); cudaFree(st->epart); cudaFree(st->ppart);
+    cudaFree(st->w); cudaFree(st->g); cudaFree(st->gedge); cudaFree(st->tcnt); cudaFree(st->gright); cudaFree(st->gcorner); cudaFree(st->ft); cudaFree(st->epart); cudaFree(st->ppart);
     if (st->phase_ns) {   // FOE_PERSIST_PHASES diagnostics: mean phase durations of the last launch
         std::vector<unsigned long long> h(4 * foe::kPhaseRounds, 0);
         cudaMemcpy(h.data(), st->phase_ns, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost);
@@ -1333,12 +1363,13 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
                               (cfg.solver == FOE_SOLVER_AUTO && cfg.stencil != FOE_STENCIL_TENSOR &&
                                (npx < (1LL << 16) || (md->tc_np == 0 && npx <= (1LL << 18))));
     const int pref = want_persist ? FOE_STENCIL_FFMA : cfg.stencil;
-    const Plan pl = plan_stencil(md, B, H, W, H, pref, cfg.filter_groups, !t_slab_member, cfg.tile_rows);
+    const Plan pl = plan_stencil(md, B, H, W, H, pref, cfg.filter_groups, !t_slab_member, cfg.tile_rows, true);
     st->kind = pl.kind;
     st->tiles_x = pl.tiles_x;
     st->tc_rem = pl.tc_rem;
     st->tc_spt = pl.tc_spt;
     st->tc_rows = pl.tc_rows;
+    st->tc_mode = pl.kind == FOE_STENCIL_TENSOR ? pl.tc_mode : 0;
     st->ntiles = pl.ntiles;
     st->ncp = pl.kind == FOE_STENCIL_FFMA ? pl.ncp : kNCP;
     st->nchunks = pl.kind == FOE_STENCIL_FFMA ? pl.nchunks : div_up(md->nf, Tr<7>::NC);
@@ -1389,10 +1420,14 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     CKS(cudaMalloc((void**)&st->g, sizeof(float) * 2 * st->groups * n));
     // K8 without row halos (foe_th.cuh): the batch path's tensor-core stencil when the bands tile H
     // and are at least 2C rows tall (a row near a band edge then takes contributions from two bands)
-    if (FOE_K8_NH && st->kind == FOE_STENCIL_TENSOR && !t_slab_member && H % st->tc_rows == 0 &&
-        st->tc_rows >= md->m - 1) {
-        CKS(cudaMalloc((void**)&st->gedge, sizeof(float) * 2 * (size_t)B * (H / st->tc_rows) * (md->m - 1) * W));
-        const size_t nc = (size_t)B * (H / st->tc_rows) * (st->tiles_x + 1);
+    if (st->tc_mode >= 1) {   // (plan_stencil: bands of R that tile H, R >= 2C; mode 2: W % 128 == 0)
+        const size_t nb = H / st->tc_rows, c2 = md->m - 1;
+        CKS(cudaMalloc((void**)&st->gedge, sizeof(float) * 2 * (size_t)B * nb * c2 * W));
+        if (st->tc_mode == 2) {
+            CKS(cudaMalloc((void**)&st->gright, sizeof(float) * 2 * (size_t)B * st->tiles_x * H * c2));
+            CKS(cudaMalloc((void**)&st->gcorner, sizeof(float) * 2 * (size_t)B * nb * st->tiles_x * c2 * c2));
+        }
+        const size_t nc = 3 * (size_t)B * nb * (st->tiles_x + 1);
         CKS(cudaMalloc((void**)&st->tcnt, sizeof(unsigned int) * nc));
         CKS(cudaMemset(st->tcnt, 0, sizeof(unsigned int) * nc));
     }

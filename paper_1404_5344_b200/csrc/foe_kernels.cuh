@@ -111,6 +111,12 @@ struct K1Args {
     float* gedge;
     size_t gedge_slot_stride;
     unsigned int* tcnt;
+    // ... and without column halos either (W % 128 == 0, 128-column tiles): the pieces of the
+    // rows near band edges x the columns near tile edges -- gright [slots][B][ns][H][2C] (column
+    // boundary s = the right tile), gcorner [slots][B][nb][ns][2C][2C]; counters [3][B][nb][ns + 1]
+    float* gright;
+    float* gcorner;
+    size_t gright_slot_stride, gcorner_slot_stride;
     // HVP only
     const double* v;        // [B][H][W]
     const float* gw;        // [B][H][W] gradient at w

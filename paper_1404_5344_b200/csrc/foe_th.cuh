@@ -115,9 +115,12 @@ struct ThGeom {
     static constexpr int SM_Z = SM_U + UY * UP * 4;
     static constexpr int NZ8 = (NB + 7) / 8;            // Z read-out chunks of 8 taps
     static constexpr int ZP = NB + 2;                   // Z pitch (floats): zs[lane][column], ZP/2 odd
-    static constexpr int SM_HAND = SM_Z + (LANES + 8) * ZP * 4;   // (+8 lanes: reads at l + b past 127)
-    static constexpr int SM_ZL = SM_HAND + 8 * LANES * 4;
-    static constexpr int SMEM_BYTES = SM_ZL + 4 * LANES * 4 + 64;
+    // Z rows of lanes [-8, LANES + 8) (zs = SM_Z + 8 lanes): the col2im of a tile without column
+    // halos reads lanes l - 2C .. l + 2C (zero outside [0, LANES))
+    static constexpr int SM_HAND = SM_Z + (LANES + 16) * ZP * 4;
+    static constexpr int LZ = LANES + 16;               // last-tap partial row pitch (lanes [-8, LANES + 8))
+    static constexpr int SM_ZL = SM_HAND + 8 * LANES * 4 + 8 * 8 * 4;   // (+ the extra columns' hand-offs)
+    static constexpr int SMEM_BYTES = SM_ZL + 4 * LZ * 4 + 64;
     static_assert(NP % 16 == 0 && NBP <= ND, "MMA shapes");
     static_assert(TAPS - NB <= 1, "at most one CUDA-core tap");
     static_assert(TCOLS_USED <= 256, "TMEM budget: two CTAs per SM");
@@ -263,22 +266,24 @@ __device__ __forceinline__ void th_z_to_smem(uint32_t t_z, float* zs, int l) {
 // NH (tiles without row halos, K1Args::gedge): output rows o >= -C are emitted (the wg0 share of
 // a row o < 0 is zero: its kernel rows a <= C would need Z rows below the first, C); Z0: a drain
 // step with no Z row (the accumulators only roll on).
-template <int M, int NB, int ZP, bool Z0 = false>
-__device__ __forceinline__ float th_col2im(const float* zs, const float* zl, float* hand, int l, int jz, int wg,
+// lb: the first Z lane of the thread's output (l; l - 2C without column halos), hand slot
+// (o & 7) HS + hl; zl rows of pitch LZ.
+template <int M, int NB, int ZP, bool Z0 = false, int HS = 128, int LZ = 144>
+__device__ __forceinline__ float th_col2im(const float* zs, const float* zl, float* hand, int hl, int lb, int jz, int wg,
                                            float* acc, bool nh = false) {
-    constexpr int C = (M - 1) / 2, A0 = C + 1, A1 = M - A0, L = 128;
-    const float* zr = zs + l * ZP;
+    constexpr int C = (M - 1) / 2, A0 = C + 1, A1 = M - A0;
+    const float* zr = zs + lb * ZP;
     if (Z0) {
         if (wg == 0) {
             const int o = jz - (A0 - 1);
-            if (o >= 0) hand[(o & 7) * L + l] = acc[A0 - 1];
+            if (o >= 0) hand[(o & 7) * HS + hl] = acc[A0 - 1];
 #pragma unroll
             for (int k = A0 - 1; k > 0; --k) acc[k] = acc[k - 1];
             acc[0] = 0.f;
             return 0.f;
         }
         const int o = jz - 2 * C;
-        const float s_tot = acc[A1 - 1] + (o >= 0 ? hand[(o & 7) * L + l] : 0.f);
+        const float s_tot = acc[A1 - 1] + (o >= 0 ? hand[(o & 7) * HS + hl] : 0.f);
 #pragma unroll
         for (int k = A1 - 1; k > 0; --k) acc[k] = acc[k - 1];
         acc[0] = 0.f;
@@ -301,7 +306,7 @@ __device__ __forceinline__ float th_col2im(const float* zs, const float* zl, flo
             acc[A0 - 1] += sa;
         }
         const int o = jz - (A0 - 1);                    // wg0's share of row o is complete
-        if (o >= 0) hand[(o & 7) * L + l] = acc[A0 - 1];
+        if (o >= 0) hand[(o & 7) * HS + hl] = acc[A0 - 1];
 #pragma unroll
         for (int k = A0 - 1; k > 0; --k) acc[k] = acc[k - 1];
         acc[0] = 0.f;
@@ -324,11 +329,11 @@ __device__ __forceinline__ float th_col2im(const float* zs, const float* zl, flo
             float sa = 0.f;
 #pragma unroll
             for (int bb = 0; bb < M; ++bb)
-                sa += th_zcol(M, a, bb) < NB ? zr[bb * ZP + th_zcol(M, a, bb)] : zl[l + bb] + zl[L + l + bb];
+                sa += th_zcol(M, a, bb) < NB ? zr[bb * ZP + th_zcol(M, a, bb)] : zl[lb + bb] + zl[LZ + lb + bb];
             acc[k] += sa;
         }
         const int o = jz - 2 * C;
-        const float s_tot = o >= 0 ? acc[A1 - 1] + hand[(o & 7) * L + l] : (nh ? acc[A1 - 1] : 0.f);
+        const float s_tot = o >= 0 ? acc[A1 - 1] + hand[(o & 7) * HS + hl] : (nh ? acc[A1 - 1] : 0.f);
 #pragma unroll
         for (int k = A1 - 1; k > 0; --k) acc[k] = acc[k - 1];
         acc[0] = 0.f;
@@ -336,15 +341,17 @@ __device__ __forceinline__ float th_col2im(const float* zs, const float* zl, flo
     }
 }
 
-template <int M, int NP, int R, bool NH = false>
+// MODE 0: tiles with row and column halos; 1: no row halos (NH); 2: no row or column halos (the
+// tile's 128 lanes are its own 128 columns; W % 128 == 0, no packed tiles)
+template <int M, int NP, int R, int MODE = 0>
 __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const __grid_constant__ ThConst cc) {
     using G = ThGeom<M, NP, R>;
     constexpr int C = G::C, L = G::LANES, RS = G::RS;
     extern __shared__ __align__(128) unsigned char smb[];
     float* us = reinterpret_cast<float*>(smb + G::SM_U);
-    float* zs = reinterpret_cast<float*>(smb + G::SM_Z);
+    float* zs = reinterpret_cast<float*>(smb + G::SM_Z) + 8 * G::ZP;   // lanes [-8, 136)
     float* hand = reinterpret_cast<float*>(smb + G::SM_HAND);   // [8][L] wg0 -> wg1 partial sums
-    float* zls = reinterpret_cast<float*>(smb + G::SM_ZL);      // [2 rows][2 groups][L] last-tap partials
+    float* zls = reinterpret_cast<float*>(smb + G::SM_ZL) + 8;  // [2 rows][2 groups][LZ] last-tap partials (lanes -8 ..)
     __shared__ uint32_t tbase_s;
     __shared__ __align__(8) uint64_t mbar_f, mbar_b;   // forward / backward MMA completion
     __shared__ __align__(8) uint64_t mbar_bimg;        // TMA bulk copy of the B images
@@ -389,7 +396,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
     const int SP = (args.tc_rem + 4 * C + 7) & ~7;             // strip pitch in lanes (packed)
     if (!packed) {
         const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
-        y0 = ty * R; x0 = tx * G::OW; sy0 = y0; ocol = l;
+        y0 = ty * R; x0 = tx * (MODE == 2 ? L : G::OW); sy0 = y0; ocol = l;
     } else {
         const int band0 = (tile - nnorm) * args.tc_spt;
         const int st = l / SP;
@@ -411,13 +418,20 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
     const float cst = (float)(udom ? wc : exp(wc));
     // NH (no row halos, args.gedge): response rows [C, C + R) only (output rows 0 .. R-1), u rows
     // [C, R + 3C) staged; else response rows [0, R + 2C), u rows [0, R + 4C)
-    constexpr bool nh = NH;
+    constexpr bool nh = MODE >= 1, ncol = MODE == 2;
     const int j0 = nh ? C : 0, jre = nh ? C + R : G::RR;
     const int uy_lo = nh ? C : 0, uy_hi = nh ? G::UY - C : G::UY;
     if (!packed)
-        tc_stage_u<G::UY, G::UX, G::UP, 8>(us, w, args.halo, H, W, y0, x0, 2 * C, udom, cst, wc, warp, t & 31, uy_lo, uy_hi);
+        tc_stage_u<G::UY, G::UX, G::UP, 8>(us, w, args.halo, H, W, y0, ncol ? x0 + C : x0, 2 * C, udom, cst, wc, warp,
+                                           t & 31, uy_lo, uy_hi);
     else tc_stage_u_packed<G::UY, G::UX, G::UP, 8>(us, w, H, W, R, x0, 2 * C, SP, args.tc_spt, y0 / R, nbands, udom,
                                                    cst, wc, warp, t & 31, uy_lo, uy_hi);
+    // zero padding lanes of Z and of the last-tap partials (read by the col2im at the tile's edges)
+    for (int i = t; i < 16 * G::ZP; i += 256) {
+        const int ln = i / G::ZP;
+        zs[(ln < 8 ? ln - 8 : L + ln - 8) * G::ZP + (i - ln * G::ZP)] = 0.f;
+    }
+    if (t < 64) zls[(t >> 4) * G::LZ + ((t & 15) < 8 ? (t & 15) - 8 : L + (t & 15) - 8)] = 0.f;
     tc::fence_before_sync();
     __syncthreads();
     // tile scale s_u = 2^(13 - e), 2^e <= 2 max|u - cst| < 2^(e+1): every U and A2 entry (a
@@ -455,16 +469,16 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
 
     // energy ownership of this lane's response column, output column of this thread
     const int ow = packed ? args.tc_rem : G::OW;
-    const bool col_own = svalid && (ocol >= C) && (ocol < C + ow) && (x0 - C + ocol < W);
+    const bool col_own = ncol ? x0 + l < W : svalid && (ocol >= C) && (ocol < C + ow) && (x0 - C + ocol < W);
     const bool out_col = svalid && (ocol < ow) && (x0 + ocol < W);
 
     double e_acc = 0.0;
     constexpr int NZ8 = G::NZ8, HZ8 = (NZ8 + 1) / 2;       // Z tap chunks: wg0 [0,HZ8), wg1 [HZ8,NZ8)
     constexpr int NF8 = NP / 8, HF8 = NF8 / 2;             // filter chunks: wg0 [0,HF8), wg1 [HF8,NF8)
     constexpr int A0 = C + 1, A1 = M - A0;                 // col2im rows: wg0 a < A0, wg1 a >= A0
-    float acc[A0 > A1 ? A0 : A1];
+    float acc[A0 > A1 ? A0 : A1], acc2[A0 > A1 ? A0 : A1];   // (acc2: MODE 2's extra columns)
 #pragma unroll
-    for (int k = 0; k < (A0 > A1 ? A0 : A1); ++k) acc[k] = 0.f;
+    for (int k = 0; k < (A0 > A1 ? A0 : A1); ++k) acc[k] = acc2[k] = 0.f;
     float* gout = args.g + (size_t)gslot * args.g_slot_stride + (size_t)b * HW;
     // (a6) g = u (.) s of output row o: with row halos rows [0, R) of the band; NH rows [-C, R + C)
     // (rows within C of a band edge are partial sums): [-C, R - C) into g (row o < 0 wraps to the
@@ -489,6 +503,28 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
             if (y < 0) y += H;
             gout[(size_t)y * W + x0 + ocol] = v;
         }
+    };
+    // MODE 2: output (o, c), o in [-C, R + C), c in [-C, L + C) tile-relative.  Rows: top (< C),
+    // middle, bottom (>= R - C); columns: left (< C), middle, right (>= L - C).  Top/middle x
+    // left/middle pieces into g, bottom x left/middle into gedge [nb][2C][W] (boundary of the next
+    // band), top/middle x right into gright [ns][H][2C] (column boundary of the next tile), bottom x
+    // right into gcorner [nb][ns][2C][2C]
+    const int nsx = ncol ? W / L : 1, tyb = y0 / R, txb = x0 / L;
+    const int tbn = tyb + 1 < nbh ? tyb + 1 : 0, sbn = txb + 1 < nsx ? txb + 1 : 0;
+    float* gright = ncol ? args.gright + (size_t)gslot * args.gright_slot_stride + (size_t)b * nsx * H * (2 * C) : nullptr;
+    float* gcorner = ncol ? args.gcorner + (size_t)gslot * args.gcorner_slot_stride + (size_t)b * nbh * nsx * (4 * C * C)
+                          : nullptr;
+    auto emit_c = [&](int o, int c, float s_tot) {
+        const float u = udom ? 1.0f : us[(o + 2 * C) * G::UP + c + C] + cst;
+        const float v = (u * cc.inv_z) * s_tot;
+        const bool bot = o >= R - C, rgt = c >= L - C;
+        int y = y0 + o, x = x0 + c;
+        if (y < 0) y += H;
+        if (x < 0) x += W; else if (x >= W) x -= W;
+        if (!bot && !rgt) gout[(size_t)y * W + x] = v;
+        else if (!rgt) gedge[((size_t)tbn * (2 * C) + (o - R + C)) * W + x] = v;
+        else if (!bot) gright[((size_t)sbn * H + y) * (2 * C) + (c - L + C)] = v;
+        else gcorner[(((size_t)tbn * nsx + sbn) * (2 * C) + (o - R + C)) * (2 * C) + (c - L + C)] = v;
     };
 
     // Software pipeline over response rows (iteration j):
@@ -538,8 +574,19 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
         }
         if (j > j0) {
             const int jz = j - 1;
-            const float s_tot = th_col2im<M, G::NB, G::ZP>(zs, zls + (jz & 1) * 2 * L, hand, l, jz, wg, acc, nh);
-            if (wg == 1) emit(jz - 2 * C, s_tot);   // row o = jz - 2C is complete (NH: or partial)
+            const float s_tot = th_col2im<M, G::NB, G::ZP, false, L, G::LZ>(zs, zls + (jz & 1) * 2 * G::LZ, hand, l,
+                                                                            ncol ? l - 2 * C : l, jz, wg, acc, nh);
+            if constexpr (MODE == 2) {
+                if (wg == 1) emit_c(jz - 2 * C, l - C, s_tot);
+                if (l < 2 * C) {   // the tile's 2C extra output columns [L - C, L + C) (right partials)
+                    const float s2 = th_col2im<M, G::NB, G::ZP, false, 8, G::LZ>(zs, zls + (jz & 1) * 2 * G::LZ,
+                                                                                 hand + 8 * L, l, L - 2 * C + l, jz, wg,
+                                                                                 acc2, true);
+                    if (wg == 1) emit_c(jz - 2 * C, L - C + l, s2);
+                }
+            } else {
+                if (wg == 1) emit(jz - 2 * C, s_tot);   // row o = jz - 2C is complete (NH: or partial)
+            }
         }
         if (j < jre) {
             tc::mbar_wait(&mbar_f, (uint32_t)((j - j0) & 1));
@@ -559,7 +606,7 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
             el = wg == 0
                 ? th_epilogue<0, HF8>(tl + G::COL_D, tl + G::COL_PH, tl + G::COL_PL, uq, inv, cc.sumk, cc.thl, cc.kbl, zl)
                 : th_epilogue<HF8, NF8>(tl + G::COL_D, tl + G::COL_PH, tl + G::COL_PL, uq, inv, cc.sumk, cc.thl, cc.kbl, zl);
-            if (!FOE_K8_TAP49) zls[(j & 1) * 2 * L + wg * L + l] = zl;
+            if (!FOE_K8_TAP49) zls[(j & 1) * 2 * G::LZ + wg * G::LZ + l] = zl;
             if (own) e_acc += (double)el;
             tc::wait_st();
             tc::fence_before_sync();
@@ -581,50 +628,123 @@ __global__ void __launch_bounds__(256, 2) k_prior_grad_th(const TcArgs ta, const
             }
         }
     }
-    if constexpr (NH) {
+    if constexpr (MODE >= 1) {
         // drain: the last 2C output rows (partial: the band below adds its share) from the rolling
         // sums, no Z rows left -- wg0's hand-offs of rows [jre - C, jre) first, then wg1's rows
         if (wg == 0)
-            for (int jz = jre; jz < jre + C; ++jz) th_col2im<M, G::NB, G::ZP, true>(zs, zls, hand, l, jz, 0, acc, true);
+            for (int jz = jre; jz < jre + C; ++jz) {
+                th_col2im<M, G::NB, G::ZP, true, L, G::LZ>(zs, zls, hand, l, l, jz, 0, acc, true);
+                if (ncol && l < 2 * C) th_col2im<M, G::NB, G::ZP, true, 8, G::LZ>(zs, zls, hand + 8 * L, l, l, jz, 0, acc2, true);
+            }
         __syncthreads();
         if (wg == 1)
-            for (int jz = jre; jz < jre + 2 * C; ++jz)
-                emit(jz - 2 * C, th_col2im<M, G::NB, G::ZP, true>(zs, zls, hand, l, jz, 1, acc, true));
-        // the two band boundaries of the tile (per strip of a packed tile): the second of the two
-        // tiles sharing a boundary to arrive adds the shares, g = g + gedge on its 2C rows (a
-        // two-term sum: the same bits whichever tile adds it)
-        __shared__ int fold[16];
-        const int nst = packed ? args.tc_spt : 1;
-        const int xt = packed ? ta.tiles_x : tile % ta.tiles_x;
-        __threadfence();
-        __syncthreads();
-        if (t < 2 * nst) {
-            const int band = y0 / R + (t >> 1);
-            int tb = band + (t & 1);
-            if (tb >= nbh) tb -= nbh;
-            int second = 0;
-            if (band < nbands) {
-                unsigned int* cnt = args.tcnt + ((size_t)b * nbh + tb) * (ta.tiles_x + 1) + xt;
-                if (atomicAdd(cnt, 1u) == 1u) {
-                    *cnt = 0u;   // both arrived: ready for the next launch
-                    second = 1;
+            for (int jz = jre; jz < jre + 2 * C; ++jz) {
+                const float s1 = th_col2im<M, G::NB, G::ZP, true, L, G::LZ>(zs, zls, hand, l, l, jz, 1, acc, true);
+                if constexpr (MODE == 2) {
+                    emit_c(jz - 2 * C, l - C, s1);
+                    if (l < 2 * C)
+                        emit_c(jz - 2 * C, L - C + l,
+                               th_col2im<M, G::NB, G::ZP, true, 8, G::LZ>(zs, zls, hand + 8 * L, l, l, jz, 1, acc2, true));
+                } else {
+                    emit(jz - 2 * C, s1);
+                }
+            }
+        if constexpr (MODE == 1) {
+            // the two band boundaries of the tile (per strip of a packed tile): the second of the two
+            // tiles sharing a boundary to arrive adds the shares, g = g + gedge on its 2C rows (a
+            // two-term sum: the same bits whichever tile adds it)
+            __shared__ int fold[16];
+            const int nst = packed ? args.tc_spt : 1;
+            const int xt = packed ? ta.tiles_x : tile % ta.tiles_x;
+            __threadfence();
+            __syncthreads();
+            if (t < 2 * nst) {
+                const int band = y0 / R + (t >> 1);
+                int tb = band + (t & 1);
+                if (tb >= nbh) tb -= nbh;
+                int second = 0;
+                if (band < nbands) {
+                    unsigned int* cnt = args.tcnt + ((size_t)b * nbh + tb) * (ta.tiles_x + 1) + xt;
+                    if (atomicAdd(cnt, 1u) == 1u) {
+                        *cnt = 0u;   // both arrived: ready for the next launch
+                        second = 1;
+                    }
+                    __threadfence();
+                }
+                fold[t] = second ? tb : -1;
+            }
+            __syncthreads();
+            const int ncl = packed ? args.tc_rem : min(G::OW, W - x0);
+            for (int f = 0; f < 2 * nst; ++f) {
+                const int tb = fold[f];
+                if (tb < 0) continue;
+                const float* ge = gedge + (size_t)tb * (2 * C) * W;
+                for (int i = t; i < 2 * C * ncl; i += 256) {
+                    const int k = i / ncl, x = x0 + (i - k * ncl);
+                    int y = tb * R - C + k;
+                    if (y < 0) y += H;
+                    float* gp = gout + (size_t)y * W + x;
+                    *gp = __ldcg(gp) + __ldcg(ge + (size_t)k * W + x);
+                }
+            }
+        } else {
+            // MODE 2: the second of the two tiles of a row segment (band boundary x the tile's
+            // middle columns) or of a column segment (column boundary x middle rows), the fourth of
+            // the four tiles of a corner, adds the pieces -- ((g + gedge) + gright) + gcorner, a
+            // fixed expression whichever tile evaluates it.  Counters tcnt [3][B][nb][ns + 1].
+            __shared__ int fold2[8];
+            __threadfence();
+            __syncthreads();
+            if (t < 8) {
+                const int kind = t < 2 ? 0 : (t < 4 ? 1 : 2);
+                int tb = tyb + ((t == 1 || t == 6 || t == 7) ? 1 : 0);
+                int sb = txb + ((t == 3 || t == 5 || t == 7) ? 1 : 0);
+                if (tb >= nbh) tb -= nbh;
+                if (sb >= nsx) sb -= nsx;
+                unsigned int* cnt = args.tcnt + (((size_t)kind * gridDim.y + b) * nbh + tb) * (nsx + 1) + sb;
+                const unsigned int need = kind == 2 ? 4u : 2u;
+                int f = -1;
+                if (atomicAdd(cnt, 1u) == need - 1u) {
+                    *cnt = 0u;
+                    f = (kind << 28) | (tb << 14) | sb;
                 }
                 __threadfence();
+                fold2[t] = f;
             }
-            fold[t] = second ? tb : -1;
-        }
-        __syncthreads();
-        const int xa = packed ? x0 : x0, ncol = packed ? args.tc_rem : min(G::OW, W - x0);
-        for (int f = 0; f < 2 * nst; ++f) {
-            const int tb = fold[f];
-            if (tb < 0) continue;
-            const float* ge = gedge + (size_t)tb * (2 * C) * W;
-            for (int i = t; i < 2 * C * ncol; i += 256) {
-                const int k = i / ncol, x = xa + (i - k * ncol);
-                int y = tb * R - C + k;
-                if (y < 0) y += H;
-                float* gp = gout + (size_t)y * W + x;
-                *gp = __ldcg(gp) + __ldcg(ge + (size_t)k * W + x);
+            __syncthreads();
+            for (int q = 0; q < 8; ++q) {
+                const int f = fold2[q];
+                if (f < 0) continue;
+                const int kind = f >> 28, tb = (f >> 14) & 0x3fff, sb = f & 0x3fff;
+                if (kind == 0) {          // rows tb R - C + k, columns [sb L + C, sb L + L - C)
+                    constexpr int NCm = L - 2 * C;
+                    for (int i = t; i < 2 * C * NCm; i += 256) {
+                        const int k = i / NCm, x = sb * L + C + (i - k * NCm);
+                        int y = tb * R - C + k;
+                        if (y < 0) y += H;
+                        float* gp = gout + (size_t)y * W + x;
+                        *gp = __ldcg(gp) + __ldcg(gedge + ((size_t)tb * (2 * C) + k) * W + x);
+                    }
+                } else if (kind == 1) {   // rows [tb R + C, tb R + R - C), columns sb L - C + kc
+                    for (int i = t; i < (R - 2 * C) * 2 * C; i += 256) {
+                        const int yr = i / (2 * C), kc = i - yr * (2 * C), y = tb * R + C + yr;
+                        int x = sb * L - C + kc;
+                        if (x < 0) x += W;
+                        float* gp = gout + (size_t)y * W + x;
+                        *gp = __ldcg(gp) + __ldcg(gright + ((size_t)sb * H + y) * (2 * C) + kc);
+                    }
+                } else {                  // corner rows tb R - C + k, columns sb L - C + kc
+                    for (int i = t; i < 4 * C * C; i += 256) {
+                        const int k = i / (2 * C), kc = i - k * (2 * C);
+                        int y = tb * R - C + k, x = sb * L - C + kc;
+                        if (y < 0) y += H;
+                        if (x < 0) x += W;
+                        float* gp = gout + (size_t)y * W + x;
+                        const float v = __ldcg(gp) + __ldcg(gedge + ((size_t)tb * (2 * C) + k) * W + x);
+                        const float v2 = v + __ldcg(gright + ((size_t)sb * H + y) * (2 * C) + kc);
+                        *gp = v2 + __ldcg(gcorner + (((size_t)tb * nsx + sb) * (2 * C) + k) * (2 * C) + kc);
+                    }
+                }
             }
         }
     }
@@ -749,9 +869,9 @@ __global__ void __launch_bounds__(256, 1) k_hvp_th(const TcArgs ta, const __grid
     extern __shared__ __align__(128) unsigned char smb[];
     float* us = reinterpret_cast<float*>(smb + G::SM_U);
     float* ts = reinterpret_cast<float*>(smb + GH::SM_T);
-    float* zs = reinterpret_cast<float*>(smb + G::SM_Z);
+    float* zs = reinterpret_cast<float*>(smb + G::SM_Z) + 8 * G::ZP;   // lanes [-8, 136)
     float* hand = reinterpret_cast<float*>(smb + G::SM_HAND);
-    float* zls = reinterpret_cast<float*>(smb + G::SM_ZL);
+    float* zls = reinterpret_cast<float*>(smb + G::SM_ZL) + 8;
     __shared__ uint32_t tbase_s;
     __shared__ __align__(8) uint64_t mbar_f, mbar_b, mbar_bimg;
     __shared__ float wmax[16];
@@ -898,7 +1018,8 @@ __global__ void __launch_bounds__(256, 1) k_hvp_th(const TcArgs ta, const __grid
         }
         if (j > 0) {
             const int jz = j - 1;
-            const float s_sum = th_col2im<M, G::NB, G::ZP>(zs, zls + (jz & 1) * 2 * L, hand, l, jz, wg, acc);
+            const float s_sum = th_col2im<M, G::NB, G::ZP, false, L, G::LZ>(zs, zls + (jz & 1) * 2 * G::LZ, hand, l, l, jz,
+                                                                            wg, acc);
             const int o = jz - 2 * C;
             if (wg == 1 && o >= 0 && o < R && out_col && y0 + o < H) {
                 const float s_tot = s_sum * inv_zt;
@@ -922,7 +1043,7 @@ __global__ void __launch_bounds__(256, 1) k_hvp_th(const TcArgs ta, const __grid
             else
                 th_hvp_epilogue<HF8, NF8>(tl + GH::COL_D, tl + GH::COL_DT, tl + GH::COL_PH, tl + GH::COL_PL, uq, inv,
                                           inv_t, cc.sumk, cc.kbl, zl);
-            if (!FOE_K8_TAP49) zls[(j & 1) * 2 * L + wg * L + l] = zl;
+            if (!FOE_K8_TAP49) zls[(j & 1) * 2 * G::LZ + wg * G::LZ + l] = zl;
             tc::wait_st();
             tc::fence_before_sync();
             __syncthreads();

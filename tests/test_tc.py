@@ -169,12 +169,15 @@ def test_tc_slabs_bitwise_g_invariant():
 
 
 @pytest.mark.parametrize("rows", [8, 32])
-@pytest.mark.parametrize("B,H,W", [(2, 300, 260), (1, 520, 512), (2, 256, 260), (1, 8, 300)])
+@pytest.mark.parametrize("B,H,W", [(2, 300, 260), (1, 520, 512), (2, 256, 260), (1, 8, 300), (2, 256, 256),
+                                   (1, 64, 128), (1, 8, 128)])
 def test_tc_tile_rows_P3(rows, B, H, W):
     """K8 with forced tile heights (ipiano_config.tile_rows) against the oracle on batch shapes.
-    Bands that tile H (and are >= 2C = 6 rows tall) run without row halos (the partial sums of the
-    rows near band edges, incl. the periodic wrap and a single band H = 8, meet in K2); the others
-    (300 rows; 520 in 32-row bands; 8 rows in 32-row tiles) with halos and a short last band.
+    Bands that tile H (and are >= 2C = 6 rows tall) run without row halos, and without column halos
+    too when 128-column tiles tile W (the partial sums of the rows / columns near tile edges and the
+    four-tile corners, incl. the periodic wrap, a single band H = 8, a single column tile W = 128 and
+    a single tile, are added by the last tile to finish); the others (300 rows; 520 in 32-row
+    bands; 8 rows in 32-row tiles) with halos and a short last band.
     Ragged and packed remainder columns (W = 512: the 24 remainder columns of several bands share
     one tile), every image of a batch.  P3 bars (final image rel L2 <= 1e-4, |dPSNR| <= 0.01 dB,
     identical L_n / trials, H trace to 1e-6) over 30 iterations."""
