@@ -1389,6 +1389,11 @@ foe_status ipiano_state_create(const foe_model* md, const float* f, int B, int H
     // a launch of fewer than ~4 blocks per SM at 8 px/thread (one 512^2 image: 128 blocks) is
     // fp64-latency bound: more, smaller blocks
     if (!t_slab_member && (long long)B * H * W < 4LL * md->nsm * kThreads * kPxt2) st->pxt2 = FOE_K2_PXT_SMALL;
+#ifndef FOE_K2_PXT_TINY
+#define FOE_K2_PXT_TINY 1
+#endif
+    // below one block per SM at 4 px/thread (c2: 256^2 = 64 blocks): one pixel per thread
+    if (!t_slab_member && (long long)B * H * W < (long long)md->nsm * kThreads * FOE_K2_PXT_SMALL) st->pxt2 = FOE_K2_PXT_TINY;
     if (t_slab_member && t_force_pxt > 0) st->pxt2 = t_force_pxt;
     if (want_persist && pl.kind == FOE_STENCIL_FFMA) {
         // K2 items: one pixel per thread while the grid can hold them all, else four
