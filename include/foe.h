@@ -292,6 +292,9 @@ foe_status foe_comm_unique_id(void* id_out);
 /* Creates this rank's NCCL communicator (one process per GPU; collective over the nranks
  * processes).  cuda_device must be the device of the models used with it. */
 foe_status foe_comm_create(const void* id, int nranks, int rank, int cuda_device, foe_comm** out);
+/* SURVEY.md 8(b)'s name of the same call: foe_comm_create on the calling thread's current CUDA
+ * device (cudaGetDevice); FOE_ERR_CUDA if that query fails. */
+foe_status foe_comm_init(const void* nccl_unique_id, int nranks, int rank, foe_comm** out);
 void foe_comm_destroy(foe_comm* comm);
 
 /* The ghost-row exchange of one trial as the NCCL point-to-point calls

@@ -2088,6 +2088,13 @@ foe_status foe_comm_unique_id(void* id_out) {
     return FOE_OK;
 }
 
+foe_status foe_comm_init(const void* nccl_unique_id, int nranks, int rank, foe_comm** out) {
+    int dev = 0;
+    const cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice", __LINE__);
+    return foe_comm_create(nccl_unique_id, nranks, rank, dev, out);
+}
+
 foe_status foe_comm_create(const void* id, int nranks, int rank, int cuda_device, foe_comm** out) {
     if (!out) return fail(FOE_ERR_INVALID_ARGUMENT, "out is NULL");
     *out = nullptr;

@@ -31,7 +31,7 @@ EXPORTED = (
     "ipiano_state_create", "ipiano_state_reset", "ipiano_step", "ipiano_solve", "ipiano_get_iterate",
     "ipiano_get_counters", "ipiano_get_trace", "ipiano_profile", "ipiano_profile_read", "ipiano_profile_read_k2",
     "ipiano_state_destroy", "ipiano_state_stencil", "ipiano_state_solver", "ipiano_run",
-    "foe_model_set_stencil", "foe_slab_exchange_plan", "foe_comm_unique_id", "foe_comm_create", "foe_comm_destroy", "ipiano_slabs_create", "ipiano_slabs_reset",
+    "foe_model_set_stencil", "foe_slab_exchange_plan", "foe_comm_unique_id", "foe_comm_create", "foe_comm_init", "foe_comm_destroy", "ipiano_slabs_create", "ipiano_slabs_reset",
     "ipiano_slabs_solve", "ipiano_slabs_advance", "ipiano_slabs_get_iterate", "ipiano_slabs_member", "ipiano_slabs_destroy",
     "ipiano_slabs_halo_handle", "ipiano_slabs_connect_peers", "ipiano_slabs_disconnect_peers",
     "foe_psnr", "foe_ssim", "foe_add_speckle",
@@ -106,6 +106,7 @@ def lib():
     L.foe_comm_unique_id.argtypes = [_vp]
     L.foe_slab_exchange_plan.argtypes = [C.c_int, C.c_int, _vp]
     L.foe_comm_create.argtypes = [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(_vp)]
+    L.foe_comm_init.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(_vp)]
     L.foe_comm_destroy.argtypes = [_vp]
     L.foe_comm_destroy.restype = None
     L.ipiano_slabs_create.argtypes = [_vp, _vp, C.c_int, C.c_int, C.c_int, _dp, C.c_double,
@@ -516,6 +517,12 @@ def foe_comm_create(unique_id: bytes, nranks: int, rank: int, device: int) -> Co
     h = C.c_void_p()
     _check(lib().foe_comm_create(C.cast(buf, _vp), int(nranks), int(rank), int(device), C.byref(h)))
     return Comm(h, nranks, rank, device)
+
+
+def foe_comm_init(unique_id: bytes, nranks: int, rank: int) -> Comm:
+    """SURVEY.md 8(b)'s name: foe_comm_create on the current CUDA device."""
+    import torch
+    return foe_comm_create(unique_id, nranks, rank, torch.cuda.current_device())
 
 
 def foe_comm_destroy(comm: Comm):
