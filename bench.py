@@ -201,7 +201,7 @@ def run_reference(args, cfg):
     return 0
 
 
-def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cfg, persistent=False):
+def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cfg, persistent=False, tiling=None):
     """Roofline of the dominant kernel (the prior stencil, ~90% of the step).
 
     achieved = ALGORITHMIC flops (4 N_f m^2 per pixel per evaluation) / the
@@ -243,11 +243,11 @@ def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cf
         nb = ((m * m // 8) * 8 + 15) // 16 * 16
         kf = ((m + 1) // 2) * 16                         # forward K: (m + 1) ring slots of 8 halves
         c = (m - 1) // 2
-        ow = 128 - 2 * c
-        R = 64
+        R, ow, mode = tiling if tiling else (64, 128 - 2 * c, 0)
+        rows = R if mode >= 1 else R + 2 * c          # response rows per tile (no row halos: R)
         # executed tensor flops per output pixel: 3 passes x 2 x (fwd Kf x NP + bwd NP x NB) per
-        # response pixel, x (R + 2C) 128-lane response rows per R x OW output tile
-        exec_px = 3 * 2 * (kf * np_ + np_ * nb) * (R + 2 * c) * 128 / (R * ow)
+        # response pixel, x `rows` 128-lane response rows per R x OW output tile (ipiano_state_tiling)
+        exec_px = 3 * 2 * (kf * np_ + np_ * nb) * rows * 128 / (R * ow)
         alg_px = 4.0 * nf * m * m
         ex = alg_tflops * exec_px / alg_px if alg_tflops else None
         if micro.get("fp32_tflops", -1) > 0:
@@ -259,7 +259,9 @@ def roofline_entry(stencil, alg_tflops, k_ms, k_launches, step_ms, args, dev, cf
                     peak_fp32_emulated=bf16 / 3.0,
                     frac_fp32_emulated=(3.0 * alg_tflops / bf16) if alg_tflops else None,
                     tensor_executed_tflops=ex, tensor_executed_frac=(ex / bf16) if ex else None,
-                    executed_per_algorithmic=exec_px / alg_px)
+                    executed_per_algorithmic=exec_px / alg_px,
+                    tiling={"tile_rows": R, "tile_cols": ow, "halo_mode": mode,
+                            "halo_modes": "0 row+column halos, 1 no row halos, 2 neither (DESIGN.md 5, K8)"})
     kname = ("k_ipiano_persistent (all trial rounds of a solve in one cooperative launch: K2 + K1 FFMA2 "
              "stencil + K3 per round; timed around ipiano_solve, so achieved covers the whole round)"
              if persistent else "k_prior_grad2 (K1: FFMA2 fused FoE energy+gradient stencil)")
@@ -466,6 +468,7 @@ def main():
     k1_flops = flops_per_eval_px * H * W * trials_per_step * args.steps
     k1_tflops = k1_flops / (k1_ms / 1e3) / 1e12 if k1_ms > 0 else None
     roofline = roofline_entry(P.ipiano_state_stencil(st), k1_tflops, k1_ms, k1_launches, step_ms, args, dev, cfg,
+                              tiling=P.ipiano_state_tiling(st),
                               persistent=persistent)
     roofline["kernel_timing"] = kernel_timing
     fp32_peak = roofline["fp32_peak"]
@@ -674,7 +677,8 @@ def run_slabs(args, cfg):
     flops_px = 4.0 * cfg.n_filters * cfg.m * cfg.m
     k1_flops = flops_px * (r1 - r0) * W * trials_per_step * args.steps
     k1_tflops = k1_flops / (k1_ms / 1e3) / 1e12 if k1_ms > 0 else None
-    roof = roofline_entry(P.ipiano_state_stencil(member), k1_tflops, k1_ms, k1_launches, step_ms, args, dev, cfg)
+    roof = roofline_entry(P.ipiano_state_stencil(member), k1_tflops, k1_ms, k1_launches, step_ms, args, dev, cfg,
+                          tiling=P.ipiano_state_tiling(member))
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,

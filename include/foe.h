@@ -254,6 +254,11 @@ foe_status ipiano_profile_read_k2(ipiano_state* st, double* k2_ms, long long* k2
 
 /* The stencil this state resolved to (FOE_STENCIL_FFMA or FOE_STENCIL_TENSOR). */
 int ipiano_state_stencil(const ipiano_state* st);
+/* The tensor-core stencil's tiling of a state (diagnostics, bench.py's executed-flops count):
+ * output rows and columns per tile (64 x 122 with halos; x 128 without column halos) and the halo
+ * mode -- 0 row and column halos, 1 no row halos, 2 neither (K8).  Zeros for
+ * an FFMA-stencil state.  FOE_ERR_INVALID_ARGUMENT for a NULL state or output. */
+foe_status ipiano_state_tiling(const ipiano_state* st, int* tile_rows, int* tile_cols, int* halo_mode);
 
 /* The trial-loop driver this state resolved to (FOE_SOLVER_GRAPH or FOE_SOLVER_PERSISTENT). */
 int ipiano_state_solver(const ipiano_state* st);

@@ -1258,6 +1258,14 @@ foe_status state_init(ipiano_state* st, const float* f, const double* lipschitz_
 extern "C" {
 
 int ipiano_state_stencil(const ipiano_state* st) { return st ? st->kind : -1; }
+foe_status ipiano_state_tiling(const ipiano_state* st, int* tile_rows, int* tile_cols, int* halo_mode) {
+    if (!st || !tile_rows || !tile_cols || !halo_mode) return fail(FOE_ERR_INVALID_ARGUMENT, "NULL state or output");
+    const bool tc = st->kind == FOE_STENCIL_TENSOR;
+    *tile_rows = tc ? st->tc_rows : 0;
+    *tile_cols = tc ? (st->tc_mode == 2 ? 128 : 128 - (st->model->m - 1)) : 0;
+    *halo_mode = tc ? st->tc_mode : 0;
+    return FOE_OK;
+}
 int ipiano_state_solver(const ipiano_state* st) { return st ? st->solver : -1; }
 
 void ipiano_state_destroy(ipiano_state* st) {

@@ -30,7 +30,7 @@ EXPORTED = (
     "foe_energy_grad", "foe_hvp", "foe_estimate_lipschitz", "ipiano_config_default",
     "ipiano_state_create", "ipiano_state_reset", "ipiano_step", "ipiano_solve", "ipiano_get_iterate",
     "ipiano_get_counters", "ipiano_get_trace", "ipiano_profile", "ipiano_profile_read", "ipiano_profile_read_k2",
-    "ipiano_state_destroy", "ipiano_state_stencil", "ipiano_state_solver", "ipiano_run",
+    "ipiano_state_destroy", "ipiano_state_stencil", "ipiano_state_tiling", "ipiano_state_solver", "ipiano_run",
     "foe_model_set_stencil", "foe_slab_exchange_plan", "foe_comm_unique_id", "foe_comm_create", "foe_comm_init", "foe_comm_destroy", "ipiano_slabs_create", "ipiano_slabs_reset",
     "ipiano_slabs_solve", "ipiano_slabs_advance", "ipiano_slabs_get_iterate", "ipiano_slabs_member", "ipiano_slabs_destroy",
     "ipiano_slabs_halo_handle", "ipiano_slabs_connect_peers", "ipiano_slabs_disconnect_peers",
@@ -96,6 +96,7 @@ def lib():
     L.ipiano_profile_read_k2.argtypes = [_vp, _dp, _llp]
     L.ipiano_state_stencil.argtypes = [_vp]
     L.ipiano_state_stencil.restype = C.c_int
+    L.ipiano_state_tiling.argtypes = [_vp, _ip, _ip, _ip]
     L.ipiano_state_solver.argtypes = [_vp]
     L.ipiano_state_solver.restype = C.c_int
     L.ipiano_state_destroy.argtypes = [_vp]
@@ -410,6 +411,13 @@ def ipiano_profile_read_k2(state: State):
     ms = C.c_double(); n = C.c_longlong()
     _check(lib().ipiano_profile_read_k2(state.handle, C.byref(ms), C.byref(n)))
     return ms.value, n.value
+
+
+def ipiano_state_tiling(state: State):
+    """(tile_rows, tile_cols, halo_mode) of the state's tensor-core stencil (zeros for FFMA)."""
+    r, c, m = C.c_int(), C.c_int(), C.c_int()
+    _check(lib().ipiano_state_tiling(state.handle, C.byref(r), C.byref(c), C.byref(m)))
+    return r.value, c.value, m.value
 
 
 def ipiano_state_stencil(state: State) -> int:
