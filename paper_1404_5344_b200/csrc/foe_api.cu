@@ -128,6 +128,11 @@ void k1_dispatch(int m, bool hvp, const K1Args& a, const TapParams& tp, const fo
 // path when the launch fills the GPU), or 32 / 16 for single images that cannot fill 148 SMs with
 // 64-row tiles (plan_stencil)
 constexpr int kTcR = 64;
+// 1: the Lipschitz estimate's HVPs after the first read S_i = rho''(K_i u)/2 stored by the first
+// (k_hvp_s); 0: every HVP recomputes it (A/B knob)
+#ifndef FOE_HVP_STORE_S
+#define FOE_HVP_STORE_S 1
+#endif
 // 1: the batch path's K8 tiles compute their own rows' responses only (no row halos; the partial
 // sums of the rows near band edges meet in K2); 0: tiles with row halos (A/B knob)
 #ifndef FOE_K8_NH
@@ -148,6 +153,8 @@ template <int M, int NP>
 cudaError_t tc_set_attr() {
     cudaError_t e = cudaFuncSetAttribute(foe::k_hvp_th<M, NP, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          foe::ThHGeom<M, NP, 64>::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(foe::k_hvp_s<M, NP, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, th_smem<M, NP, 64>());
     if (e != cudaSuccess) return e;
     const cudaError_t es[] = {th_attr<M, NP, 64, 0>(), th_attr<M, NP, 32, 0>(), th_attr<M, NP, 16, 0>(),
                               th_attr<M, NP, 8, 0>(),  th_attr<M, NP, 4, 0>(),  th_attr<M, NP, 64, 1>(),
@@ -212,6 +219,11 @@ struct foe_model {
     mutable ipiano_state* run_state = nullptr;
     mutable float* io_buf = nullptr;   // [2][n] device staging of host f and u
     mutable size_t io_n = 0;
+    // foe_estimate_lipschitz's S_i = rho''(K_i u)/2 buffer ([B][NP][H][W] fp32, grown on demand),
+    // guarded by s_mu (a concurrent estimate recomputes K u in every HVP instead)
+    mutable std::mutex s_mu;
+    mutable float* s_buf = nullptr;
+    mutable size_t s_n = 0;
 };
 
 struct ipiano_state {
@@ -431,7 +443,10 @@ foe_status foe_model_create(const float* filters, int n_filters, int m, const fl
             delete md->tp; delete md->tp2; delete md;
             return fail(FOE_ERR_CUDA, "cudaMemPoolCreate failed");
         }
-        uint64_t keep = 256ull << 20;
+        // the pool keeps up to 4 GiB mapped between calls (a c4 Lipschitz estimate's scratch is
+        // 0.4 GB: released and re-mapped on every call at a 256 MB threshold, tens of ms); the
+        // pool is private to the model and released with it
+        uint64_t keep = 4ull << 30;
         cudaMemPoolSetAttribute(md->pool, cudaMemPoolAttrReleaseThreshold, &keep);
         cudaGetLastError();
     }
@@ -493,6 +508,7 @@ void foe_model_destroy(foe_model* model) {
     if (!model) return;
     if (model->run_state) ipiano_state_destroy(model->run_state);
     if (model->io_buf) cudaFree(model->io_buf);
+    if (model->s_buf) cudaFree(model->s_buf);
     if (model->th_bimg) cudaFree(model->th_bimg);
     delete model->th_const;
     // outstanding stream-ordered frees are honoured: the pool is released once they land
@@ -696,7 +712,8 @@ bool is_device_ptr(const void* p) {
 foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int W, int groups,
                         double* epart, float* gparts, bool hvp, const double* v, const float* gw,
                         cudaStream_t s, int kind = FOE_STENCIL_FFMA, int tiles_x_tc = 0, int ntiles_tc = 0,
-                        int tc_rem = 0, int tc_spt = 0, int tc_rows = kTcR, int ncp = kNCP, int nchunks2 = 0) {
+                        int tc_rem = 0, int tc_spt = 0, int tc_rows = kTcR, int ncp = kNCP, int nchunks2 = 0,
+                        float* sbuf = nullptr, bool s_stored = false) {
     K1Args a{};
     a.w = w;
     a.w_slot_stride = 0;
@@ -744,6 +761,17 @@ foe_status run_k1_plain(const foe_model* md, const double* w, int B, int H, int 
         ta.tiles_x = ta.k.tiles_x;
         count_launch(1);
         const dim3 grid(ta.k.ntiles, B);
+        // sbuf (the Lipschitz estimate): the first HVP stores S_i = rho''(K_i u)/2 of every pixel,
+        // the later ones (same w) read it (k_hvp_s: one GEMM fewer, two CTAs per SM)
+        ta.k.sbuf = sbuf;
+        if (sbuf != nullptr && s_stored) {
+            if (md->tc_np == 48)
+                foe::k_hvp_s<7, 48, kTcR><<<grid, 256, th_smem<7, 48, kTcR>(), s>>>(ta, *md->th_const);
+            else
+                foe::k_hvp_s<5, 32, kTcR><<<grid, 256, th_smem<5, 32, kTcR>(), s>>>(ta, *md->th_const);
+            CKL("k_hvp_s");
+            return FOE_OK;
+        }
         if (md->tc_np == 48)
             foe::k_hvp_th<7, 48, kTcR><<<grid, 256, foe::ThHGeom<7, 48, kTcR>::SMEM_BYTES, s>>>(ta, *md->th_const);
         else
@@ -898,8 +926,27 @@ foe_status foe_estimate_lipschitz(const foe_model* md, const float* f, int B, in
     count_launch(1);
     CKL("power-iteration init");
     st = grad_direct(md, w0, B, H, W, gw, s);
+    // S_i = rho''(K_i u)/2 at w0 for the tensor-core HVPs after the first (k_hvp_s); without the
+    // memory for it every HVP recomputes K u
+    float* sbuf = nullptr;
+    std::unique_lock<std::mutex> slk(md->s_mu, std::try_to_lock);
+    if (md->tc_np && FOE_HVP_STORE_S && slk.owns_lock()) {
+        const size_t need = (size_t)md->tc_np * n;
+        if (md->s_n < need) {
+            if (md->s_buf) {
+                CK(cudaStreamSynchronize(s));   // (an earlier estimate's kernels may still read it)
+                cudaFree(md->s_buf);
+                md->s_buf = nullptr;
+                md->s_n = 0;
+            }
+            if (cudaMalloc((void**)&md->s_buf, sizeof(float) * need) == cudaSuccess) md->s_n = need;
+            else { cudaGetLastError(); md->s_buf = nullptr; }
+        }
+        sbuf = md->s_buf;
+    }
     for (int it = 0; it < power_iters && st == FOE_OK; ++it) {
-        st = run_k1_plain(md, w0, B, H, W, 1, epart, h, true, v, gw, s);   // h = Hess v
+        st = run_k1_plain(md, w0, B, H, W, 1, epart, h, true, v, gw, s, FOE_STENCIL_FFMA, 0, 0, 0, 0, kTcR, kNCP, 0,
+                          sbuf, it > 0);   // h = Hess v
         foe::k_dot3<<<dim3(nblk, B), kThreads, 0, s>>>(v, h, part, nblk, HW, kPxt2);
         count_launch(1);
         foe::k_reduce_rows<<<B, kThreads, 0, s>>>(part, nblk, 3, 3, sums);  // <v,h>, <h,h>

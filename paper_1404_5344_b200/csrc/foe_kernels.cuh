@@ -118,6 +118,7 @@ struct K1Args {
     float* gcorner;
     size_t gright_slot_stride, gcorner_slot_stride;
     // HVP only
+    float* sbuf;            // [B][NP][H][W] S_i = rho''(K_i u)/2 (k_hvp_th writes it when set, k_hvp_s reads)
     const double* v;        // [B][H][W]
     const float* gw;        // [B][H][W] gradient at w
 };

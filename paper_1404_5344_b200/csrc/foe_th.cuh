@@ -828,7 +828,7 @@ __device__ __forceinline__ void th_build_trow(const float* ts, int y, int l, flo
 template <int F0, int F1>
 __device__ __forceinline__ void th_hvp_epilogue(uint32_t t_d, uint32_t t_dt, uint32_t t_ph, uint32_t t_pl, float uq,
                                                 float inv, float it_s, const float* css, const float* kbl,
-                                                float& zlast) {
+                                                float& zlast, float* sout = nullptr, size_t plane = 0) {
     float r[(F1 - F0) * 8], tv[(F1 - F0) * 8];
 #pragma unroll
     for (int f8 = F0; f8 < F1; ++f8) {
@@ -851,7 +851,39 @@ __device__ __forceinline__ void th_hvp_epilogue(uint32_t t_d, uint32_t t_dt, uin
             const float2 omr = __ffma2_rn(make_float2(-rv.x, -rv.y), rv, one2);   // 1 - r^2
             const float q = rcp_approx(d.x * d.y);
             const float2 id = __fmul2_rn(make_float2(d.y, d.x), make_float2(q, q));   // 1 / d
-            const float2 pv = __fmul2_rn(__fmul2_rn(omr, t2), __fmul2_rn(id, id));
+            const float2 s2 = __fmul2_rn(omr, __fmul2_rn(id, id));   // rho''(r) / 2
+            const float2 pv = __fmul2_rn(s2, t2);
+            if (sout != nullptr) {   // (owned responses) S_i for the later HVPs at the same w (k_hvp_s)
+                sout[(size_t)i * plane] = s2.x;
+                sout[(size_t)(i + 1) * plane] = s2.y;
+            }
+            if (!FOE_K8_TAP49) zl2 = __ffma2_rn(pv, make_float2(kbl[i], kbl[i + 1]), zl2);
+            h2_split(pv, ph[e / 2], pl[e / 2]);
+        }
+        tc::tmem_st4u(t_ph + f8 * 4, ph);
+        tc::tmem_st4u(t_pl + f8 * 4, pl);
+    }
+    zlast = zl2.x + zl2.y;
+}
+
+// HVP epilogue from stored S (k_hvp_s): P = s_p S_i tv, tv = T / (s_t s_f) (it_s as above)
+template <int F0, int F1>
+__device__ __forceinline__ void th_hvps_epilogue(uint32_t t_dt, uint32_t t_ph, uint32_t t_pl, float it_s,
+                                                 const float* sv, const float* kbl, float& zlast) {
+    float tv[(F1 - F0) * 8];
+#pragma unroll
+    for (int f8 = F0; f8 < F1; ++f8) tc::tmem_ld8(t_dt + f8 * 8, *reinterpret_cast<float(*)[8]>(tv + (f8 - F0) * 8));
+    tc::wait_ld();
+    const float2 it2 = make_float2(it_s, it_s);
+    float2 zl2 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int f8 = F0; f8 < F1; ++f8) {
+        uint32_t ph[4], pl[4];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+            const int i = f8 * 8 + e, k = (f8 - F0) * 8 + e;
+            const float2 t2 = __fmul2_rn(make_float2(tv[k], tv[k + 1]), it2);
+            const float2 pv = __fmul2_rn(make_float2(sv[k], sv[k + 1]), t2);
             if (!FOE_K8_TAP49) zl2 = __ffma2_rn(pv, make_float2(kbl[i], kbl[i + 1]), zl2);
             h2_split(pv, ph[e / 2], pl[e / 2]);
         }
@@ -1037,12 +1069,17 @@ __global__ void __launch_bounds__(256, 1) k_hvp_th(const TcArgs ta, const __grid
             tc::mbar_wait(&mbar_f, (uint32_t)(j & 1));
             tc::fence_after_sync();
             float zl;
+            // (args.sbuf) S of this tile's owned responses, planes [b][i][H][W], for k_hvp_s
+            float* sout = nullptr;
+            if (args.sbuf != nullptr && j >= C && j < C + R && l >= C && l < C + G::OW && y0 - C + j < H &&
+                x0 - C + l < W)
+                sout = args.sbuf + (size_t)b * NP * HW + (size_t)(y0 - C + j) * W + (x0 - C + l);
             if (wg == 0)
                 th_hvp_epilogue<0, HF8>(tl + GH::COL_D, tl + GH::COL_DT, tl + GH::COL_PH, tl + GH::COL_PL, uq, inv,
-                                        inv_t, cc.sumk, cc.kbl, zl);
+                                        inv_t, cc.sumk, cc.kbl, zl, sout, HW);
             else
                 th_hvp_epilogue<HF8, NF8>(tl + GH::COL_D, tl + GH::COL_DT, tl + GH::COL_PH, tl + GH::COL_PL, uq, inv,
-                                          inv_t, cc.sumk, cc.kbl, zl);
+                                          inv_t, cc.sumk, cc.kbl, zl, sout, HW);
             if (!FOE_K8_TAP49) zls[(j & 1) * 2 * G::LZ + wg * G::LZ + l] = zl;
             tc::wait_st();
             tc::fence_before_sync();
@@ -1067,6 +1104,202 @@ __global__ void __launch_bounds__(256, 1) k_hvp_th(const TcArgs ta, const __grid
     tc::fence_before_sync();
     __syncthreads();
     if (warp == 0) tc::tmem_dealloc<GH::TCOLS>(tb);
+}
+
+// =============================================================================================
+// K8s: the later Hessian-vector products of one Lipschitz estimate (the same w, new v): S_i =
+// rho''(K_i u) / 2 is the same for all of them, so the first HVP (k_hvp_th with args.sbuf) stores it
+// for the owned responses ([B][NP][H][W] fp32) and this kernel runs only the T = K t GEMM, P = s_p
+// S T, the backward GEMM and the col2im -- one TMEM ring (224 columns: two CTAs per SM) and no u tile.
+//   Hv = v (.) grad F + u (.) sum_i theta_i K_i^T [S_i (.) K_i t],  t = u (.) v   (w domain)
+template <int M, int NP, int R>
+struct ThSGeom {
+    using G = ThGeom<M, NP, R>;
+    static constexpr int RINGC = 2 * G::RS * 4;
+    static constexpr int COL_TH = 0, COL_TL = RINGC, COL_DT = 2 * RINGC, COL_Z = COL_DT;
+    static constexpr int ND = NP > G::NBP ? NP : G::NBP;
+    static constexpr int COL_PH = COL_DT + ND, COL_PL = COL_PH + NP / 2;
+    static constexpr int TCOLS = 256;
+    static_assert(COL_PL + NP / 2 <= TCOLS, "TMEM budget: two CTAs per SM");
+};
+
+template <int M, int NP, int R>
+__global__ void __launch_bounds__(256, 2) k_hvp_s(const TcArgs ta, const __grid_constant__ ThConst cc) {
+    using G = ThGeom<M, NP, R>;
+    using GS = ThSGeom<M, NP, R>;
+    constexpr int C = G::C, L = G::LANES, RS = G::RS;
+    extern __shared__ __align__(128) unsigned char smb[];
+    float* ts = reinterpret_cast<float*>(smb + G::SM_U);   // the t tile in the u tile's place
+    float* zs = reinterpret_cast<float*>(smb + G::SM_Z) + 8 * G::ZP;
+    float* hand = reinterpret_cast<float*>(smb + G::SM_HAND);
+    float* zls = reinterpret_cast<float*>(smb + G::SM_ZL) + 8;
+    __shared__ uint32_t tbase_s;
+    __shared__ __align__(8) uint64_t mbar_f, mbar_b, mbar_bimg;
+    __shared__ float wmax[8];
+
+    const K1Args& args = ta.k;
+    const int b = blockIdx.y;
+    const int H = args.H, W = args.W;
+    const size_t HW = (size_t)H * W;
+    const int tile = blockIdx.x;
+    const double* w = args.w + (size_t)b * HW;
+    const double* vv = args.v + (size_t)b * HW;
+    const float* sb = args.sbuf + (size_t)b * NP * HW;
+    const int t = threadIdx.x, warp = __shfl_sync(0xffffffffu, t >> 5, 0);
+    const int wg = warp >> 2;
+    const int l = (warp & 3) * 32 + (t & 31);
+    const int ty = tile / ta.tiles_x, tx = tile - ty * ta.tiles_x;
+    const int y0 = ty * R, x0 = tx * G::OW;
+
+    if (warp == 0) tc::tmem_alloc<GS::TCOLS>(&tbase_s);
+    if (t == 0) {
+        tc::mbar_init(&mbar_f, 1);
+        tc::mbar_init(&mbar_b, 1);
+        tc::mbar_init(&mbar_bimg, 1);
+        tc::mbar_fence_init();
+        tc::bulk_g2s(smb + G::SM_B, ta.bimg, (uint32_t)G::B_BYTES, &mbar_bimg);
+    }
+    const bool udom = args.udom != 0;
+    th_stage_t<G::UY, G::UX, G::UP, 8>(ts, w, vv, H, W, y0, x0, 2 * C, udom, warp, t & 31);
+    for (int i = t; i < 16 * G::ZP; i += 256) {   // zero padding lanes (as K8)
+        const int ln = i / G::ZP;
+        zs[(ln < 8 ? ln - 8 : L + ln - 8) * G::ZP + (i - ln * G::ZP)] = 0.f;
+    }
+    if (t < 64) zls[(t >> 4) * G::LZ + ((t & 15) < 8 ? (t & 15) - 8 : L + (t & 15) - 8)] = 0.f;
+    tc::fence_before_sync();
+    __syncthreads();
+    float mt = 0.f;
+    for (int y = warp; y < G::UY; y += 8)
+        for (int x = t & 31; x < G::UX; x += 32) mt = fmaxf(mt, fabsf(ts[y * G::UP + x]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+    if ((t & 31) == 0) wmax[warp] = mt;
+    __syncthreads();
+    tc::fence_after_sync();
+    mt = wmax[0];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) mt = fmaxf(mt, wmax[k]);
+    auto scale_of = [](float m2) {
+        int e2 = ((int)((__float_as_uint(m2) >> 23) & 0xffu)) - 127;
+        e2 = max(e2, -47);
+        if (!(m2 < 3.0e38f)) e2 = 13;
+        return __uint_as_float((uint32_t)(127 + 13 - e2) << 23);
+    };
+    const float st = scale_of(mt), sp = scale_of(4.0f * mt * cc.kabs);   // (as k_hvp_th)
+    const float inv_t = cc.inv_sf / st * sp;
+    const float inv_zt = cc.inv_z * (kThPScale / sp);
+    const uint32_t tb = tbase_s;
+    const uint32_t tl = tb + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t t_th = tl + GS::COL_TH, t_tl = tl + GS::COL_TL;
+    {   // the ring's A2 slots stay zero (no DC shift of t)
+        const uint32_t z4[4] = {0u, 0u, 0u, 0u};
+        for (int c = wg * 4; c < GS::RINGC; c += 8) {
+            tc::tmem_st4u(t_th + c, z4);
+            tc::tmem_st4u(t_tl + c, z4);
+        }
+    }
+    tc::wait_st();
+#pragma unroll 1
+    for (int y = 0; y < M - 1; ++y) {
+        if (wg == 0) th_build_trow<M, G::UP, RS, 0>(ts, y, l, st, t_th, t_tl, y % RS);
+        else th_build_trow<M, G::UP, RS, 1>(ts, y, l, st, t_th, t_tl, y % RS);
+    }
+    tc::mbar_wait(&mbar_bimg, 0);
+    const uint32_t idf = tc::idesc_f16(128, NP);
+    const uint32_t idb = tc::idesc_f16(128, G::NBP);
+    const uint32_t b_base = tc::smem_u32(smb + G::SM_B);
+    const bool out_col = (l < G::OW) && (x0 + l < W);
+    const int xr = wrap_idx(x0 - C + l, W);   // this lane's response column
+
+    constexpr int NZ8 = G::NZ8, HZ8 = (NZ8 + 1) / 2;
+    constexpr int NF8 = NP / 8, HF8 = NF8 / 2;
+    constexpr int A0 = C + 1, A1 = M - A0;
+    float acc[A0 > A1 ? A0 : A1];
+#pragma unroll
+    for (int k = 0; k < (A0 > A1 ? A0 : A1); ++k) acc[k] = 0.f;
+    float* gout = args.g + (size_t)b * HW;
+
+#pragma unroll 1
+    for (int j = 0; j <= G::RR; ++j) {
+        const int ws = (j + RS - 1) % RS;
+        float sv[HF8 * 8];   // S of this response pixel and warp group's filters (loaded early)
+        if (j < G::RR) {
+            const float* sp_ = sb + (size_t)(wg * HF8 * 8) * HW + (size_t)wrap_idx(y0 - C + j, H) * W + xr;
+#pragma unroll
+            for (int k = 0; k < HF8 * 8; ++k) sv[k] = __ldg(sp_ + (size_t)k * HW);
+            const int yn = j + M - 1;
+            if (wg == 0) th_build_trow<M, G::UP, RS, 0>(ts, yn, l, st, t_th, t_tl, yn % RS);
+            else th_build_trow<M, G::UP, RS, 1>(ts, yn, l, st, t_th, t_tl, yn % RS);
+            tc::tmem_st2u(t_th + ws * 4 + wg * 2, 0u, 0u);
+            tc::tmem_st2u(t_tl + ws * 4 + wg * 2, 0u, 0u);
+        }
+        if (j > 0) {
+            tc::mbar_wait(&mbar_b, (uint32_t)((j - 1) & 1));
+            tc::fence_after_sync();
+            if (wg == 0) th_z_to_smem<G::ZP, 0, HZ8>(tl + GS::COL_Z, zs, l);
+            else th_z_to_smem<G::ZP, HZ8, NZ8>(tl + GS::COL_Z, zs, l);
+        }
+        tc::wait_st();
+        tc::fence_before_sync();
+        __syncthreads();
+        if (warp == 0 && j < G::RR) {
+            tc::fence_after_sync();
+#pragma unroll
+            for (int pass = 0; pass < 3; ++pass) {
+                const uint32_t boff = pass == 0 ? (uint32_t)G::BF_BYTES : 0u;
+#pragma unroll
+                for (int c = 0; c < G::NCH; ++c) {
+                    const uint64_t bd = tc::sdesc_kmajor(b_base + boff + c * 2 * NP * 16, NP * 16, 128);
+                    tc::mma_f16_ts_warp(tb + GS::COL_DT, tb + (pass == 1 ? GS::COL_TL : GS::COL_TH) + 4 * (ws + 2 * c),
+                                        bd, pass == 1 ? idf | kLoNeg : idf, (pass | c) != 0);
+                }
+            }
+            tc::mma_commit_warp(&mbar_f);
+        }
+        if (j > 0) {
+            const int jz = j - 1;
+            const float s_sum = th_col2im<M, G::NB, G::ZP, false, L, G::LZ>(zs, zls + (jz & 1) * 2 * G::LZ, hand, l, l, jz,
+                                                                            wg, acc);
+            const int o = jz - 2 * C;
+            if (wg == 1 && o >= 0 && o < R && out_col && y0 + o < H) {
+                const float s_tot = s_sum * inv_zt;
+                const size_t gi = (size_t)(y0 + o) * W + x0 + l;
+                float val;
+                if (udom) val = s_tot;
+                else val = (float)(vv[gi] * (double)args.gw[(size_t)b * HW + gi] + (double)((float)exp(w[gi]) * s_tot));
+                gout[gi] = val;
+            }
+        }
+        if (j < G::RR) {
+            tc::mbar_wait(&mbar_f, (uint32_t)(j & 1));
+            tc::fence_after_sync();
+            float zl;
+            if (wg == 0) th_hvps_epilogue<0, HF8>(tl + GS::COL_DT, tl + GS::COL_PH, tl + GS::COL_PL, inv_t, sv, cc.kbl, zl);
+            else th_hvps_epilogue<HF8, NF8>(tl + GS::COL_DT, tl + GS::COL_PH, tl + GS::COL_PL, inv_t, sv, cc.kbl, zl);
+            if (!FOE_K8_TAP49) zls[(j & 1) * 2 * G::LZ + wg * G::LZ + l] = zl;
+            tc::wait_st();
+            tc::fence_before_sync();
+            __syncthreads();
+            if (warp == 0) {
+                tc::fence_after_sync();
+#pragma unroll
+                for (int pass = 0; pass < 3; ++pass) {
+                    const uint32_t acol = pass == 1 ? GS::COL_PL : GS::COL_PH;
+                    const uint32_t boff = 2 * G::BF_BYTES + (pass == 0 ? (uint32_t)G::BB_BYTES : 0u);
+#pragma unroll
+                    for (int kc = 0; kc < G::NKB; ++kc) {
+                        const uint64_t bd = tc::sdesc_kmajor(b_base + boff + kc * 2 * G::NBP * 16, G::NBP * 16, 128);
+                        tc::mma_f16_ts_warp(tb + GS::COL_Z, tb + acol + kc * 8, bd, pass == 1 ? idb | kLoNeg : idb,
+                                            (pass | kc) != 0);
+                    }
+                }
+                tc::mma_commit_warp(&mbar_b);
+            }
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<GS::TCOLS>(tb);
 }
 
 }  // namespace foe

@@ -101,6 +101,21 @@ def test_lipschitz_estimate_same_power_of_two():
     assert L[0] == L_o
 
 
+def test_lipschitz_estimate_stored_S_batch_ragged():
+    """The 48 x 7x7 bank on two ragged images (150 x 260: halo responses read across the wrap from
+    the neighbour tiles' stored S_i = rho''(K_i u)/2, k_hvp_s): rho to 1e-4 and the same power of two
+    as the oracle for each image (R-10)."""
+    cfg = S.config("c4", B=2, H=150, W=260)
+    d = S.make_inputs(cfg)
+    v0 = S.lipschitz_start_vector(2, cfg.H, cfg.W)
+    md = _model(d["filters"], d["theta"])
+    rho, L = P.foe_estimate_lipschitz(md, _cuda(d["f"], torch.float32), _cuda(v0, torch.float64), 25)
+    for b in range(2):
+        rho_o, L_o = oracle.estimate_lipschitz(d["f"][b], d["filters"], d["theta"], v0[b], 25)
+        assert rho[b] == pytest.approx(rho_o, rel=1e-4), (b, rho[b], rho_o)
+        assert L[b] == L_o
+
+
 # ---------------------------------------------------------------------- iPiano steps
 
 def _setup(name, **over):
