@@ -32,6 +32,12 @@ constexpr int kThreads = 256;
 #ifndef FOE_K2_ETAB
 #define FOE_K2_ETAB 1     // K2 fast path: table-driven fp64 exponential (k2_etab in shared memory)
 #endif
+#ifndef FOE_K2_RCP1
+#define FOE_K2_RCP1 1     // K2 fast path: the fp64 Newton step's 1/phi' with one refinement step
+#endif
+#ifndef FOE_K2_ETAB_G
+#define FOE_K2_ETAB_G 1   // ... read from global memory through L1 (no per-CTA shared-memory copy)
+#endif
 #ifndef FOE_K2_PAIRS
 #define FOE_K2_PAIRS 1    // K2 by pixel pairs (inertial_prox_pairs) when HW % 4 == 0
 #endif
@@ -795,10 +801,17 @@ __device__ __forceinline__ void exp2a_pm_tab(double a, double& ep, double& em) {
     const double r = fma(-kd, 3.623510646634843e-19, fma(-kd, 1.0830424696249145e-02, x));   // x - kd ln2/64
     const int k = (int)kd, j = k & 63, m = k >> 6;
     const double r2 = r * r;
+#if FOE_K2_ETAB_G
+    // |r| <= ln2/128: the r^6/720 term of the even part is below 4e-17 (half an ulp of c ~ 1)
+    const double c = fma(r2, fma(r2, 1.0 / 24.0, 0.5), 1.0);
+    const double tp = __ldg(kK2Etab + j), tm = __ldg(kK2Etab + 64 + j);
+#else
     const double c = fma(r2, fma(r2, fma(r2, 1.0 / 720.0, 1.0 / 24.0), 0.5), 1.0);
-    const double s = r * fma(r2, fma(r2, 1.0 / 120.0, 1.0 / 6.0), 1.0);
     const double* t = k2_etab();
-    const double tp = t[j], tm = t[64 + j];                 // 2^{+-m} by the exponent field (|m| <= 127)
+    const double tp = t[j], tm = t[64 + j];
+#endif
+    const double s = r * fma(r2, fma(r2, 1.0 / 120.0, 1.0 / 6.0), 1.0);
+    // 2^{+-m} by the exponent field (|m| <= 127)
     ep = (c + s) * __hiloint2double(__double2hiint(tp) + (m << 20), __double2loint(tp));
     em = (c - s) * __hiloint2double(__double2hiint(tm) - (m << 20), __double2loint(tm));
 }
@@ -867,7 +880,15 @@ __device__ __forceinline__ bool prox_fast(double what, double f2, float ff, cons
     const double am = tau * l1 * f2 * Em0, bp = tau * l2 * Ep0;
     const double phi = (double)d + tau * (l1 - l2 * f2) - am + bp;
     const double dphi = 1.0 + 2.0 * (am + bp);
+#if FOE_K2_RCP1
+    // one Newton step on the MUFU seed (2^-22 -> ~2^-44 relative): st is accepted only when
+    // |st| <= 1e-6, so its relative error contributes < 1e-19 to z
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(dphi));
+    const double st = phi * fma(y, fma(-dphi, y, 1.0), y);
+#else
     const double st = phi * rcp_f64(dphi);
+#endif
     const double e = -2.0 * st;                                  // e^{+-e}, |e| <= 2e-6 when accepted
     z_out = z0 - st;
     ep_out = Ep0 * fma(0.5 * e, e, 1.0 + e);
@@ -1163,7 +1184,7 @@ __device__ __forceinline__ void l2_prefetch_range(const void* p, size_t n) {
 template <int PXT>
 __global__ void __launch_bounds__(kThreads, FOE_K2_CTAS)
 k_inertial_prox(const K2Args a) {
-#if FOE_K2_ETAB
+#if FOE_K2_ETAB && !FOE_K2_ETAB_G
     k2_etab_init();
     __syncthreads();
 #endif

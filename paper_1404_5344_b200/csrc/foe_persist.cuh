@@ -81,7 +81,7 @@ k_ipiano_persistent(const PersistArgs pa, const __grid_constant__ TapParams2 tp)
         long long* dst = reinterpret_cast<long long*>(my);
         for (int i = threadIdx.x; i < words; i += kThreads) dst[i] = src[i];
     }
-#if FOE_K2_ETAB
+#if FOE_K2_ETAB && !FOE_K2_ETAB_G
     k2_etab_init();   // the prox's exponential table (phase A)
 #endif
     __syncthreads();
