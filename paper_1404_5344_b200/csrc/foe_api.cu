@@ -922,7 +922,8 @@ foe_status foe_estimate_lipschitz(const foe_model* md, const float* f, int B, in
     count_launch(1);
     foe::k_reduce_rows<<<B, kThreads, 0, s>>>(part, nblk, 3, 3, sums);
     count_launch(1);
-    foe::k_normalize<double><<<eb, 256, 0, s>>>(v0, v, sums, 3, 2, HW, B);
+    const dim3 nb_grid((unsigned)div_up((long long)HW, 1024), B);   // ~4 pixels per thread
+    foe::k_normalize<double><<<nb_grid, 256, 0, s>>>(v0, v, sums, 3, 2, HW, B);
     count_launch(1);
     CKL("power-iteration init");
     st = grad_direct(md, w0, B, H, W, gw, s);
@@ -947,10 +948,11 @@ foe_status foe_estimate_lipschitz(const foe_model* md, const float* f, int B, in
     for (int it = 0; it < power_iters && st == FOE_OK; ++it) {
         st = run_k1_plain(md, w0, B, H, W, 1, epart, h, true, v, gw, s, FOE_STENCIL_FFMA, 0, 0, 0, 0, kTcR, kNCP, 0,
                           sbuf, it > 0);   // h = Hess v
-        foe::k_dot3<<<dim3(nblk, B), kThreads, 0, s>>>(v, h, part, nblk, HW, kPxt2);
+        // <h,h> every step, <v,h> (the Rayleigh quotient) at the last one
+        foe::k_dot3<<<dim3(nblk, B), kThreads, 0, s>>>(it + 1 < power_iters ? nullptr : v, h, part, nblk, HW, kPxt2);
         count_launch(1);
         foe::k_reduce_rows<<<B, kThreads, 0, s>>>(part, nblk, 3, 3, sums);  // <v,h>, <h,h>
-        foe::k_normalize<float><<<eb, 256, 0, s>>>(h, v, sums, 3, 1, HW, B);
+        foe::k_normalize<float><<<nb_grid, 256, 0, s>>>(h, v, sums, 3, 1, HW, B);
         count_launch(1);
         CKL("power iteration");
     }

@@ -1463,8 +1463,8 @@ k_dot3(const double* v, const float* h, double* part, int nblk, size_t HW, int p
         const size_t p = base + (size_t)k * kThreads + threadIdx.x;
         if (p >= HW) break;
         const size_t gi = (size_t)b * HW + p;
-        const double a = v[gi];
-        const double c = h ? (double)h[gi] : 0.0;
+        const double a = v ? v[gi] : 0.0;    // (v == nullptr: only <h,h>, the power iteration's
+        const double c = h ? (double)h[gi] : 0.0;   //  steps before the last)
         vh += a * c; hh += c * c; vv += a * a;
     }
     const double s0 = block_sum_d(vh, red), s1 = block_sum_d(hh, red), s2 = block_sum_d(vv, red);
@@ -1474,13 +1474,15 @@ k_dot3(const double* v, const float* h, double* part, int nblk, size_t HW, int p
     }
 }
 
-// v <- src / sqrt(norm2[b*K + k])
+// v <- src / sqrt(norm2[b*K + k]) (grid: x = chunks of image b = blockIdx.y; the norm once per thread)
 template <typename T>
 __global__ void k_normalize(const T* src, double* v, const double* sums, int K, int k, size_t HW, int B) {
-    const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= HW * B) return;
-    const int b = (int)(i / HW);
-    v[i] = (double)src[i] / sqrt(sums[(size_t)b * K + k]);
+    const int b = blockIdx.y;
+    const double nrm = sqrt(sums[(size_t)b * K + k]);
+    const T* sp = src + (size_t)b * HW;
+    double* vp = v + (size_t)b * HW;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < HW; i += (size_t)gridDim.x * blockDim.x)
+        vp[i] = (double)sp[i] / nrm;
 }
 
 __global__ void k_log_ftilde(const float* f, double* w, size_t n, int idiv) {

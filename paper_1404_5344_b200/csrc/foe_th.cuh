@@ -149,6 +149,11 @@ struct ThConst {
 #ifndef FOE_K8_NEGLO
 #define FOE_K8_NEGLO 1
 #endif
+// 1: k_hvp_s loads row j+1's S right after row j's epilogue (in flight under the backward MMA and
+// the next row's ring build); 0: at the start of row j
+#ifndef FOE_HVP_S_AHEAD
+#define FOE_HVP_S_AHEAD 1
+#endif
 #ifndef FOE_K8_ESKIP
 #define FOE_K8_ESKIP 1   // halo response rows: epilogue without the energy logarithms (c4: -1.4 %)
 #endif
@@ -1218,15 +1223,27 @@ __global__ void __launch_bounds__(256, 2) k_hvp_s(const TcArgs ta, const __grid_
 #pragma unroll
     for (int k = 0; k < (A0 > A1 ? A0 : A1); ++k) acc[k] = 0.f;
     float* gout = args.g + (size_t)b * HW;
+    // S of response row j for this lane and warp group's filters
+    auto load_s = [&](float* sv_, int jj) {
+        const float* sp_ = sb + (size_t)(wg * HF8 * 8) * HW + (size_t)wrap_idx(y0 - C + jj, H) * W + xr;
+#pragma unroll
+        for (int k = 0; k < HF8 * 8; ++k) sv_[k] = __ldg(sp_ + (size_t)k * HW);
+    };
+#if FOE_HVP_S_AHEAD
+    float sv[HF8 * 8];
+    load_s(sv, 0);
+#endif
 
 #pragma unroll 1
     for (int j = 0; j <= G::RR; ++j) {
         const int ws = (j + RS - 1) % RS;
+#if !FOE_HVP_S_AHEAD
         float sv[HF8 * 8];   // S of this response pixel and warp group's filters (loaded early)
+#endif
         if (j < G::RR) {
-            const float* sp_ = sb + (size_t)(wg * HF8 * 8) * HW + (size_t)wrap_idx(y0 - C + j, H) * W + xr;
-#pragma unroll
-            for (int k = 0; k < HF8 * 8; ++k) sv[k] = __ldg(sp_ + (size_t)k * HW);
+#if !FOE_HVP_S_AHEAD
+            load_s(sv, j);
+#endif
             const int yn = j + M - 1;
             if (wg == 0) th_build_trow<M, G::UP, RS, 0>(ts, yn, l, st, t_th, t_tl, yn % RS);
             else th_build_trow<M, G::UP, RS, 1>(ts, yn, l, st, t_th, t_tl, yn % RS);
@@ -1276,6 +1293,9 @@ __global__ void __launch_bounds__(256, 2) k_hvp_s(const TcArgs ta, const __grid_
             float zl;
             if (wg == 0) th_hvps_epilogue<0, HF8>(tl + GS::COL_DT, tl + GS::COL_PH, tl + GS::COL_PL, inv_t, sv, cc.kbl, zl);
             else th_hvps_epilogue<HF8, NF8>(tl + GS::COL_DT, tl + GS::COL_PH, tl + GS::COL_PL, inv_t, sv, cc.kbl, zl);
+#if FOE_HVP_S_AHEAD
+            if (j + 1 < G::RR) load_s(sv, j + 1);   // the next row's S, in flight during this row's tail
+#endif
             if (!FOE_K8_TAP49) zls[(j & 1) * 2 * G::LZ + wg * G::LZ + l] = zl;
             tc::wait_st();
             tc::fence_before_sync();
