@@ -1,6 +1,7 @@
 """The Fig. 2 data-term protocol (paper_1404_5344_b200/fig2.py) on the GPU, with
 each model's chosen run redone by the fp64 oracle: the three models (8), (6) and (10) on a seeded
-512^2 image with L = 8 speckle, lambda per model by the best PSNR on a small grid.  Per model: GPU
+image with L = 8 speckle, lambda per model by the best PSNR on a small grid (256^2 here so the
+oracle's three 300-iteration runs take under a minute; `bench.py --protocol fig2` runs 512^2).  Per model: GPU
 vs oracle final image relative L2 <= 1e-4 and |dPSNR| <= 0.01 dB (the P3 bars); PSNR/SSIM of the
 library's kernels against the oracle's metrics to 1e-6 / 1e-5.  The table goes to $FIG2_OUT if set
 (profiles/r02_fig2.json is such a run).  The paper's ordering (10) > (8) > (6) is NOT asserted:
@@ -28,8 +29,9 @@ def rel_l2(a, b):
 def test_fig2_protocol_against_oracle():
     if not torch.cuda.is_available():
         pytest.fail("CUDA device required for -m gpu tests")
-    res = fig2.run(iters=300)
-    clean, f, k, th = fig2.inputs()
+    H = W = int(os.environ.get("FIG2_SIZE", "256"))
+    res = fig2.run(iters=300, H=H, W=W)
+    clean, f, k, th = fig2.inputs(H, W)
     table = {"image": res["image"], "noisy": {"psnr": res["noisy"][0], "ssim": res["noisy"][1]}, "models": {}}
     assert res["noisy"][0] == pytest.approx(OM.psnr(f, clean), abs=1e-6)
     for name, m in res["models"].items():
